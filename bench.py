@@ -1,0 +1,387 @@
+#!/usr/bin/env python
+"""Benchmark of the batched FSSCS-RM polar decoder (BASELINE.json metric).
+
+Workload (default C2, BASELINE.json configs[1]): PC(1024,512), Bhattacharyya
+construction at 2 dB, no CRC, D=32, L=8; 100,000 frames at each Eb/N0 in
+{1.0,1.5,2.0,2.5,3.0} dB = 500,000 frames per step per GPU.  LLRs come from the
+library's seeded device generator (Philox + BPSK/AWGN), resident in HBM before
+the timed region; the 2 GB LLR buffer exceeds the 126 MB L2, so no flush.
+
+A step = one polar_scs_decode call over the whole batch (stack decode incl.
+LLR staging, node decisions, CRC and output).  value = info-bit Mbps over
+all GPUs = frames * K / time (K = 512 information bits per frame).
+
+  python bench.py [--gpus N --steps K --warmup W] [--config C2] [--impl reference]
+  torchrun --nproc-per-node N bench.py --gpus N ...  (weak scaling: each rank
+  decodes its own frame range, no data-path collective)
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import inputgen as ig  # noqa: E402
+
+METRIC = "info-bit Mbps (decoded frames/s) for PC(1024,512) SCS D=32 on 1 B200 vs roofline"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--frames", type=int, default=0, help="override frames per Eb/N0 point")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--snap-global", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def workload_name(cfg, c):
+    crc = {0: "no CRC", 0x11021: "CRC-16 0x1021", 0x107: "CRC-8 0x07"}[c["crc_poly"]]
+    return (f"{cfg}: PC({c['N']},{c['K']}) Bhattacharyya@{c['design_db']}dB, {crc}, D={c['D']}, L={c['L']}, "
+            f"{c['frames']} frames x Eb/N0 {c['ebno']} dB, BPSK-AWGN float32 LLRs, seed {c['seed']}")
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            try:
+                sm.append(float(r[0]))
+                mx = max(mx, float(r[1]))
+                for nm, v in zip(names, r[4:8]):
+                    if v.lower() == "active":
+                        reasons.add(nm)
+            except (ValueError, IndexError):
+                continue
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ CPU oracle leg
+def oracle_sample(cfg, c, seconds, rank=0):
+    """Time the oracle (as it stands) on host cores over a bounded sample of the
+    workload: the same synthetic frames (inputgen draws, oracle-side encoding)."""
+    import oracle as O
+    threads = os.cpu_count() or 1
+    fr = O.bhattacharyya_mask(c["N"], c["K"], c["design_db"])
+    dec = O.SCSDecoder(fr, c["D"], c["L"], c["crc_poly"])
+    cc = O.crc_degree(c["crc_poly"]) if c["crc_poly"] else 0
+    # calibrate on a small prefix, then size the sample for ~`seconds` of work
+    per_point = max(threads, 64)
+    total_frames, total_t = 0, 0.0
+    rounds = 0
+    while True:
+        nf = per_point
+        pay = ig.payload_bits(c["seed"], 0, nf, c["K"] - cc)
+        nz = ig.unit_normals(c["seed"], 0, nf, c["N"])
+        cw = O.encode_systematic(fr, O.crc_attach(pay, c["crc_poly"]))
+        llrs = [O.awgn_llr(cw, nz, eb, c["K"] / c["N"]) for eb in c["ebno"]]
+        t0 = time.perf_counter()
+        for l in llrs:
+            dec.decode(l, threads=threads)
+        dt = time.perf_counter() - t0
+        rounds += 1
+        if dt > 0.2 * seconds or rounds >= 6:
+            total_frames, total_t = nf * len(c["ebno"]), dt
+            if dt < 0.8 * seconds and rounds < 6:
+                per_point = int(per_point * max(1.5, 0.9 * seconds / max(dt, 1e-3)))
+                continue
+            break
+        per_point = int(per_point * min(8.0, max(2.0, 0.5 * seconds / max(dt, 1e-3))))
+    fps = total_frames / total_t
+    return {
+        "value": fps * c["K"] / 1e6, "unit": "Mbps", "cores": threads, "kind": "oracle",
+        "frames_per_s": fps, "seconds": total_t,
+        "sample": f"{total_frames // len(c['ebno'])} frames (ids 0..) at each of {len(c['ebno'])} Eb/N0 points "
+                  f"of {cfg}, same draws as the GPU workload recipe, {threads} threads, decode only",
+    }
+
+
+def run_reference(args, cfg, c):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    # each timed "step" is a bounded sample; the whole run stays within minutes
+    per_step_s = max(2.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
+    for _ in range(args.warmup):
+        oracle_sample(cfg, c, per_step_s / 4)
+    vals = [oracle_sample(cfg, c, per_step_s) for _ in range(args.steps)]
+    fps = statistics.median(v["frames_per_s"] for v in vals)
+    value = fps * c["K"] / 1e6
+    cb = dict(vals[0])
+    cb["value"] = value
+    out = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "Mbps", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.median(v["seconds"] for v in vals),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": workload_name(cfg, c), "note": "CPU oracle (oracle/oracle.c) on host cores"},
+        "cpu_baseline": cb,
+        "e2e": {"value": value, "unit": "Mbps", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "frames_per_s": fps,
+    }
+    print(json.dumps(out), flush=True)
+
+
+# ------------------------------------------------------------------ our arm
+def run_ours(args, cfg, c):
+    import torch
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    import paper_1809_03606_b200 as P
+
+    nf = args.frames or c["frames"]
+    npts = len(c["ebno"])
+    frames = nf * npts
+    fr = P.bhattacharyya_mask(c["N"], c["K"], c["design_db"])
+    dec = P.PolarSCS(fr, c["D"], c["L"], c["crc_poly"], snap_global=args.snap_global)
+    K, N = c["K"], c["N"]
+
+    # inputs: device generator, each rank its own frame range; all points share
+    # the draws (common random numbers)
+    first = rank * nf
+    llr = torch.empty((frames, N), dtype=torch.float32, device="cuda")
+    blocks = None
+    tg0 = time.perf_counter()
+    for p, eb in enumerate(c["ebno"]):
+        blk, _ = dec.generate(c["seed"], eb, first, nf, want_block=(p == 0), llr_out=llr[p * nf:(p + 1) * nf])
+        if p == 0:
+            blocks = blk
+    torch.cuda.synchronize()
+    gen_s = time.perf_counter() - tg0
+    out = torch.empty((frames, K), dtype=torch.uint8, device="cuda")
+
+    stream = torch.cuda.current_stream()
+
+    def step():
+        dec.decode(llr, out=out, stream=stream)
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    barrier()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    per_launch = []
+    with ClockSampler(local) as clk:
+        barrier()
+        ev0.record(stream)
+        for _ in range(args.steps):
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            step()
+            b.record(stream)
+            per_launch.append((a, b))
+        ev1.record(stream)
+        barrier()
+    t_ms = ev0.elapsed_time(ev1)
+    launch_ms = [a.elapsed_time(b) for a, b in per_launch]
+    if dist is not None:
+        tt = torch.tensor([t_ms], device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_ms = float(tt.item())
+    ms_per_step = t_ms / args.steps
+    fps_rank = frames / (ms_per_step / 1e3)
+    value = world * frames * K / (ms_per_step / 1e3) / 1e6
+
+    # quality (outside the timed region): FER per Eb/N0 point and search stats
+    stats = dec.decode_stats(llr)
+    torch.cuda.synchronize()
+    fer = []
+    for p in range(npts):
+        errs = (stats["bits"][p * nf:(p + 1) * nf] != blocks).any(1).float().mean().item()
+        fer.append(errs)
+    pops_mean = [float(stats["pops"][p * nf:(p + 1) * nf].float().mean().item()) for p in range(npts)]
+    sw_mean = [float(stats["switches"][p * nf:(p + 1) * nf].float().mean().item()) for p in range(npts)]
+    assert torch.equal(stats["bits"], out), "decode and decode_stats disagree"
+
+    # e2e through the public host-buffer API (H2D + decode + D2H in the timed region)
+    e2e = None
+    if not args.no_e2e:
+        host_llr = torch.empty((frames, N), dtype=torch.float32, pin_memory=True)
+        host_llr.copy_(llr)
+        host_out = torch.empty((frames, K), dtype=torch.uint8, pin_memory=True)
+        dec.decode_host(host_llr, host_out)          # warm-up (allocates staging once)
+        reps = max(1, min(3, args.steps))
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            dec.decode_host(host_llr, host_out)
+        barrier()
+        e2e_s = (time.perf_counter() - t0) / reps
+        if dist is not None:
+            tt = torch.tensor([e2e_s], device="cuda")
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            e2e_s = float(tt.item())
+        assert torch.equal(host_out, out.cpu()), "host-path decode differs"
+        e2e = {"value": world * frames * K / e2e_s / 1e6, "unit": "Mbps",
+               "h2d_bytes_per_step": frames * N * 4, "d2h_bytes_per_step": frames * K,
+               "ms_per_step": e2e_s * 1e3}
+        del host_llr, host_out
+
+    peaks = {}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            peaks = json.load(fh)
+    except OSError:
+        pass
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+    kern_s = statistics.median(launch_ms) / 1e3
+    alg_bytes = frames * (4 * N + K)
+    achieved_gbs = alg_bytes / kern_s / 1e9
+    roofline_hbm = {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm_peak, "unit": "GB/s",
+                    "frac": achieved_gbs / hbm_peak, "traffic": None,
+                    "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6.65 TB/s"}
+    # ALU roofline: algorithmic lane-ops per frame counted by the oracle (O10) on
+    # a sample of the same workload, scaled to the batch; peak = 148 SMs x 128
+    # FP32/INT lanes x max SM clock
+    roofline = roofline_hbm
+    cpu = None
+    if rank == 0:
+        try:
+            ops_per_frame = oracle_ops_per_frame(c, npts)
+            alu_peak = 148 * 128 * sm_max * 1e6 / 1e12       # Tops/s
+            achieved_alu = ops_per_frame * frames / kern_s / 1e12
+            roofline_alu = {"bound": "alu", "achieved": achieved_alu, "peak": alu_peak, "unit": "Tops/s",
+                            "frac": achieved_alu / alu_peak, "traffic": None,
+                            "ops_per_frame": ops_per_frame,
+                            "peak_source": "148 SM x 128 lanes x sm_max_mhz (MEASURED_PEAKS.json)"}
+            roofline = roofline_alu if roofline_alu["frac"] > roofline_hbm["frac"] else roofline_hbm
+            roofline_other = roofline_hbm if roofline is roofline_alu else roofline_alu
+        except Exception as e:  # noqa: BLE001
+            roofline_other = {"error": str(e)}
+        if not args.no_cpu:
+            cpu = oracle_sample(cfg, c, args.cpu_seconds)
+    clocks = clk.summary()
+    info = dec.info
+    res = {
+        "metric": METRIC, "value": value, "unit": "Mbps", "n_gpus": world, "steps": args.steps,
+        "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded device generator: Philox payload, "
+        "systematic polar encoding, BPSK-AWGN LLRs)",
+        "config": {"workload": workload_name(cfg, c), "frames_per_step_per_gpu": frames,
+                   "l2": f"inputs {frames * N * 4 / 1e9:.2f} GB per step > 126 MB L2 (no flush needed)",
+                   "launch": {"ctas": info["ctas"], "warps_per_cta": info["warps_per_cta"],
+                              "smem_per_cta": info["smem_per_cta"], "snap_in_smem": info["snap_in_smem"]}},
+        "frames_per_s": world * frames / (ms_per_step / 1e3),
+        "frames_per_s_per_gpu": fps_rank,
+        "roofline": roofline,
+        "e2e": e2e, "gpu_launches": args.steps, "clocks": clocks,
+        "kernel_ms_median": statistics.median(launch_ms),
+        "fer": dict(zip([str(e) for e in c["ebno"]], fer)),
+        "pops_mean": dict(zip([str(e) for e in c["ebno"]], pops_mean)),
+        "switches_mean": dict(zip([str(e) for e in c["ebno"]], sw_mean)),
+        "gen_s": gen_s,
+    }
+    if rank == 0:
+        res["roofline_other"] = roofline_other
+        res["cpu_baseline"] = cpu
+        print(json.dumps(res), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def oracle_ops_per_frame(c, npts, n_sample=64):
+    """Algorithmic lane-ops per frame (mean over a sample at every Eb/N0 point):
+    f/g evaluations (clean pass + spines) + node elements + BETA XOR bits +
+    stack key compares (D per pop and per candidate insert)."""
+    import oracle as O
+    fr = O.bhattacharyya_mask(c["N"], c["K"], c["design_db"])
+    dec = O.SCSDecoder(fr, c["D"], c["L"], c["crc_poly"])
+    cc = O.crc_degree(c["crc_poly"]) if c["crc_poly"] else 0
+    pay = ig.payload_bits(c["seed"], 0, n_sample, c["K"] - cc)
+    nz = ig.unit_normals(c["seed"], 0, n_sample, c["N"])
+    cw = O.encode_systematic(fr, O.crc_attach(pay, c["crc_poly"]))
+    tot = 0
+    for eb in c["ebno"]:
+        r = dec.decode(O.awgn_llr(cw, nz, eb, c["K"] / c["N"]), counters=True, threads=os.cpu_count() or 1)
+        ct = r["counters"]
+        tot += (ct["f_ops"] + ct["g_ops"] + ct["node_elems"] + ct["beta_xor_bits"]
+                + c["D"] * (ct["pops"] + ct["cand_created"]))
+    return tot / (n_sample * npts)
+
+
+def main():
+    args = parse()
+    cfg = args.config
+    c = dict(ig.CONFIGS[cfg])
+    if args.frames:
+        c["frames"] = args.frames
+    if args.impl == "reference":
+        run_reference(args, cfg, c)
+    else:
+        run_ours(args, cfg, c)
+
+
+if __name__ == "__main__":
+    main()

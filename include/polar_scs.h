@@ -1,0 +1,180 @@
+/*
+ * polar_scs.h — C ABI of the B200-native batched fast-simplified successive
+ * cancellation stack (FSSCS-RM) polar decoder.
+ *
+ * Method: H. Aurora, W. Gross, "Towards Practical Software Stack Decoding of
+ * Polar Codes", arXiv:1809.03606.  Citations below are
+ * PAPER.md:L<line> (section / equation / algorithm / figure).  Where the paper
+ * is silent or garbled the reading adopted is listed in DESIGN.md §Readings
+ * (R1..R19); the same readings define the CPU oracle the tests compare with.
+ *
+ * Conventions (all entry points):
+ *   - Return value: POLAR_OK (0) or a negative POLAR_E* code; no exception or
+ *     abort crosses the ABI.  polar_scs_strerror() names the code.
+ *   - "device" pointers are CUDA device (or managed) memory on the handle's
+ *     device; "host" pointers are CPU memory (pinned for full copy speed).
+ *     The caller owns every I/O buffer; the handle owns its tables and
+ *     workspace, all allocated in polar_scs_create (decode calls allocate
+ *     nothing, except the host-staging buffers of polar_scs_decode_host,
+ *     allocated once on first use).
+ *   - Layouts are row-major per frame: llr [n_frames][N] float32, bits and
+ *     codewords [n_frames][K] / [n_frames][N] uint8 holding 0/1.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default
+ *     stream).  Device-pointer calls are asynchronous: results are valid once
+ *     the stream is synchronised.  A handle serves ONE in-flight call at a
+ *     time (its frame queue and snapshot arena are per handle).
+ *   - n_frames == 0 is a no-op returning POLAR_OK.
+ *   - Input contract: LLRs are finite (NaN/Inf is undefined behaviour).
+ */
+#ifndef POLAR_SCS_H
+#define POLAR_SCS_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define POLAR_OK        0
+#define POLAR_EINVAL   (-1)   /* bad argument (sizes, mask weight, NULL pointer) */
+#define POLAR_ENOMEM   (-2)   /* device or host allocation failed                */
+#define POLAR_ECUDA    (-3)   /* a CUDA runtime call or kernel launch failed     */
+#define POLAR_ENOTSYS  (-4)   /* unsupported for this code (e.g. not systematic) */
+
+/* create() flags */
+#define POLAR_FLAG_BIT_LEVEL    0x1u  /* leaf-only schedule: bit-level SCS-RM
+                                          */
+#define POLAR_FLAG_SNAP_GLOBAL  0x2u  /* force the path-snapshot arena into
+                                         global memory (L2) instead of shared */
+
+typedef struct polar_scs_s *polar_scs_t;
+
+/* Read-only description of a handle (for benches and tests). */
+typedef struct {
+    int32_t N, n, K, crc_bits, D, L;
+    int32_t num_ops;          /* FSSC schedule length |S|        */
+    int32_t num_nodes;        /* M = decision nodes in the schedule               */
+    int32_t warps_per_cta, ctas, smem_per_cta;  /* decode launch configuration   */
+    int32_t snap_in_smem;     /* 1: path snapshots in shared memory, 0: global    */
+    int32_t systematic_ok;    /* 1 if the mask is systematic-encodable            */
+    uint32_t flags;
+} polar_scs_info_t;
+
+/*
+ * Bhattacharyya-parameter code construction (host only, no device work).
+ * z0 = exp(-(K/N) 10^(EbN0/10)); the bits of index i, MSB first, map
+ * 1 -> z^2 and 0 -> 2z - z^2 (BEC bound), in the log domain; the K indices
+ * of smallest z carry information (ties: higher index).
+ * (information set A); reading R16.
+ *   N: power of two in [1, 65536]; 0 <= K <= N; frozen_mask: host [N],
+ *   written 1 = frozen, 0 = information.  Returns POLAR_EINVAL on bad sizes.
+ */
+int polar_construct_bhattacharyya(int32_t N, int32_t K, double design_ebno_db, uint8_t *frozen_mask);
+
+/*
+ * Create a decoder for PC(N, K) with a stack of depth D and
+ * per-length visit limit L and an optional CRC selecting
+ * among complete paths.  Compiles the FSSC schedule
+ * (Fig. 5; node precedence R0 > R1 > REP > SPC, reading R5),
+ * uploads it with the information-set and CRC tables, and sizes the
+ * persistent decode launch and its workspace.  Host only + cudaMalloc/copies.
+ *   N: power of two in [2, 4096]; K = number of information bits INCLUDING
+ *   the crc bits (reading R14), 1 <= K <= N; frozen_mask: host [N], 1 =
+ *   frozen, must have exactly N-K ones; D in [1, 128]; L >= 1 (values above
+ *   65535 are clamped: they never prune); crc_poly: 0 = none, else the full
+ *   generator including the x^c term (0x11021 = CRC-16 0x1021, 0x107 = CRC-8
+ *   0x07), degree c in [1, 31] and c < K; flags: POLAR_FLAG_*.
+ *   On success *out receives the handle (owned by the caller; release with
+ *   polar_scs_destroy).  Errors: POLAR_EINVAL, POLAR_ENOMEM, POLAR_ECUDA.
+ */
+int polar_scs_create(polar_scs_t *out, int32_t N, int32_t K, const uint8_t *frozen_mask,
+                     int32_t stack_depth_D, int32_t visit_limit_L, uint32_t crc_poly);
+int polar_scs_create_ex(polar_scs_t *out, int32_t N, int32_t K, const uint8_t *frozen_mask,
+                        int32_t stack_depth_D, int32_t visit_limit_L, uint32_t crc_poly,
+                        uint32_t flags);
+
+void polar_scs_destroy(polar_scs_t h);                 /* NULL is a no-op */
+int  polar_scs_get_info(polar_scs_t h, polar_scs_info_t *out);
+const char *polar_scs_strerror(int status);
+
+/*
+ * Decode n_frames independent frames with the FSSCS-RM stack decoder
+ * (PAPER.md:L589-599 SCS; L797-799 reduced memory; L815-842 Alg. 4 alpha
+ * recompute on a path switch; L846-854 fast-simplified nodes, schedule
+ * progress and flat beta).  One warp per frame, persistent kernel with a
+ * frame queue.
+ *   llr: device [n_frames][N] float32 channel LLRs (positive favours 0),
+ *   rows 16-byte aligned when N >= 4.
+ *   out_bits: device [n_frames][K] uint8 — the decoded K-bit block (payload ||
+ *   CRC), read from the systematic codeword estimate x_hat at the ascending
+ *   information indices (reading R15).
+ * polar_scs_decode_stats additionally writes, per frame (any may be NULL):
+ *   pm: final path metric (float32, PAPER.md:L511-517 Eq. PMupd summed over
+ *   nodes), pops: stack pops (selections), switches: path switches (pops of
+ *   a path other than the one just extended), status: 0 = a complete path
+ *   passed the CRC (or no CRC), 1 = every complete path failed the CRC and
+ *   the first complete path popped is returned (reading R13).
+ */
+int polar_scs_decode(polar_scs_t h, const float *llr, int64_t n_frames, uint8_t *out_bits,
+                     void *stream);
+int polar_scs_decode_stats(polar_scs_t h, const float *llr, int64_t n_frames, uint8_t *out_bits,
+                           float *pm, uint32_t *pops, uint32_t *switches, uint8_t *status,
+                           void *stream);
+
+/*
+ * End-to-end decode from HOST buffers: copies llr_host ([n][N] float32) to the
+ * device in chunks, decodes, and copies the bits back to out_bits_host
+ * ([n][K] uint8), overlapping the copies of one chunk with the decode of the
+ * other on three internal streams (H2D, decode, D2H).  Blocking: returns when out_bits_host is
+ * complete.  Pinned host memory gives full PCIe/C2C speed.  `stream` orders
+ * the call after prior work on it.
+ */
+int polar_scs_decode_host(polar_scs_t h, const float *llr_host, int64_t n_frames,
+                          uint8_t *out_bits_host, void *stream);
+
+/*
+ * CRC attach: block = payload || crc(payload), CRC computed MSB first with zero
+ * init, no reflection, no output XOR.
+ *   payload: device [n][K-c] uint8; block: device [n][K] uint8.
+ *   Without a CRC the payload is copied.
+ */
+int polar_crc_attach_batch(polar_scs_t h, const uint8_t *payload, int64_t n_frames,
+                           uint8_t *block, void *stream);
+
+/*
+ * Systematic encoding (PAPER.md:L30-36 c = u F^{(x)n}; L503, L854): u[A] =
+ * block, u[A^c] = 0, x = u F^{(x)n}, zero x on A^c, codeword = x F^{(x)n};
+ * then codeword restricted to A (ascending) equals block.
+ *   block: device [n][K] uint8; codeword: device [n][N] uint8.
+ *   POLAR_ENOTSYS if the mask is not systematic-encodable.
+ */
+int polar_encode_batch(polar_scs_t h, const uint8_t *block, int64_t n_frames,
+                       uint8_t *codeword, void *stream);
+
+/*
+ * BPSK over AWGN with caller-supplied unit normals (formula
+ * SURVEY §8(c) O4): sigma^2 = 1/(2 (K/N) 10^(EbN0/10)), sigma_f = (float)sigma,
+ * scale_f = (float)(2/sigma^2) computed in double on the host, then per bit
+ * llr = scale_f * ((1 - 2 x) + sigma_f * noise), two float32 roundings, no FMA.
+ *   codeword: device [n][N] uint8; noise: device [n][N] float32; llr: device
+ *   [n][N] float32.
+ */
+int polar_modulate_batch(polar_scs_t h, const uint8_t *codeword, const float *noise,
+                         int64_t n_frames, double ebno_db, float *llr, void *stream);
+
+/*
+ * Seeded device-side workload generator (one fused kernel): Philox4x32-10
+ * payload bits (stream 0) -> CRC attach -> systematic encode -> Philox unit
+ * normals (stream 1, Box-Muller in double) -> BPSK/AWGN LLRs as in
+ * polar_modulate_batch.  Counter layout: DESIGN.md §Input recipe; frame f of
+ * the batch is global frame first_frame + f, so any frame range is
+ * reproducible independently.
+ *   block: device [n][K] uint8 (may be NULL); llr: device [n][N] float32.
+ */
+int polar_generate_batch(polar_scs_t h, uint64_t seed, double ebno_db, int64_t first_frame,
+                         int64_t n_frames, uint8_t *block, float *llr, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* POLAR_SCS_H */

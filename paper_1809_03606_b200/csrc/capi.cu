@@ -1,0 +1,302 @@
+// capi.cu — the extern "C" boundary of libpolarscs (include/polar_scs.h):
+// argument validation, handle lifetime, launch configuration and the
+// host-buffer pipeline.  Every computation runs in the kernels of decode.cu
+// and codec.cu; this file only moves pointers, sizes and tables.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <new>
+
+#include "internal.h"
+
+namespace polar {
+cudaError_t launch_decode(const DecodeParams &p, int slots, bool snap_smem, int ctas, int smem, cudaStream_t st);
+cudaError_t decode_occupancy(int slots, bool snap_smem, int smem, int *blocks_per_sm);
+cudaError_t launch_crc_attach(const CodecParams &p, cudaStream_t st);
+cudaError_t launch_encode(const CodecParams &p, cudaStream_t st);
+cudaError_t launch_modulate(const CodecParams &p, cudaStream_t st);
+cudaError_t launch_generate(const CodecParams &p, cudaStream_t st);
+}  // namespace polar
+
+using namespace polar;
+
+namespace {
+
+template <class T>
+cudaError_t upload(T **dst, const std::vector<T> &src) {
+    const size_t bytes = std::max<size_t>(1, src.size()) * sizeof(T);
+    cudaError_t e = cudaMalloc(reinterpret_cast<void **>(dst), bytes);
+    if (e != cudaSuccess) return e;
+    if (!src.empty()) e = cudaMemcpy(*dst, src.data(), src.size() * sizeof(T), cudaMemcpyHostToDevice);
+    return e;
+}
+
+int slots_for(int D) { return D <= 32 ? 1 : (D <= 64 ? 2 : 4); }
+int round4(int w) { return (w + 3) & ~3; }
+
+void free_handle(polar_scs_t h) {
+    if (!h) return;
+    cudaFree(h->t.ops); cudaFree(h->t.info); cudaFree(h->t.crc_tab); cudaFree(h->t.info_words);
+    cudaFree(h->d_queue); cudaFree(h->d_snap);
+    for (int b = 0; b < 2; b++) {
+        cudaFree(h->d_stage_llr[b]); cudaFree(h->d_stage_bits[b]);
+        if (h->ev_h2d[b]) cudaEventDestroy(h->ev_h2d[b]);
+        if (h->ev_dec[b]) cudaEventDestroy(h->ev_dec[b]);
+        if (h->ev_d2h[b]) cudaEventDestroy(h->ev_d2h[b]);
+    }
+    if (h->s_h2d) cudaStreamDestroy(h->s_h2d);
+    if (h->s_comp) cudaStreamDestroy(h->s_comp);
+    if (h->s_d2h) cudaStreamDestroy(h->s_d2h);
+    delete h;
+}
+
+double sigma2_of(double ebno_db, double rate) { return 1.0 / (2.0 * rate * std::pow(10.0, ebno_db / 10.0)); }
+
+CodecParams codec_params(polar_scs_t h, int64_t n) {
+    CodecParams p{};
+    p.n_frames = n;
+    p.N = h->t.N; p.n = h->t.n; p.K = h->t.K; p.c = h->t.c;
+    p.nw = std::max(1, h->t.N / 32);
+    p.info = h->t.info; p.crc_tab = h->t.crc_tab; p.info_words = h->t.info_words;
+    return p;
+}
+
+int cuda_status(cudaError_t e) { return e == cudaSuccess ? POLAR_OK : (e == cudaErrorMemoryAllocation ? POLAR_ENOMEM : POLAR_ECUDA); }
+
+int decode_impl(polar_scs_t h, const float *llr, int64_t n, uint8_t *bits, float *pm, uint32_t *pops,
+                uint32_t *sw, uint8_t *status, cudaStream_t st) {
+    DecodeParams p = h->base;
+    p.llr = llr; p.n_frames = n; p.out_bits = bits;
+    p.pm = pm; p.pops = pops; p.switches = sw; p.status = status;
+    cudaError_t e = cudaMemsetAsync(h->d_queue, 0, sizeof(unsigned long long), st);
+    if (e != cudaSuccess) return cuda_status(e);
+    return cuda_status(launch_decode(p, slots_for(h->D), h->snap_in_smem != 0, h->ctas, h->smem_per_cta, st));
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *polar_scs_strerror(int status) {
+    switch (status) {
+    case POLAR_OK: return "ok";
+    case POLAR_EINVAL: return "invalid argument";
+    case POLAR_ENOMEM: return "out of memory";
+    case POLAR_ECUDA: return "CUDA error";
+    case POLAR_ENOTSYS: return "not supported for this code";
+    default: return "unknown status";
+    }
+}
+
+int polar_scs_create_ex(polar_scs_t *out, int32_t N, int32_t K, const uint8_t *frozen_mask, int32_t D, int32_t L,
+                        uint32_t crc_poly, uint32_t flags) {
+    if (!out) return POLAR_EINVAL;
+    *out = nullptr;
+    if (D < 1 || D > kMaxD || L < 1 || (flags & ~(POLAR_FLAG_BIT_LEVEL | POLAR_FLAG_SNAP_GLOBAL))) return POLAR_EINVAL;
+    HostCode hc;
+    int rc = build_host_code(N, K, frozen_mask, crc_poly, (flags & POLAR_FLAG_BIT_LEVEL) != 0, hc);
+    if (rc != POLAR_OK) return rc;
+
+    polar_scs_t h = new (std::nothrow) polar_scs_s();
+    if (!h) return POLAR_ENOMEM;
+    h->flags = flags;
+    h->D = D;
+    h->L = std::min(L, 65535);
+    cudaError_t e = cudaGetDevice(&h->device);
+    CodeTables &t = h->t;
+    t.N = hc.N; t.n = hc.n; t.K = hc.K; t.c = hc.c; t.M = hc.M; t.crc_poly = crc_poly;
+    t.systematic_ok = hc.systematic_ok;
+    t.nops = (int)hc.ops.size();
+    if (e == cudaSuccess) e = upload(&t.ops, hc.ops);
+    if (e == cudaSuccess) e = upload(&t.info, hc.info);
+    if (e == cudaSuccess) e = upload(&t.crc_tab, hc.crc_tab);
+    if (e == cudaSuccess) e = upload(&t.info_words, hc.info_words);
+    if (e == cudaSuccess) e = cudaMalloc(&h->d_queue, sizeof(unsigned long long));
+    if (e != cudaSuccess) { free_handle(h); return cuda_status(e); }
+
+    // ---- decode launch layout (per-warp shared memory)
+    int sms = 148, optin = 227 * 1024;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device);
+    cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device);
+    const int nw = std::max(1, N / 32);
+    const int cnt_words = ((t.M + 1) * 2 + 3) / 4;
+    const int sstride = nw + 2;
+    const int base_words = 2 * N + 2 * nw + cnt_words;
+    const int sched_words = (t.nops * 4 <= 16384) ? round4(t.nops) : 0;
+    const int slots = slots_for(D);
+
+    DecodeParams &p = h->base;
+    p.ops = t.ops; p.info = t.info; p.crc_tab = t.crc_tab; p.queue = h->d_queue;
+    p.N = N; p.n = t.n; p.K = K; p.c = t.c; p.D = D; p.L = h->L; p.M = t.M; p.nops = t.nops;
+    p.nw = nw; p.snap_stride = sstride; p.sched_words = sched_words; p.cnt_words = cnt_words;
+
+    int occ = 0;
+    bool use_smem = false;
+    if (!(flags & POLAR_FLAG_SNAP_GLOBAL)) {
+        const int ww = round4(base_words + D * sstride);
+        const int smem = 4 * (sched_words + kDecodeWarps * ww);
+        if (smem <= optin && decode_occupancy(slots, true, smem, &occ) == cudaSuccess && occ * kDecodeWarps >= 16) {
+            use_smem = true;
+            p.warp_words = ww;
+            h->smem_per_cta = smem;
+        }
+    }
+    if (!use_smem) {
+        const int ww = round4(base_words);
+        const int smem = 4 * (sched_words + kDecodeWarps * ww);
+        if (smem > optin) { free_handle(h); return POLAR_EINVAL; }
+        e = decode_occupancy(slots, false, smem, &occ);
+        if (e != cudaSuccess || occ < 1) { free_handle(h); return e != cudaSuccess ? cuda_status(e) : POLAR_EINVAL; }
+        p.warp_words = ww;
+        h->smem_per_cta = smem;
+    }
+    cudaGetLastError();
+    h->snap_in_smem = use_smem ? 1 : 0;
+    h->warps_per_cta = kDecodeWarps;
+    h->ctas = occ * sms;
+    if (!use_smem) {
+        h->snap_bytes = (size_t)h->ctas * kDecodeWarps * (size_t)D * sstride * 4;
+        e = cudaMalloc(&h->d_snap, h->snap_bytes);
+        if (e != cudaSuccess) { free_handle(h); return cuda_status(e); }
+        p.snap_global = h->d_snap;
+    }
+    *out = h;
+    return POLAR_OK;
+}
+
+int polar_scs_create(polar_scs_t *out, int32_t N, int32_t K, const uint8_t *frozen_mask, int32_t D, int32_t L,
+                     uint32_t crc_poly) {
+    return polar_scs_create_ex(out, N, K, frozen_mask, D, L, crc_poly, 0u);
+}
+
+void polar_scs_destroy(polar_scs_t h) {
+    if (!h) return;
+    cudaDeviceSynchronize();
+    free_handle(h);
+}
+
+int polar_scs_get_info(polar_scs_t h, polar_scs_info_t *o) {
+    if (!h || !o) return POLAR_EINVAL;
+    o->N = h->t.N; o->n = h->t.n; o->K = h->t.K; o->crc_bits = h->t.c; o->D = h->D; o->L = h->L;
+    o->num_ops = h->t.nops; o->num_nodes = h->t.M;
+    o->warps_per_cta = h->warps_per_cta; o->ctas = h->ctas; o->smem_per_cta = h->smem_per_cta;
+    o->snap_in_smem = h->snap_in_smem; o->systematic_ok = h->t.systematic_ok ? 1 : 0; o->flags = h->flags;
+    return POLAR_OK;
+}
+
+int polar_scs_decode_stats(polar_scs_t h, const float *llr, int64_t n, uint8_t *bits, float *pm, uint32_t *pops,
+                           uint32_t *sw, uint8_t *status, void *stream) {
+    if (!h || n < 0) return POLAR_EINVAL;
+    if (n == 0) return POLAR_OK;
+    if (!llr || !bits) return POLAR_EINVAL;
+    if (h->t.N >= 4 && (reinterpret_cast<uintptr_t>(llr) & 15u)) return POLAR_EINVAL;
+    return decode_impl(h, llr, n, bits, pm, pops, sw, status, static_cast<cudaStream_t>(stream));
+}
+
+int polar_scs_decode(polar_scs_t h, const float *llr, int64_t n, uint8_t *bits, void *stream) {
+    return polar_scs_decode_stats(h, llr, n, bits, nullptr, nullptr, nullptr, nullptr, stream);
+}
+
+int polar_scs_decode_host(polar_scs_t h, const float *llr_host, int64_t n, uint8_t *bits_host, void *stream) {
+    if (!h || n < 0) return POLAR_EINVAL;
+    if (n == 0) return POLAR_OK;
+    if (!llr_host || !bits_host) return POLAR_EINVAL;
+    const int N = h->t.N, K = h->t.K;
+    cudaError_t e = cudaSuccess;
+    if (!h->s_comp) {
+        // chunk of about 128 MiB of LLRs, double-buffered
+        h->stage_frames = std::max<int64_t>(1, (int64_t)(128ll << 20) / (4ll * N));
+        for (int b = 0; b < 2 && e == cudaSuccess; b++) {
+            e = cudaMalloc(&h->d_stage_llr[b], (size_t)h->stage_frames * N * 4);
+            if (e == cudaSuccess) e = cudaMalloc(&h->d_stage_bits[b], (size_t)h->stage_frames * K);
+            if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_h2d[b], cudaEventDisableTiming);
+            if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_dec[b], cudaEventDisableTiming);
+            if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_d2h[b], cudaEventDisableTiming);
+        }
+        if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->s_h2d, cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->s_comp, cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->s_d2h, cudaStreamNonBlocking);
+        if (e != cudaSuccess) return cuda_status(e);
+    }
+    cudaEvent_t start;
+    e = cudaEventCreateWithFlags(&start, cudaEventDisableTiming);
+    if (e != cudaSuccess) return cuda_status(e);
+    cudaEventRecord(start, static_cast<cudaStream_t>(stream));
+    cudaStreamWaitEvent(h->s_h2d, start, 0);
+    cudaStreamWaitEvent(h->s_comp, start, 0);
+    int rc = POLAR_OK;
+    int64_t i = 0;
+    for (int64_t off = 0; off < n && rc == POLAR_OK; off += h->stage_frames, i++) {
+        const int b = (int)(i & 1);
+        const int64_t cnt = std::min<int64_t>(h->stage_frames, n - off);
+        cudaStreamWaitEvent(h->s_h2d, h->ev_dec[b], 0);       // buffer b's previous decode has read it
+        e = cudaMemcpyAsync(h->d_stage_llr[b], llr_host + off * N, (size_t)cnt * N * 4, cudaMemcpyHostToDevice, h->s_h2d);
+        if (e != cudaSuccess) { rc = cuda_status(e); break; }
+        cudaEventRecord(h->ev_h2d[b], h->s_h2d);
+        cudaStreamWaitEvent(h->s_comp, h->ev_h2d[b], 0);
+        cudaStreamWaitEvent(h->s_comp, h->ev_d2h[b], 0);      // bits buffer b has been copied out
+        rc = decode_impl(h, h->d_stage_llr[b], cnt, h->d_stage_bits[b], nullptr, nullptr, nullptr, nullptr, h->s_comp);
+        cudaEventRecord(h->ev_dec[b], h->s_comp);
+        cudaStreamWaitEvent(h->s_d2h, h->ev_dec[b], 0);
+        e = cudaMemcpyAsync(bits_host + off * K, h->d_stage_bits[b], (size_t)cnt * K, cudaMemcpyDeviceToHost, h->s_d2h);
+        if (e != cudaSuccess) { rc = cuda_status(e); break; }
+        cudaEventRecord(h->ev_d2h[b], h->s_d2h);
+    }
+    e = cudaStreamSynchronize(h->s_d2h);
+    if (rc == POLAR_OK && e != cudaSuccess) rc = cuda_status(e);
+    e = cudaStreamSynchronize(h->s_comp);
+    if (rc == POLAR_OK && e != cudaSuccess) rc = cuda_status(e);
+    cudaEventDestroy(start);
+    return rc;
+}
+
+int polar_crc_attach_batch(polar_scs_t h, const uint8_t *payload, int64_t n, uint8_t *block, void *stream) {
+    if (!h || n < 0) return POLAR_EINVAL;
+    if (n == 0) return POLAR_OK;
+    if (!payload || !block) return POLAR_EINVAL;
+    CodecParams p = codec_params(h, n);
+    p.payload = payload; p.block_out = block;
+    return cuda_status(launch_crc_attach(p, static_cast<cudaStream_t>(stream)));
+}
+
+int polar_encode_batch(polar_scs_t h, const uint8_t *block, int64_t n, uint8_t *codeword, void *stream) {
+    if (!h || n < 0) return POLAR_EINVAL;
+    if (!h->t.systematic_ok) return POLAR_ENOTSYS;
+    if (n == 0) return POLAR_OK;
+    if (!block || !codeword) return POLAR_EINVAL;
+    CodecParams p = codec_params(h, n);
+    p.block_in = block; p.codeword = codeword;
+    return cuda_status(launch_encode(p, static_cast<cudaStream_t>(stream)));
+}
+
+int polar_modulate_batch(polar_scs_t h, const uint8_t *codeword, const float *noise, int64_t n, double ebno_db,
+                         float *llr, void *stream) {
+    if (!h || n < 0) return POLAR_EINVAL;
+    if (n == 0) return POLAR_OK;
+    if (!codeword || !noise || !llr) return POLAR_EINVAL;
+    CodecParams p = codec_params(h, n);
+    const double var = sigma2_of(ebno_db, (double)h->t.K / (double)h->t.N);
+    p.sigma_f = (float)std::sqrt(var);
+    p.scale_f = (float)(2.0 / var);
+    p.codeword = const_cast<uint8_t *>(codeword); p.noise = noise; p.llr = llr;
+    return cuda_status(launch_modulate(p, static_cast<cudaStream_t>(stream)));
+}
+
+int polar_generate_batch(polar_scs_t h, uint64_t seed, double ebno_db, int64_t first_frame, int64_t n,
+                         uint8_t *block, float *llr, void *stream) {
+    if (!h || n < 0 || first_frame < 0) return POLAR_EINVAL;
+    if (!h->t.systematic_ok) return POLAR_ENOTSYS;
+    if (n == 0) return POLAR_OK;
+    if (!llr) return POLAR_EINVAL;
+    if (h->t.N >= 4 && (reinterpret_cast<uintptr_t>(llr) & 15u)) return POLAR_EINVAL;
+    CodecParams p = codec_params(h, n);
+    const double var = sigma2_of(ebno_db, (double)h->t.K / (double)h->t.N);
+    p.sigma_f = (float)std::sqrt(var);
+    p.scale_f = (float)(2.0 / var);
+    p.seed = seed; p.first_frame = first_frame; p.block_out = block; p.llr = llr;
+    return cuda_status(launch_generate(p, static_cast<cudaStream_t>(stream)));
+}
+
+}  // extern "C"

@@ -1,0 +1,661 @@
+// decode.cu — the FSSCS-RM decode kernel for sm_100a.
+//
+// One warp decodes one frame at a time; a persistent grid pulls frames from a
+// global queue so early-terminating frames free their warp.  Per warp, shared
+// memory holds the channel LLRs (alpha_n), the single alpha memory (stage
+// lambda = Lambda floats), the flat N-bit beta
+// and the per-length counters.  The path-metric stack lives in
+// registers: lane l owns entries l, l+32, ... (SLOTS = ceil(D/32) per lane) and
+// selection / replacement use warp reductions (REDUX) — the paper's linear
+// search done as a 32-wide parallel search.  Each stack entry
+// references a snapshot slot holding the beta prefix of its fork plus a flip
+// descriptor (paths store beta, not u_hat), so a path switch
+// restores beta without repopulation and recomputes the alpha spine from the
+// root (Alg. 4).
+//
+// Arithmetic is float32 with the operation order of the oracle (reading R3):
+// f/g per Eq. (1) and corrected Eq. (2) (reading R1), tree-order sums, argmin
+// keys (|alpha| bits, index), candidates sorted by (dPM, mask), stack order
+// (PM, serial).  Built with -fmad=false; no fast-math.
+#include <cuda_runtime.h>
+
+#include "internal.h"
+
+namespace polar {
+
+constexpr uint32_t FULL = 0xFFFFFFFFu;
+constexpr uint32_t EMPTY = 0xFFFFFFFFu;
+constexpr uint32_t NO_SNAP = 0xFFFFu;
+
+__device__ __forceinline__ float f_minsum(float a, float b) {      // Eq. (1)
+    const float m = fminf(fabsf(a), fabsf(b));
+    return ((a < 0.f) != (b < 0.f)) ? -m : m;
+}
+// corrected Eq. (2): g = a_hi + (1 - 2 beta) a_lo (reading R1); a_hi - a_lo is
+// a_hi + (-a_lo) exactly, so flipping the sign bit of a_lo is exact.
+__device__ __forceinline__ float g_exact(float lo, float hi, uint32_t bit) {
+    return hi + __uint_as_float(__float_as_uint(lo) ^ (bit << 31));
+}
+__device__ __forceinline__ float negpart(float x) { return x < 0.f ? -x : 0.f; }
+__device__ __forceinline__ float pospart(float x) { return x < 0.f ? 0.f : x; }
+
+// ALPHA(s, psi): alpha_s from alpha_{s+1} (Eq. 4, Alg. 1).  Stage s lives at
+// alpha[2^s, 2^{s+1}); stage n is the channel row.
+__device__ __forceinline__ void alpha_stage(const float *chan, float *alpha, const uint32_t *beta,
+                                            int n, int s, int psi, int lane) {
+    const int Ls = 1 << s;
+    const float *src = (s + 1 == n) ? chan : alpha + (2 << s);
+    float *dst = alpha + Ls;
+    if ((psi & 1) == 0) {
+        if (Ls >= 128) {
+            for (int i = lane * 4; i < Ls; i += 128) {
+                const float4 lo = *reinterpret_cast<const float4 *>(src + i);
+                const float4 hi = *reinterpret_cast<const float4 *>(src + Ls + i);
+                float4 o;
+                o.x = f_minsum(lo.x, hi.x); o.y = f_minsum(lo.y, hi.y);
+                o.z = f_minsum(lo.z, hi.z); o.w = f_minsum(lo.w, hi.w);
+                *reinterpret_cast<float4 *>(dst + i) = o;
+            }
+        } else {
+            for (int i = lane; i < Ls; i += 32) dst[i] = f_minsum(src[i], src[i + Ls]);
+        }
+    } else {
+        const int boff = (psi - 1) * Ls;            // left sibling's segment of the flat beta
+        if (Ls >= 128) {
+            for (int i = lane * 4; i < Ls; i += 128) {
+                const float4 lo = *reinterpret_cast<const float4 *>(src + i);
+                const float4 hi = *reinterpret_cast<const float4 *>(src + Ls + i);
+                const uint32_t b = beta[(boff + i) >> 5] >> ((boff + i) & 31);
+                float4 o;
+                o.x = g_exact(lo.x, hi.x, b & 1); o.y = g_exact(lo.y, hi.y, (b >> 1) & 1);
+                o.z = g_exact(lo.z, hi.z, (b >> 2) & 1); o.w = g_exact(lo.w, hi.w, (b >> 3) & 1);
+                *reinterpret_cast<float4 *>(dst + i) = o;
+            }
+        } else {
+            for (int i = lane; i < Ls; i += 32) {
+                const int p = boff + i;
+                dst[i] = g_exact(src[i], src[i + Ls], (beta[p >> 5] >> (p & 31)) & 1);
+            }
+        }
+    }
+    __syncwarp();
+}
+
+// BETA(lam, phi): beta[(phi-1)Lam + i] ^= beta[phi Lam + i] (Fig. 7d)
+__device__ __forceinline__ void beta_op(uint32_t *beta, int lam, int phi, int lane) {
+    const int Lam = 1 << lam;
+    if (Lam >= 32) {
+        const int wd = ((phi - 1) * Lam) >> 5, ws = (phi * Lam) >> 5, nwd = Lam >> 5;
+        for (int t = lane; t < nwd; t += 32) beta[wd + t] ^= beta[ws + t];
+    } else if (lane == 0) {
+        const int p = (phi - 1) * Lam;             // 2*Lam bits inside one word
+        const int w = p >> 5, o = p & 31;
+        const uint32_t x = beta[w];
+        const uint32_t r = (x >> (o + Lam)) & ((1u << Lam) - 1u);
+        beta[w] = x ^ (r << o);
+    }
+    __syncwarp();
+}
+
+// Warp minimum of 64-bit keys (hi, lo) with unique lo among equal hi.
+__device__ __forceinline__ void warp_min_key(uint32_t hi, uint32_t lo, uint32_t &mh, uint32_t &ml) {
+    mh = __reduce_min_sync(FULL, hi);
+    ml = __reduce_min_sync(FULL, hi == mh ? lo : 0xFFFFFFFFu);
+}
+
+__device__ __forceinline__ void top4_insert(unsigned long long key, unsigned long long &t0, unsigned long long &t1,
+                                            unsigned long long &t2, unsigned long long &t3) {
+    if (key < t3) {
+        if (key < t2) {
+            t3 = t2;
+            if (key < t1) {
+                t2 = t1;
+                if (key < t0) { t1 = t0; t0 = key; } else t1 = key;
+            } else t2 = key;
+        } else t3 = key;
+    }
+}
+
+template <int SLOTS, bool SNAP_SMEM>
+__global__ void __launch_bounds__(kDecodeWarps * 32)
+fsscs_decode_kernel(const DecodeParams P) {
+    extern __shared__ __align__(16) uint32_t smem[];
+    const int lane = threadIdx.x & 31;
+    const int warp = threadIdx.x >> 5;
+    const int N = P.N, n = P.n, K = P.K, D = P.D, nw = P.nw, nops = P.nops;
+
+    // stage the schedule (read by every op) in shared memory when it fits
+    const uint32_t *ops = P.ops;
+    if (P.sched_words > 0) {
+        for (int i = threadIdx.x; i < nops; i += blockDim.x) smem[i] = P.ops[i];
+        __syncthreads();
+        ops = smem;
+    }
+    uint32_t *wb = smem + P.sched_words + warp * P.warp_words;
+    float *chan = reinterpret_cast<float *>(wb);
+    float *alpha = chan + N;
+    uint32_t *beta = reinterpret_cast<uint32_t *>(alpha + N);
+    uint32_t *best = beta + nw;
+    uint16_t *cnt = reinterpret_cast<uint16_t *>(best + nw);
+    uint32_t *snap;
+    if (SNAP_SMEM) snap = best + nw + P.cnt_words;
+    else snap = P.snap_global + (size_t)(blockIdx.x * kDecodeWarps + warp) * (size_t)D * P.snap_stride;
+    const int sstride = P.snap_stride;
+
+    unsigned long long f = 0;
+    if (lane == 0) f = atomicAdd(P.queue, 1ull);
+    f = __shfl_sync(FULL, f, 0);
+
+    while (f < (unsigned long long)P.n_frames) {
+        unsigned long long fnext = 0;
+        if (lane == 0) fnext = atomicAdd(P.queue, 1ull);
+
+        // ---- stage the channel row (the only mandatory HBM read) ----------
+        const float *row = P.llr + (size_t)f * N;
+        if (N >= 4) {
+            for (int i = lane * 4; i < N; i += 128)
+                *reinterpret_cast<float4 *>(chan + i) = __ldcs(reinterpret_cast<const float4 *>(row + i));
+        } else if (lane < N) {
+            chan[lane] = row[lane];
+        }
+        for (int i = lane; i < P.cnt_words; i += 32) reinterpret_cast<uint32_t *>(cnt)[i] = 0;
+        __syncwarp();
+
+        // ---- stack: root path (PM 0, serial 0, k 0, j 0) ------------------
+        uint32_t s_pm[SLOTS], s_ser[SLOTS], s_kj[SLOTS], s_sm[SLOTS];
+#pragma unroll
+        for (int s = 0; s < SLOTS; s++) { s_pm[s] = EMPTY; s_ser[s] = EMPTY; s_kj[s] = 0; s_sm[s] = NO_SNAP; }
+        if (lane == 0) { s_pm[0] = 0u; s_ser[0] = 0u; }
+        int nS = 1;
+        uint32_t work = 0, next_serial = 1, pops = 0, switches = 0;
+        int work_pl = 0;
+        bool have_best = false;
+        float best_pm = 0.f, out_pm = 0.f;
+        int status = 0;
+        bool from_best = false;
+        const uint32_t pop_cap = (uint32_t)P.L * (uint32_t)(P.M + 1);
+
+        for (;;) {
+            if (nS == 0) { from_best = true; out_pm = best_pm; status = 1; break; }   // reading R13
+            if (pops >= pop_cap) { status = 2; out_pm = -1.f; break; }   // watchdog: cannot happen (cnt[j] <= L)
+            // ---- select: min (PM, serial) (reading R7)
+            uint32_t lpm = EMPTY, lser = EMPTY;
+            int ls = 0;
+#pragma unroll
+            for (int s = 0; s < SLOTS; s++)
+                if (s_pm[s] < lpm || (s_pm[s] == lpm && s_ser[s] < lser)) { lpm = s_pm[s]; lser = s_ser[s]; ls = s; }
+            uint32_t mpm, mser;
+            warp_min_key(lpm, lser, mpm, mser);
+            const int owner = __ffs(__ballot_sync(FULL, lpm == mpm && lser == mser)) - 1;
+            uint32_t mykj = 0, mysm = 0;
+#pragma unroll
+            for (int s = 0; s < SLOTS; s++) if (s == ls) { mykj = s_kj[s]; mysm = s_sm[s]; }
+            const uint32_t p_kj = __shfl_sync(FULL, mykj, owner);
+            const uint32_t p_sm = __shfl_sync(FULL, mysm, owner);
+            if (lane == owner) {
+#pragma unroll
+                for (int s = 0; s < SLOTS; s++) if (s == ls) { s_pm[s] = EMPTY; s_ser[s] = EMPTY; }
+            }
+            nS--;
+            pops++;
+            const float p_pm = __uint_as_float(mpm);
+            const uint32_t p_ser = mser;
+            const int p_k = (int)(p_kj & 0xFFFFu), p_j = (int)(p_kj >> 16);
+
+            // ---- per-length counter and prune (readings R9, R10)
+            const int c_j = (int)cnt[p_j] + 1;
+            __syncwarp();
+            if (lane == 0) cnt[p_j] = (uint16_t)c_j;
+            if (c_j == P.L) {
+                int cntv = 0;
+#pragma unroll
+                for (int s = 0; s < SLOTS; s++) {
+                    if (s_ser[s] != EMPTY && (int)(s_kj[s] >> 16) <= p_j) { s_pm[s] = EMPTY; s_ser[s] = EMPTY; }
+                    cntv += __popc(__ballot_sync(FULL, s_ser[s] != EMPTY));
+                }
+                nS = cntv;
+            }
+
+            // ---- path switch ---------------------
+            bool dirty = false;
+            if (p_ser != work) {
+                switches++;
+                // the path being left keeps its beta in a snapshot if it is still live
+                int wsl = -1;
+#pragma unroll
+                for (int s = 0; s < SLOTS; s++) if (s_ser[s] == work) wsl = s;
+                const uint32_t wb_ = __ballot_sync(FULL, wsl >= 0);
+                if (wb_) {
+                    const int wl = __ffs(wb_) - 1;
+                    uint32_t wsm = 0;
+#pragma unroll
+                    for (int s = 0; s < SLOTS; s++) if (s == wsl) wsm = s_sm[s];
+                    wsm = __shfl_sync(FULL, wsm, wl);
+                    const int wslot = __shfl_sync(FULL, wsl, wl);
+                    if ((wsm & 0xFFFFu) == NO_SNAP) {
+                        // allocate a free slot (not referenced by a live entry nor by p)
+                        int slot = -1;
+#pragma unroll
+                        for (int w = 0; w < SLOTS; w++) {
+                            uint32_t used = 0;
+#pragma unroll
+                            for (int s = 0; s < SLOTS; s++) {
+                                const uint32_t sn = s_sm[s] & 0xFFFFu;
+                                if (s_ser[s] != EMPTY && sn != NO_SNAP && (int)(sn >> 5) == w) used |= 1u << (sn & 31);
+                            }
+                            used = __reduce_or_sync(FULL, used);
+                            const uint32_t ps = p_sm & 0xFFFFu;
+                            if (ps != NO_SNAP && (int)(ps >> 5) == w) used |= 1u << (ps & 31);
+                            const int lim = D - w * 32;
+                            uint32_t freem = ~used;
+                            if (lim < 32) freem &= (1u << lim) - 1u;
+                            if (slot < 0 && freem) slot = w * 32 + __ffs(freem) - 1;
+                        }
+                        uint32_t *dst = snap + (size_t)slot * sstride;
+                        const int nwords = (work_pl + 31) >> 5;
+                        for (int w = lane; w < nwords; w += 32) dst[w] = beta[w];
+                        if (lane == wl) {
+#pragma unroll
+                            for (int s = 0; s < SLOTS; s++) if (s == wslot) s_sm[s] = (uint32_t)slot;
+                        }
+                    }
+                }
+                // restore p's beta: fork snapshot + flip descriptor
+                const uint32_t ps = p_sm & 0xFFFFu, rel = p_sm >> 16;
+                const uint32_t nop = ops[p_k - 1];
+                const int nk = (int)op_kind(nop), nl = (int)op_lam(nop), nphi = (int)op_phi(nop);
+                const int p_pl = (nphi + 1) << nl;
+                const uint32_t *src = snap + (size_t)ps * sstride;
+                const int nwords = (p_pl + 31) >> 5;
+                for (int w = lane; w < nwords; w += 32) beta[w] = SNAP_SMEM ? src[w] : __ldcg(src + w);
+                __syncwarp();
+                if (rel != 0u) {
+                    const int seg = nphi << nl, Lam = 1 << nl;
+                    if (nk == OP_REP) {
+                        if (Lam >= 32) {
+                            for (int t = lane; t < (Lam >> 5); t += 32) beta[(seg >> 5) + t] ^= FULL;
+                        } else if (lane == 0) {
+                            beta[seg >> 5] ^= ((Lam == 32) ? FULL : ((1u << Lam) - 1u)) << (seg & 31);
+                        }
+                    } else if (lane == 0) {
+                        const uint32_t h0 = SNAP_SMEM ? src[nw] : __ldcg(src + nw);
+                        const uint32_t h1 = SNAP_SMEM ? src[nw + 1] : __ldcg(src + nw + 1);
+                        const uint32_t m[4] = {h0 & 0xFFFFu, h0 >> 16, h1 & 0xFFFFu, h1 >> 16};
+#pragma unroll
+                        for (int q = 0; q < 4; q++)
+                            if ((rel >> q) & 1u) {
+                                const int pos = seg + (int)m[q];
+                                beta[pos >> 5] ^= 1u << (pos & 31);
+                            }
+                    }
+                    __syncwarp();
+                }
+                work = p_ser;
+                work_pl = p_pl;
+                dirty = true;
+            }
+
+            // ---- continue the schedule from the stored progress
+            int k = p_k;
+            for (; k < nops; k++) {
+                const uint32_t op = ops[k];
+                const uint32_t kind = op_kind(op);
+                if (kind >= OP_R0) break;
+                const int lam = (int)op_lam(op), phi = (int)op_phi(op);
+                if (kind == OP_BETA) {
+                    beta_op(beta, lam, phi, lane);
+                } else {
+                    if (dirty) {                      // Alg. 4: spine from the root
+                        for (int s = n - 1; s > lam; s--) alpha_stage(chan, alpha, beta, n, s, phi >> (s - lam), lane);
+                        dirty = false;
+                    }
+                    alpha_stage(chan, alpha, beta, n, lam, phi, lane);
+                }
+            }
+
+            if (k == nops) {
+                // ---- complete path: CRC on the systematic bits
+                bool ok = true;
+                if (P.c > 0) {
+                    uint32_t syn = 0;
+                    for (int q = lane; q < K; q += 32) {
+                        const int idx = P.info[q];
+                        if ((beta[idx >> 5] >> (idx & 31)) & 1u) syn ^= P.crc_tab[q];
+                    }
+                    syn = __reduce_xor_sync(FULL, syn);
+                    ok = (syn == 0);
+                }
+                if (ok) { out_pm = p_pm; status = 0; break; }
+                if (!have_best) {
+                    for (int w = lane; w < nw; w += 32) best[w] = beta[w];
+                    __syncwarp();
+                    have_best = true;
+                    best_pm = p_pm;
+                }
+                continue;
+            }
+
+            // ---- decision node ----------
+            const uint32_t op = ops[k];
+            const int kind = (int)op_kind(op), lam = (int)op_lam(op), phi = (int)op_phi(op);
+            const int Lam = 1 << lam;
+            const int seg = phi << lam;
+            float *a = (lam == n) ? chan : alpha + Lam;
+            if (lam == n && (kind == OP_R0 || kind == OP_REP)) {
+                // whole code is one node: copy the channel so the sums can work in place
+                for (int i = lane; i < N; i += 32) alpha[i] = chan[i];
+                __syncwarp();
+                a = alpha;
+            }
+            float dpm[8];
+            int msk[8];
+            int nc = 1;
+            uint32_t mi[4] = {0, 0, 0, 0};
+#pragma unroll
+            for (int t = 0; t < 8; t++) { dpm[t] = 0.f; msk[t] = t; }
+
+            if (kind == OP_R0 || kind == OP_REP) {
+                // tree-order sums T(neg(a)) and T(pos(a)) (reading R3)
+                const bool rep = (kind == OP_REP);
+                float vn, vp;
+                if (Lam > 32) {
+                    const int R = Lam >> 5, H = R >> 1;
+                    for (int t = 0; t < H; t++) {        // first level, in place, lane-private columns
+                        const float x = a[32 * t + lane], y = a[32 * (t + H) + lane];
+                        a[32 * t + lane] = negpart(x) + negpart(y);
+                        a[32 * (t + H) + lane] = pospart(x) + pospart(y);
+                    }
+                    for (int h = H >> 1; h >= 1; h >>= 1)
+                        for (int t = 0; t < h; t++) {
+                            a[32 * t + lane] += a[32 * (t + h) + lane];
+                            if (rep) a[32 * (H + t) + lane] += a[32 * (H + t + h) + lane];
+                        }
+                    vn = a[lane];
+                    vp = a[32 * H + lane];
+                    for (int h = 16; h >= 1; h >>= 1) {
+                        vn += __shfl_down_sync(FULL, vn, h);
+                        vp += __shfl_down_sync(FULL, vp, h);
+                    }
+                    __syncwarp();
+                } else {
+                    const float x = (lane < Lam) ? a[lane] : 0.f;
+                    vn = negpart(x);
+                    vp = pospart(x);
+                    for (int h = Lam >> 1; h >= 1; h >>= 1) {
+                        vn += __shfl_down_sync(FULL, vn, h);
+                        vp += __shfl_down_sync(FULL, vp, h);
+                    }
+                }
+                vn = __shfl_sync(FULL, vn, 0);
+                vp = __shfl_sync(FULL, vp, 0);
+                if (!rep) {
+                    nc = 1; dpm[0] = vn; msk[0] = 0;
+                } else {
+                    nc = 2;
+                    if (vp < vn) { dpm[0] = vp; msk[0] = 1; dpm[1] = vn; msk[1] = 0; }
+                    else         { dpm[0] = vn; msk[0] = 0; dpm[1] = vp; msk[1] = 1; }
+                }
+            } else {
+                // R1 / SPC: hard-decision word, parity, least reliable positions
+                const int need = (kind == OP_SPC) ? 4 : 2;
+                unsigned long long t0 = ~0ull, t1 = ~0ull, t2 = ~0ull, t3 = ~0ull;
+                uint32_t par = 0, hdw = 0;
+                if (Lam >= 32) {
+                    const int R = Lam >> 5;
+                    for (int t = 0; t < R; t++) {
+                        const float x = a[32 * t + lane];
+                        const uint32_t b = __ballot_sync(FULL, x < 0.f);
+                        if (lane == (t & 31)) beta[(seg >> 5) + t] = b;
+                        par ^= (uint32_t)__popc(b);
+                        top4_insert(((unsigned long long)__float_as_uint(fabsf(x)) << 32) | (uint32_t)(32 * t + lane),
+                                    t0, t1, t2, t3);
+                    }
+                } else {
+                    const float x = (lane < Lam) ? a[lane] : 0.f;
+                    hdw = __ballot_sync(FULL, lane < Lam && x < 0.f);
+                    par = (uint32_t)__popc(hdw);
+                    if (lane < Lam) t0 = ((unsigned long long)__float_as_uint(fabsf(x)) << 32) | (uint32_t)lane;
+                }
+                par &= 1u;
+                float A[4] = {0.f, 0.f, 0.f, 0.f};
+                if (Lam == 1) {
+                    // R1 at Lambda = 1: HD and its flip (reading R6)
+                    A[0] = fabsf(a[0]);
+                    mi[0] = 0;
+                } else {
+#pragma unroll
+                    for (int r = 0; r < 4; r++) {
+                        if (r < need) {
+                            uint32_t mh, ml;
+                            warp_min_key((uint32_t)(t0 >> 32), (uint32_t)t0, mh, ml);
+                            mi[r] = ml;
+                            A[r] = __uint_as_float(mh);
+                            if ((uint32_t)t0 == ml && (uint32_t)(t0 >> 32) == mh) { t0 = t1; t1 = t2; t2 = t3; t3 = ~0ull; }
+                        }
+                    }
+                }
+                if (kind == OP_R1) {
+                    if (Lam == 1) {
+                        nc = 2; dpm[0] = 0.f; msk[0] = 0; dpm[1] = A[0]; msk[1] = 1;
+                    } else {
+                        nc = 4;   // Chase-II: order (0, m1, m2, m1+m2) is already sorted
+                        dpm[0] = 0.f; msk[0] = 0;
+                        dpm[1] = A[0]; msk[1] = 1;
+                        dpm[2] = A[1]; msk[2] = 2;
+                        dpm[3] = A[0] + A[1]; msk[3] = 3;
+                    }
+                } else {
+                    // SPC: the 8 flip sets S of {m1..m4} with |S| = parity (mod 2), mask order
+                    nc = 8;
+                    constexpr int kEven[8] = {0, 3, 5, 6, 9, 10, 12, 15};
+                    constexpr int kOdd[8] = {1, 2, 4, 7, 8, 11, 13, 14};
+#pragma unroll
+                    for (int t = 0; t < 8; t++) {
+                        const int s = par ? kOdd[t] : kEven[t];
+                        float d = 0.f;
+                        bool first = true;
+#pragma unroll
+                        for (int q = 0; q < 4; q++)
+                            if ((s >> q) & 1) { d = first ? A[q] : d + A[q]; first = false; }
+                        dpm[t] = d;
+                        msk[t] = s;
+                    }
+                    // stable sort by dPM (ties keep mask order)
+#pragma unroll
+                    for (int i = 0; i < 7; i++)
+#pragma unroll
+                        for (int j = 0; j < 7 - i; j++)
+                            if (dpm[j] > dpm[j + 1]) {
+                                const float td = dpm[j]; dpm[j] = dpm[j + 1]; dpm[j + 1] = td;
+                                const int tm = msk[j]; msk[j] = msk[j + 1]; msk[j + 1] = tm;
+                            }
+                }
+                if (Lam < 32) {
+                    // HD word of the node (Lam < 32 bits) into beta, c1's flips applied below
+                    if (lane == 0) {
+                        const uint32_t lm = (1u << Lam) - 1u;
+                        const int w = seg >> 5, o = seg & 31;
+                        beta[w] = (beta[w] & ~(lm << o)) | ((hdw & lm) << o);
+                    }
+                }
+                __syncwarp();
+            }
+
+            // ---- c1 continues in the working memory ------------------------
+            {
+                const int m0 = msk[0];
+                if (kind == OP_R0 || kind == OP_REP) {
+                    const uint32_t fill = (kind == OP_REP && m0) ? FULL : 0u;
+                    if (Lam >= 32) {
+                        for (int t = lane; t < (Lam >> 5); t += 32) beta[(seg >> 5) + t] = fill;
+                    } else if (lane == 0) {
+                        const uint32_t lm = ((1u << Lam) - 1u) << (seg & 31);
+                        beta[seg >> 5] = (beta[seg >> 5] & ~lm) | (fill & lm);
+                    }
+                } else if (lane == 0 && m0) {
+#pragma unroll
+                    for (int q = 0; q < 4; q++)
+                        if ((m0 >> q) & 1) {
+                            const int pos = seg + (int)mi[q];
+                            beta[pos >> 5] ^= 1u << (pos & 31);
+                        }
+                }
+                __syncwarp();
+            }
+            const int kn = k + 1, jn = p_j + 1, pl = (phi + 1) << lam;
+            const uint32_t ser0 = next_serial;
+            next_serial += (uint32_t)nc;
+            const uint32_t kj_new = (uint32_t)kn | ((uint32_t)jn << 16);
+
+            // insert c1 into a free entry (p's was freed, reading R8)
+            int c1_lane = 0, c1_slot = 0;
+            {
+                bool placed = false;
+#pragma unroll
+                for (int s = 0; s < SLOTS; s++) {
+                    const uint32_t fb = __ballot_sync(FULL, s_ser[s] == EMPTY);
+                    if (!placed && fb) {
+                        c1_lane = __ffs(fb) - 1; c1_slot = s; placed = true;
+                        if (lane == c1_lane) {
+                            s_pm[s] = __float_as_uint(p_pm + dpm[0]); s_ser[s] = ser0; s_kj[s] = kj_new; s_sm[s] = NO_SNAP;
+                        }
+                    }
+                }
+                nS++;
+            }
+            work = ser0;
+            work_pl = pl;
+
+            // siblings c2..: insert if room, else replace the least reliable iff
+            // strictly better; they share one fork snapshot.
+            int fslot = -1;
+            for (int t = 1; t < nc; t++) {
+                float dt = 0.f; int mt = 0;
+#pragma unroll
+                for (int q = 1; q < 8; q++) if (q == t) { dt = dpm[q]; mt = msk[q]; }
+                const uint32_t cpm = __float_as_uint(p_pm + dt);
+                int tl = -1, ts = 0;
+                if (nS < D) {
+#pragma unroll
+                    for (int s = 0; s < SLOTS; s++) {
+                        const uint32_t fb = __ballot_sync(FULL, s_ser[s] == EMPTY);
+                        if (tl < 0 && fb) { tl = __ffs(fb) - 1; ts = s; }
+                    }
+                    nS++;
+                } else {
+                    uint32_t xpm = 0, xser = 0;
+                    int xs = 0;
+#pragma unroll
+                    for (int s = 0; s < SLOTS; s++)
+                        if (s_ser[s] != EMPTY && (s_pm[s] > xpm || (s_pm[s] == xpm && s_ser[s] >= xser))) { xpm = s_pm[s]; xser = s_ser[s]; xs = s; }
+                    const uint32_t Mpm = __reduce_max_sync(FULL, xpm);
+                    const uint32_t Mser = __reduce_max_sync(FULL, xpm == Mpm ? xser : 0u);
+                    if (cpm < Mpm) {
+                        tl = __ffs(__ballot_sync(FULL, xpm == Mpm && xser == Mser)) - 1;
+                        ts = __shfl_sync(FULL, xs, tl);
+                    }
+                }
+                if (tl < 0) continue;                    // dropped
+                if (fslot < 0) {
+                    // fork snapshot: beta prefix [0, pl) with c1's segment + m1..m4
+                    int slot = -1;
+#pragma unroll
+                    for (int w = 0; w < SLOTS; w++) {
+                        uint32_t used = 0;
+#pragma unroll
+                        for (int s = 0; s < SLOTS; s++) {
+                            const uint32_t sn = s_sm[s] & 0xFFFFu;
+                            const bool victim = (lane == tl && s == ts);
+                            if (s_ser[s] != EMPTY && !victim && sn != NO_SNAP && (int)(sn >> 5) == w) used |= 1u << (sn & 31);
+                        }
+                        used = __reduce_or_sync(FULL, used);
+                        const int lim = D - w * 32;
+                        uint32_t freem = ~used;
+                        if (lim < 32) freem &= (1u << lim) - 1u;
+                        if (slot < 0 && freem) slot = w * 32 + __ffs(freem) - 1;
+                    }
+                    fslot = slot;
+                    uint32_t *dst = snap + (size_t)slot * sstride;
+                    const int nwords = (pl + 31) >> 5;
+                    for (int w = lane; w < nwords; w += 32) dst[w] = beta[w];
+                    if (lane == 0) {
+                        dst[nw] = mi[0] | (mi[1] << 16);
+                        dst[nw + 1] = mi[2] | (mi[3] << 16);
+                    }
+                }
+                if (lane == tl) {
+#pragma unroll
+                    for (int s = 0; s < SLOTS; s++)
+                        if (s == ts) {
+                            s_pm[s] = cpm; s_ser[s] = ser0 + (uint32_t)t; s_kj[s] = kj_new;
+                            s_sm[s] = (uint32_t)fslot | ((uint32_t)(mt ^ msk[0]) << 16);
+                        }
+                }
+            }
+            if (fslot >= 0 && lane == c1_lane) {
+#pragma unroll
+                for (int s = 0; s < SLOTS; s++) if (s == c1_slot) s_sm[s] = (uint32_t)fslot;
+            }
+        }
+
+        // ---- output: x_hat restricted to A, ascending -----
+        {
+            const uint32_t *bsrc = from_best ? best : beta;
+            uint8_t *ob = P.out_bits + (size_t)f * K;
+            for (int q = lane; q < K; q += 32) {
+                const int idx = P.info[q];
+                ob[q] = (uint8_t)((bsrc[idx >> 5] >> (idx & 31)) & 1u);
+            }
+            if (lane == 0) {
+                if (P.pm) P.pm[f] = out_pm;
+                if (P.pops) P.pops[f] = pops;
+                if (P.switches) P.switches[f] = switches;
+                if (P.status) P.status[f] = (uint8_t)status;
+            }
+            __syncwarp();
+        }
+        f = __shfl_sync(FULL, fnext, 0);
+    }
+}
+
+template <int SLOTS, bool SM>
+static cudaError_t launch_t(const DecodeParams &p, int ctas, int smem, cudaStream_t st) {
+    auto kern = fsscs_decode_kernel<SLOTS, SM>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    kern<<<ctas, kDecodeWarps * 32, smem, st>>>(p);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_decode(const DecodeParams &p, int slots, bool snap_smem, int ctas, int smem, cudaStream_t st) {
+    if (snap_smem) {
+        if (slots == 1) return launch_t<1, true>(p, ctas, smem, st);
+        if (slots == 2) return launch_t<2, true>(p, ctas, smem, st);
+        return launch_t<4, true>(p, ctas, smem, st);
+    }
+    if (slots == 1) return launch_t<1, false>(p, ctas, smem, st);
+    if (slots == 2) return launch_t<2, false>(p, ctas, smem, st);
+    return launch_t<4, false>(p, ctas, smem, st);
+}
+
+cudaError_t decode_occupancy(int slots, bool snap_smem, int smem, int *blocks_per_sm) {
+    cudaError_t e;
+#define OCC(S, B)                                                                                       \
+    do {                                                                                                \
+        e = cudaFuncSetAttribute(fsscs_decode_kernel<S, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); \
+        if (e != cudaSuccess) return e;                                                                 \
+        return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, fsscs_decode_kernel<S, B>,   \
+                                                             kDecodeWarps * 32, smem);                  \
+    } while (0)
+    if (snap_smem) {
+        if (slots == 1) OCC(1, true);
+        if (slots == 2) OCC(2, true);
+        OCC(4, true);
+    }
+    if (slots == 1) OCC(1, false);
+    if (slots == 2) OCC(2, false);
+    OCC(4, false);
+#undef OCC
+}
+
+}  // namespace polar

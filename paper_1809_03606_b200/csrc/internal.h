@@ -1,0 +1,108 @@
+// internal.h — product-internal definitions of libpolarscs (not part of the ABI).
+// The public boundary is include/polar_scs.h.
+#pragma once
+#include <cstdint>
+#include <vector>
+#include <cuda_runtime.h>
+
+#include "../../include/polar_scs.h"
+
+namespace polar {
+
+// Schedule op word: kind | lambda << 3 | phi << 8   (Fig. 5)
+enum OpKind : uint32_t { OP_ALPHA = 0, OP_BETA = 1, OP_R0 = 2, OP_R1 = 3, OP_REP = 4, OP_SPC = 5 };
+__host__ __device__ inline uint32_t op_make(uint32_t kind, uint32_t lam, uint32_t phi) {
+    return kind | (lam << 3) | (phi << 8);
+}
+__host__ __device__ inline uint32_t op_kind(uint32_t op) { return op & 7u; }
+__host__ __device__ inline uint32_t op_lam(uint32_t op) { return (op >> 3) & 31u; }
+__host__ __device__ inline uint32_t op_phi(uint32_t op) { return op >> 8; }
+
+constexpr int kMaxN = 4096;
+constexpr int kMaxD = 128;
+constexpr int kDecodeWarps = 4;      // warps (frames in flight) per decode CTA
+constexpr int kCodecWarps = 4;       // warps per CTA of the generator/encoder kernels
+
+// Host-side compiled code description (host.cpp)
+struct CodeTables {
+    int N = 0, n = 0, K = 0, c = 0, M = 0;
+    uint32_t crc_poly = 0;
+    bool systematic_ok = false;
+    uint32_t *ops = nullptr;  int nops = 0;     // schedule
+    uint16_t *info = nullptr;                   // A ascending, [K]
+    uint32_t *crc_tab = nullptr;                // [K] syndrome contribution of block bit k
+    uint32_t *info_words = nullptr;             // [max(1,N/32)] bit i set iff i in A
+};
+
+// Kernel parameter block of the decoder
+struct DecodeParams {
+    const float *llr;
+    int64_t n_frames;
+    uint8_t *out_bits;
+    float *pm;
+    uint32_t *pops, *switches;
+    uint8_t *status;
+    const uint32_t *ops;
+    const uint16_t *info;
+    const uint32_t *crc_tab;
+    unsigned long long *queue;
+    uint32_t *snap_global;      // arena when snapshots live in global memory
+    int N, n, K, c, D, L, M, nops;
+    int nw;                     // beta words = max(1, N/32)
+    int snap_stride;            // words per snapshot slot = nw + 2 (header: m1..m4)
+    int sched_words;            // schedule words staged in shared memory (0 = read global)
+    int warp_words;             // shared-memory words per warp
+    int cnt_words;              // words of the per-length counters (u16 each)
+};
+
+struct CodecParams {
+    const uint8_t *payload;     // crc attach input
+    const uint8_t *block_in;    // encode input
+    uint8_t *block_out;
+    uint8_t *codeword;
+    const float *noise;
+    float *llr;
+    int64_t n_frames, first_frame;
+    uint64_t seed;
+    float sigma_f, scale_f;
+    int N, n, K, c, nw;
+    const uint16_t *info;
+    const uint32_t *crc_tab;
+    const uint32_t *info_words;
+};
+
+}  // namespace polar
+
+struct polar_scs_s {
+    int device = 0;
+    uint32_t flags = 0;
+    int D = 0, L = 0;
+    polar::CodeTables t;            // device pointers
+    unsigned long long *d_queue = nullptr;
+    uint32_t *d_snap = nullptr;     // global snapshot arena (or null)
+    size_t snap_bytes = 0;
+    int snap_in_smem = 0;
+    int warps_per_cta = 0, ctas = 0, smem_per_cta = 0;
+    polar::DecodeParams base{};     // prefilled params
+    // host-staging for polar_scs_decode_host (lazily allocated)
+    cudaStream_t s_h2d = nullptr, s_comp = nullptr, s_d2h = nullptr;
+    float *d_stage_llr[2] = {nullptr, nullptr};
+    uint8_t *d_stage_bits[2] = {nullptr, nullptr};
+    cudaEvent_t ev_h2d[2] = {nullptr, nullptr}, ev_dec[2] = {nullptr, nullptr}, ev_d2h[2] = {nullptr, nullptr};
+    int64_t stage_frames = 0;
+};
+
+// host.cpp — code compilation on the host (validation, schedule, tables)
+namespace polar {
+struct HostCode {
+    int N = 0, n = 0, K = 0, c = 0, M = 0;
+    uint32_t crc_poly = 0;
+    bool systematic_ok = false;
+    std::vector<uint32_t> ops;
+    std::vector<uint16_t> info;
+    std::vector<uint32_t> crc_tab;
+    std::vector<uint32_t> info_words;
+};
+int build_host_code(int N, int K, const uint8_t *frozen, uint32_t crc_poly, bool bit_level, HostCode &hc);
+int crc_degree(uint32_t poly_full);
+}  // namespace polar

@@ -1,0 +1,94 @@
+"""CPU-side checks of the boundary: the C-ABI library loads and exports every
+symbol include/polar_scs.h declares; host-only entry points validate their
+arguments (no compute call needs a GPU here)."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HDR = os.path.join(ROOT, "include", "polar_scs.h")
+
+
+def _declared():
+    src = open(HDR).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(polar_\w+)\s*\(", src)))
+
+
+def test_header_declares_boundary():
+    names = _declared()
+    for must in ("polar_scs_create", "polar_scs_decode", "polar_encode_batch", "polar_generate_batch",
+                 "polar_scs_destroy", "polar_scs_strerror"):
+        assert must in names
+
+
+def test_library_exports_every_declared_symbol():
+    import paper_1809_03606_b200 as P
+    lib = ctypes.CDLL(P.library_path())
+    for name in _declared():
+        assert hasattr(lib, name), name
+    assert set(_declared()) == set(P.EXPORTED)
+
+
+def test_product_does_not_touch_oracle():
+    """The product package never imports, links or executes oracle/."""
+    pkg = os.path.join(ROOT, "paper_1809_03606_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cpp", ".h")):
+                txt = open(os.path.join(dirpath, f)).read()
+                assert "oracle" not in re.sub(r"(#|//).*", "", txt), f
+    so = open(os.path.join(pkg, "libpolarscs.so"), "rb").read()
+    assert b"orc_" not in so and b"liboracle" not in so
+
+
+def test_strerror_and_construct_validation():
+    import paper_1809_03606_b200 as P
+    assert P.polar_scs_strerror(0) == b"ok"
+    assert P.polar_scs_strerror(-1) == b"invalid argument"
+    m = np.zeros(8, np.uint8)
+    assert P.polar_construct_bhattacharyya(6, 3, 2.0, m.ctypes.data) == P.POLAR_EINVAL
+    assert P.polar_construct_bhattacharyya(8, 9, 2.0, m.ctypes.data) == P.POLAR_EINVAL
+    assert P.polar_construct_bhattacharyya(8, 4, 2.0, None) == P.POLAR_EINVAL
+    assert P.polar_construct_bhattacharyya(8, 4, 2.0, m.ctypes.data) == 0
+    assert list(np.nonzero(m == 0)[0]) == [3, 5, 6, 7]
+
+
+@pytest.mark.parametrize("cfg", ["C1", "C2", "C3", "C4", "C5"])
+def test_product_construction_equals_oracle(cfg):
+    import inputgen as ig
+    import oracle as O
+    import paper_1809_03606_b200 as P
+    c = ig.CONFIGS[cfg]
+    assert np.array_equal(P.bhattacharyya_mask(c["N"], c["K"], c["design_db"]),
+                          O.bhattacharyya_mask(c["N"], c["K"], c["design_db"]))
+
+
+def test_create_rejects_bad_arguments():
+    """Argument validation happens before any CUDA call."""
+    import paper_1809_03606_b200 as P
+    h = ctypes.c_void_p()
+    fr = P.bhattacharyya_mask(128, 64, 2.0)
+    ok = fr.ctypes.data
+    bad = [
+        (100, 64, ok, 8, 4, 0),          # N not a power of two
+        (8192, 64, ok, 8, 4, 0),         # N above the cap
+        (128, 65, ok, 8, 4, 0),          # mask weight != N - K
+        (128, 64, ok, 0, 4, 0),          # D < 1
+        (128, 64, ok, 129, 4, 0),        # D > 128
+        (128, 64, ok, 8, 0, 0),          # L < 1
+        (128, 64, None, 8, 4, 0),        # NULL mask
+        (128, 64, ok, 8, 4, 1),          # degenerate polynomial
+    ]
+    for args in bad:
+        assert P.polar_scs_create(ctypes.byref(h), *args) == P.POLAR_EINVAL, args
+    assert P.polar_scs_create(None, 128, 64, ok, 8, 4, 0) == P.POLAR_EINVAL
+    assert P.polar_scs_create_ex(ctypes.byref(h), 128, 64, ok, 8, 4, 0, 0x80) == P.POLAR_EINVAL
+    small = P.bhattacharyya_mask(16, 4, 2.0)
+    assert P.polar_scs_create(ctypes.byref(h), 16, 4, small.ctypes.data, 8, 4, 0x11021) == P.POLAR_EINVAL  # c >= K
+    P.polar_scs_destroy(None)                                     # no-op
+    assert P.polar_scs_decode(None, None, 0, None, None) == P.POLAR_EINVAL
+    assert P.polar_scs_get_info(None, None) == P.POLAR_EINVAL

@@ -1,0 +1,221 @@
+"""GPU <-> oracle parity through the C ABI (run on a B200 with -m gpu).
+
+Inputs are seeded draws from inputgen/ (payload bits, unit normals); each side
+computes CRC, systematic encoding and LLRs itself, and the LLR buffers are
+checked equal before the decoders are compared.  Contract (north star):
+decoded bits bit-exact, path metrics within rel 1e-6, pops and switches
+exact, status exact.
+"""
+import numpy as np
+import pytest
+
+import inputgen as ig
+import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_1809_03606_b200 as P  # noqa: E402  (fails loudly if the .so is missing)
+
+PM_RTOL = 1e-6
+
+
+def _mk(cfg, **kw):
+    c = dict(ig.CONFIGS[cfg])
+    c.update(kw)
+    fr = P.bhattacharyya_mask(c["N"], c["K"], c["design_db"])
+    assert np.array_equal(fr, O.bhattacharyya_mask(c["N"], c["K"], c["design_db"]))
+    return c, fr
+
+
+def _gpu_llr(dec, payload, noise, ebno):
+    """GPU path: CRC attach -> systematic encode -> modulate (all CUDA)."""
+    pay = torch.from_numpy(payload).cuda()
+    blk = dec.crc_attach(pay)
+    cw = dec.encode(blk)
+    llr = dec.modulate(cw, torch.from_numpy(noise).cuda(), ebno)
+    return blk, cw, llr
+
+
+def _oracle_llr(fr, crc, payload, noise, ebno):
+    blk = O.crc_attach(payload, crc)
+    cw = O.encode_systematic(fr, blk)
+    K = int((fr == 0).sum())
+    return blk, cw, O.awgn_llr(cw, noise, ebno, K / fr.size)
+
+
+def _compare(gpu, ref, ctx=""):
+    g = {k: v.cpu().numpy() for k, v in gpu.items()}
+    bad = np.nonzero((g["bits"] != ref["bits"]).any(1))[0]
+    assert bad.size == 0, f"{ctx} bits differ on frames {bad[:10]}"
+    assert np.array_equal(g["status"], ref["status"]), ctx
+    assert np.array_equal(g["pops"].astype(np.uint32), ref["pops"]), f"{ctx} pops"
+    assert np.array_equal(g["switches"].astype(np.uint32), ref["switches"]), f"{ctx} switches"
+    np.testing.assert_allclose(g["pm"], ref["pm"], rtol=PM_RTOL, atol=0, err_msg=ctx)
+
+
+def test_native_library_loaded():
+    import ctypes
+    assert P.library_path().endswith("libpolarscs.so")
+    assert isinstance(P._lib, ctypes.CDLL)
+
+
+@pytest.mark.parametrize("cfg", ["C1", "C2", "C3", "C4", "C5"])
+def test_codec_parity(cfg):
+    c, fr = _mk(cfg)
+    dec = P.PolarSCS(fr, c["D"], c["L"], c["crc_poly"])
+    n = 64
+    cc = dec.c
+    pay = ig.payload_bits(c["seed"], 5, n, c["K"] - cc)
+    nz = ig.unit_normals(c["seed"], 5, n, c["N"])
+    gb, gc, gl = _gpu_llr(dec, pay, nz, c["ebno"][0])
+    ob, oc, ol = _oracle_llr(fr, c["crc_poly"], pay, nz, c["ebno"][0])
+    assert np.array_equal(gb.cpu().numpy(), ob)
+    assert np.array_equal(gc.cpu().numpy(), oc)
+    assert np.array_equal(gl.cpu().numpy(), ol)          # bit-exact float32 LLRs
+
+
+@pytest.mark.parametrize("cfg", ["C1", "C3", "C5"])
+def test_generator_parity(cfg):
+    """Device generator: payload bits equal inputgen's Philox draws; CRC/encoding
+    equal the oracle's; LLRs equal the oracle's from inputgen normals up to the
+    double-precision Box-Muller rounding (rare 1-ulp differences)."""
+    c, fr = _mk(cfg)
+    dec = P.PolarSCS(fr, c["D"], c["L"], c["crc_poly"])
+    n, first = 200, 12345
+    blk, llr = dec.generate(c["seed"], c["ebno"][0], first, n)
+    pay = ig.payload_bits(c["seed"], first, n, c["K"] - dec.c)
+    nz = ig.unit_normals(c["seed"], first, n, c["N"])
+    ob, oc, ol = _oracle_llr(fr, c["crc_poly"], pay, nz, c["ebno"][0])
+    assert np.array_equal(blk.cpu().numpy(), ob)
+    g = llr.cpu().numpy()
+    np.testing.assert_allclose(g, ol, rtol=1e-5, atol=1e-5)
+    assert (g == ol).mean() > 0.999
+    assert np.array_equal(g < 0, ol < 0) or ((g < 0) != (ol < 0)).sum() <= 2
+
+
+CASES = [
+    ("C1", 2.5, 3000), ("C1", 0.0, 1000),
+    ("C2", 1.0, 150), ("C2", 2.0, 300), ("C2", 3.0, 300),
+    ("C3", 2.0, 300), ("C3", 0.5, 150),
+    ("C4", 1.5, 100), ("C4", 2.5, 150),
+    ("C5", 3.0, 60), ("C5", 4.0, 60),
+]
+
+
+@pytest.mark.parametrize("cfg,ebno,n", CASES)
+def test_decode_parity(cfg, ebno, n):
+    c, fr = _mk(cfg)
+    dec = P.PolarSCS(fr, c["D"], c["L"], c["crc_poly"])
+    pay = ig.payload_bits(c["seed"], 0, n, c["K"] - dec.c)
+    nz = ig.unit_normals(c["seed"], 0, n, c["N"])
+    _, _, gl = _gpu_llr(dec, pay, nz, ebno)
+    _, _, ol = _oracle_llr(fr, c["crc_poly"], pay, nz, ebno)
+    assert np.array_equal(gl.cpu().numpy(), ol)
+    ref = O.SCSDecoder(fr, c["D"], c["L"], c["crc_poly"]).decode(ol, threads=8)
+    _compare(dec.decode_stats(gl), ref, f"{cfg}@{ebno}")
+    # the plain decode entry point gives the same bits
+    assert np.array_equal(dec.decode(gl).cpu().numpy(), ref["bits"])
+
+
+@pytest.mark.parametrize("cfg", ["C2", "C5"])
+def test_decode_parity_snapshots_in_global(cfg):
+    c, fr = _mk(cfg)
+    dec = P.PolarSCS(fr, c["D"], c["L"], c["crc_poly"], snap_global=True)
+    assert dec.info["snap_in_smem"] == 0
+    n = 100
+    pay = ig.payload_bits(7, 0, n, c["K"] - dec.c)
+    nz = ig.unit_normals(7, 0, n, c["N"])
+    _, _, gl = _gpu_llr(dec, pay, nz, c["ebno"][0] - 0.5)
+    _, _, ol = _oracle_llr(fr, c["crc_poly"], pay, nz, c["ebno"][0] - 0.5)
+    ref = O.SCSDecoder(fr, c["D"], c["L"], c["crc_poly"]).decode(ol, threads=8)
+    _compare(dec.decode_stats(gl), ref, cfg)
+
+
+@pytest.mark.parametrize("N,K,D,L,crc,bit_level", [
+    (128, 64, 1, 4, 0, False),       # D = 1: plain FSSC
+    (128, 64, 8, 1, 0, False),       # L = 1
+    (128, 64, 128, 64, 0, False),    # deep stack, 4 entries per lane
+    (128, 64, 40, 8, 0x107, False),  # D not a multiple of 32
+    (128, 64, 8, 4, 0, True),        # bit-level SCS-RM (leaf-only schedule)
+    (256, 128, 64, 16, 0x11021, True),
+    (64, 40, 16, 4, 0x107, False),
+    (32, 16, 8, 2, 0x107, False),    # frequent CRC exhaustion
+    (2, 1, 4, 2, 0, False), (2, 2, 4, 2, 0, False), (4, 1, 4, 2, 0, False), (4, 3, 4, 2, 0, False),
+    (8, 4, 8, 4, 0, False), (16, 8, 16, 8, 0, False), (16, 16, 8, 4, 0, False), (16, 1, 8, 4, 0, False),
+    (4096, 2048, 128, 32, 0, False),
+])
+def test_decode_parity_edge(N, K, D, L, crc, bit_level):
+    fr = P.bhattacharyya_mask(N, K, 2.0)
+    dec = P.PolarSCS(fr, D, L, crc, bit_level=bit_level)
+    n = 257 if N <= 1024 else 40
+    for ebno in (-1.0, 1.0, 3.0):
+        pay = ig.payload_bits(N + K, 0, n, K - dec.c)
+        nz = ig.unit_normals(N + K, 0, n, N)
+        _, _, gl = _gpu_llr(dec, pay, nz, ebno)
+        _, _, ol = _oracle_llr(fr, crc, pay, nz, ebno)
+        ref = O.SCSDecoder(fr, D, L, crc, bit_level).decode(ol, threads=8)
+        _compare(dec.decode_stats(gl), ref, f"N{N}K{K}D{D}L{L}@{ebno}")
+
+
+def test_decode_degenerate_inputs():
+    c, fr = _mk("C2")
+    dec = P.PolarSCS(fr, c["D"], c["L"], 0)
+    z = torch.zeros((0, c["N"]), dtype=torch.float32, device="cuda")
+    assert dec.decode(z).shape == (0, c["K"])
+    # all-zero LLRs: every decision is a tie (HD(0) = 0, lowest index, lowest serial)
+    ol = np.zeros((3, c["N"]), np.float32)
+    ol[1, ::3] = 1.0
+    ol[2, ::5] = -1.0
+    ref = O.SCSDecoder(fr, c["D"], c["L"], 0).decode(ol)
+    _compare(dec.decode_stats(torch.from_numpy(ol).cuda()), ref, "ties")
+    # noiseless: pops = M + 1, no switch, PM 0
+    blk = torch.from_numpy(ig.payload_bits(3, 0, 17, c["K"])).cuda()
+    cw = dec.encode(blk)
+    llr = (1.0 - 2.0 * cw.float()) * 4.0
+    r = dec.decode_stats(llr)
+    assert torch.equal(r["bits"], blk)
+    assert bool((r["pops"] == dec.M + 1).all()) and bool((r["switches"] == 0).all())
+
+
+def test_decode_host_matches_device():
+    c, fr = _mk("C2")
+    dec = P.PolarSCS(fr, c["D"], c["L"], 0)
+    _, llr = dec.generate(1, 1.5, 0, 3000, want_block=False)
+    ref = dec.decode(llr).cpu()
+    host = llr.cpu().pin_memory()
+    out = dec.decode_host(host)
+    assert torch.equal(out, ref)
+
+
+def test_full_size_sampled_parity_c2():
+    """BASELINE C2 at full size in the bench's launch configuration: one call
+    decodes 5 x 100,000 frames; sampled frames are checked against the oracle."""
+    c, fr = _mk("C2")
+    dec = P.PolarSCS(fr, c["D"], c["L"], 0)
+    nf = c["frames"]
+    pay = ig.payload_bits(c["seed"], 0, nf, c["K"])
+    nz = ig.unit_normals(c["seed"], 0, nf, c["N"])
+    pay_t = torch.from_numpy(pay).cuda()
+    cw = dec.encode(dec.crc_attach(pay_t))
+    nz_t = torch.from_numpy(nz).cuda()
+    llr = torch.empty((len(c["ebno"]) * nf, c["N"]), dtype=torch.float32, device="cuda")
+    for p, eb in enumerate(c["ebno"]):
+        llr[p * nf:(p + 1) * nf] = dec.modulate(cw, nz_t, eb)
+    del nz_t
+    res = dec.decode_stats(llr)
+    torch.cuda.synchronize()
+    pick = ig.sample_frames(nf, 120, seed=5)
+    for p, eb in enumerate(c["ebno"]):
+        _, _, ol = _oracle_llr(fr, 0, pay[pick], nz[pick], eb)
+        rows = (p * nf + pick)
+        assert np.array_equal(llr[torch.from_numpy(rows).cuda()].cpu().numpy(), ol)
+        ref = O.SCSDecoder(fr, c["D"], c["L"], 0).decode(ol, threads=8)
+        sub = {k: v[torch.from_numpy(rows).cuda()] for k, v in res.items()}
+        _compare(sub, ref, f"C2 full @{eb}")
+    # properties that hold on every frame: output is the systematic part of a codeword
+    # whose final PM equals its correlation discrepancy
+    assert int(res["status"].sum()) == 0
