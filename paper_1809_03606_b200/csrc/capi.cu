@@ -38,7 +38,7 @@ int round4(int w) { return (w + 3) & ~3; }
 
 void free_handle(polar_scs_t h) {
     if (!h) return;
-    cudaFree(h->t.ops); cudaFree(h->t.info); cudaFree(h->t.crc_tab); cudaFree(h->t.info_words);
+    cudaFree(h->t.nodes); cudaFree(h->t.info); cudaFree(h->t.crc_tab); cudaFree(h->t.info_words);
     cudaFree(h->d_queue); cudaFree(h->d_snap);
     for (int b = 0; b < 2; b++) {
         cudaFree(h->d_stage_llr[b]); cudaFree(h->d_stage_bits[b]);
@@ -109,7 +109,7 @@ int polar_scs_create_ex(polar_scs_t *out, int32_t N, int32_t K, const uint8_t *f
     t.N = hc.N; t.n = hc.n; t.K = hc.K; t.c = hc.c; t.M = hc.M; t.crc_poly = crc_poly;
     t.systematic_ok = hc.systematic_ok;
     t.nops = (int)hc.ops.size();
-    if (e == cudaSuccess) e = upload(&t.ops, hc.ops);
+    if (e == cudaSuccess) e = upload(&t.nodes, hc.nodes);
     if (e == cudaSuccess) e = upload(&t.info, hc.info);
     if (e == cudaSuccess) e = upload(&t.crc_tab, hc.crc_tab);
     if (e == cudaSuccess) e = upload(&t.info_words, hc.info_words);
@@ -124,12 +124,12 @@ int polar_scs_create_ex(polar_scs_t *out, int32_t N, int32_t K, const uint8_t *f
     const int cnt_words = ((t.M + 1) * 2 + 3) / 4;
     const int sstride = nw + 2;
     const int base_words = 2 * N + 2 * nw + cnt_words;
-    const int sched_words = (t.nops * 4 <= 16384) ? round4(t.nops) : 0;
+    const int sched_words = (t.M * 4 <= 16384) ? round4(t.M) : 0;
     const int slots = slots_for(D);
 
     DecodeParams &p = h->base;
-    p.ops = t.ops; p.info = t.info; p.crc_tab = t.crc_tab; p.queue = h->d_queue;
-    p.N = N; p.n = t.n; p.K = K; p.c = t.c; p.D = D; p.L = h->L; p.M = t.M; p.nops = t.nops;
+    p.nodes = t.nodes; p.info = t.info; p.crc_tab = t.crc_tab; p.queue = h->d_queue;
+    p.N = N; p.n = t.n; p.K = K; p.c = t.c; p.D = D; p.L = h->L; p.M = t.M;
     p.nw = nw; p.snap_stride = sstride; p.sched_words = sched_words; p.cnt_words = cnt_words;
 
     int occ = 0;

@@ -116,20 +116,58 @@ __device__ __forceinline__ void top4_insert(unsigned long long key, unsigned lon
     }
 }
 
+// Stack entry packing: jsm = j (13 bits: decision-node ordinal = schedule
+// progress) | snapshot slot (8 bits, 0xFF none) << 13 |
+// flip mask relative to the snapshot (4 bits) << 21.
+__device__ __forceinline__ uint32_t jsm_j(uint32_t x) { return x & 0x1FFFu; }
+__device__ __forceinline__ uint32_t jsm_snap(uint32_t x) { return (x >> 13) & 0xFFu; }
+__device__ __forceinline__ uint32_t jsm_mask(uint32_t x) { return (x >> 21) & 0xFu; }
+__device__ __forceinline__ uint32_t jsm_make(uint32_t j, uint32_t snap, uint32_t mask) {
+    return j | (snap << 13) | (mask << 21);
+}
+constexpr uint32_t SNAP_NONE = 0xFFu;
+__device__ __forceinline__ int bitlen(uint32_t x) { return 32 - __clz(x); }
+
+// first free snapshot slot: not referenced by a live entry (except `skip`),
+// nor equal to `extra` (a slot still to be read)
+template <int SLOTS>
+__device__ __forceinline__ int alloc_snapshot(const uint32_t (&s_ser)[SLOTS], const uint32_t (&s_jsm)[SLOTS], int D,
+                                              int skip_lane, int skip_slot, uint32_t extra, int lane) {
+    int slot = -1;
+#pragma unroll
+    for (int w = 0; w < SLOTS; w++) {
+        uint32_t used = 0;
+#pragma unroll
+        for (int s = 0; s < SLOTS; s++) {
+            const uint32_t sn = jsm_snap(s_jsm[s]);
+            const bool skip = (lane == skip_lane && s == skip_slot);
+            if (s_ser[s] != EMPTY && !skip && sn != SNAP_NONE && (int)(sn >> 5) == w) used |= 1u << (sn & 31);
+        }
+        used = __reduce_or_sync(FULL, used);
+        if (extra != SNAP_NONE && (int)(extra >> 5) == w) used |= 1u << (extra & 31);
+        const int lim = D - w * 32;
+        uint32_t freem = ~used;
+        if (lim < 32) freem &= (1u << lim) - 1u;
+        if (slot < 0 && freem) slot = w * 32 + __ffs(freem) - 1;
+    }
+    return slot;
+}
+
 template <int SLOTS, bool SNAP_SMEM>
 __global__ void __launch_bounds__(kDecodeWarps * 32)
 fsscs_decode_kernel(const DecodeParams P) {
     extern __shared__ __align__(16) uint32_t smem[];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
-    const int N = P.N, n = P.n, K = P.K, D = P.D, nw = P.nw, nops = P.nops;
+    const int N = P.N, n = P.n, K = P.K, D = P.D, nw = P.nw, M = P.M;
 
-    // stage the schedule (read by every op) in shared memory when it fits
-    const uint32_t *ops = P.ops;
+    // node table (kind, lambda, phi of every decision node, schedule order) in
+    // shared memory when it fits: the schedule walk is derived from it
+    const uint32_t *nodes = P.nodes;
     if (P.sched_words > 0) {
-        for (int i = threadIdx.x; i < nops; i += blockDim.x) smem[i] = P.ops[i];
+        for (int i = threadIdx.x; i < M; i += blockDim.x) smem[i] = P.nodes[i];
         __syncthreads();
-        ops = smem;
+        nodes = smem;
     }
     uint32_t *wb = smem + P.sched_words + warp * P.warp_words;
     float *chan = reinterpret_cast<float *>(wb);
@@ -161,37 +199,36 @@ fsscs_decode_kernel(const DecodeParams P) {
         for (int i = lane; i < P.cnt_words; i += 32) reinterpret_cast<uint32_t *>(cnt)[i] = 0;
         __syncwarp();
 
-        // ---- stack: root path (PM 0, serial 0, k 0, j 0) ------------------
-        uint32_t s_pm[SLOTS], s_ser[SLOTS], s_kj[SLOTS], s_sm[SLOTS];
+        // ---- stack: root path (PM 0, serial 0, j 0) ------------------------
+        uint32_t s_pm[SLOTS], s_ser[SLOTS], s_jsm[SLOTS];
 #pragma unroll
-        for (int s = 0; s < SLOTS; s++) { s_pm[s] = EMPTY; s_ser[s] = EMPTY; s_kj[s] = 0; s_sm[s] = NO_SNAP; }
+        for (int s = 0; s < SLOTS; s++) { s_pm[s] = EMPTY; s_ser[s] = EMPTY; s_jsm[s] = jsm_make(0, SNAP_NONE, 0); }
         if (lane == 0) { s_pm[0] = 0u; s_ser[0] = 0u; }
         int nS = 1;
         uint32_t work = 0, next_serial = 1, pops = 0, switches = 0;
         int work_pl = 0;
+        // alpha memory content: stages s >= lev_mem hold the node (s, pos_mem >> s)
+        // for the working path's beta (partial-spine reuse, reading R12)
+        int pos_mem = 0, lev_mem = n;
         bool have_best = false;
         float best_pm = 0.f, out_pm = 0.f;
         int status = 0;
         bool from_best = false;
-        const uint32_t pop_cap = (uint32_t)P.L * (uint32_t)(P.M + 1);
+        const uint32_t pop_cap = (uint32_t)P.L * (uint32_t)(M + 1);
 
         for (;;) {
             if (nS == 0) { from_best = true; out_pm = best_pm; status = 1; break; }   // reading R13
             if (pops >= pop_cap) { status = 2; out_pm = -1.f; break; }   // watchdog: cannot happen (cnt[j] <= L)
             // ---- select: min (PM, serial) (reading R7)
-            uint32_t lpm = EMPTY, lser = EMPTY;
+            uint32_t lpm = EMPTY, lser = EMPTY, ljsm = 0;
             int ls = 0;
 #pragma unroll
             for (int s = 0; s < SLOTS; s++)
-                if (s_pm[s] < lpm || (s_pm[s] == lpm && s_ser[s] < lser)) { lpm = s_pm[s]; lser = s_ser[s]; ls = s; }
+                if (s_pm[s] < lpm || (s_pm[s] == lpm && s_ser[s] < lser)) { lpm = s_pm[s]; lser = s_ser[s]; ljsm = s_jsm[s]; ls = s; }
             uint32_t mpm, mser;
             warp_min_key(lpm, lser, mpm, mser);
             const int owner = __ffs(__ballot_sync(FULL, lpm == mpm && lser == mser)) - 1;
-            uint32_t mykj = 0, mysm = 0;
-#pragma unroll
-            for (int s = 0; s < SLOTS; s++) if (s == ls) { mykj = s_kj[s]; mysm = s_sm[s]; }
-            const uint32_t p_kj = __shfl_sync(FULL, mykj, owner);
-            const uint32_t p_sm = __shfl_sync(FULL, mysm, owner);
+            const uint32_t p_jsm = __shfl_sync(FULL, ljsm, owner);
             if (lane == owner) {
 #pragma unroll
                 for (int s = 0; s < SLOTS; s++) if (s == ls) { s_pm[s] = EMPTY; s_ser[s] = EMPTY; }
@@ -200,24 +237,32 @@ fsscs_decode_kernel(const DecodeParams P) {
             pops++;
             const float p_pm = __uint_as_float(mpm);
             const uint32_t p_ser = mser;
-            const int p_k = (int)(p_kj & 0xFFFFu), p_j = (int)(p_kj >> 16);
+            const int j = (int)jsm_j(p_jsm);
 
             // ---- per-length counter and prune (readings R9, R10)
-            const int c_j = (int)cnt[p_j] + 1;
+            const int c_j = (int)cnt[j] + 1;
             __syncwarp();
-            if (lane == 0) cnt[p_j] = (uint16_t)c_j;
+            if (lane == 0) cnt[j] = (uint16_t)c_j;
             if (c_j == P.L) {
                 int cntv = 0;
 #pragma unroll
                 for (int s = 0; s < SLOTS; s++) {
-                    if (s_ser[s] != EMPTY && (int)(s_kj[s] >> 16) <= p_j) { s_pm[s] = EMPTY; s_ser[s] = EMPTY; }
+                    if (s_ser[s] != EMPTY && (int)jsm_j(s_jsm[s]) <= j) { s_pm[s] = EMPTY; s_ser[s] = EMPTY; }
                     cntv += __popc(__ballot_sync(FULL, s_ser[s] != EMPTY));
                 }
                 nS = cntv;
             }
 
+            // position after the node that created p (its path length)
+            int pl = 0, plam = 0, pphi = 0, pkind = 0;
+            if (j > 0) {
+                const uint32_t pn = nodes[j - 1];
+                pkind = (int)op_kind(pn); plam = (int)op_lam(pn); pphi = (int)op_phi(pn);
+                pl = (pphi + 1) << plam;
+            }
+
             // ---- path switch ---------------------
-            bool dirty = false;
+            int s_d = 0;
             if (p_ser != work) {
                 switches++;
                 // the path being left keeps its beta in a snapshot if it is still live
@@ -227,55 +272,54 @@ fsscs_decode_kernel(const DecodeParams P) {
                 const uint32_t wb_ = __ballot_sync(FULL, wsl >= 0);
                 if (wb_) {
                     const int wl = __ffs(wb_) - 1;
-                    uint32_t wsm = 0;
+                    uint32_t wj = 0;
 #pragma unroll
-                    for (int s = 0; s < SLOTS; s++) if (s == wsl) wsm = s_sm[s];
-                    wsm = __shfl_sync(FULL, wsm, wl);
+                    for (int s = 0; s < SLOTS; s++) if (s == wsl) wj = s_jsm[s];
+                    wj = __shfl_sync(FULL, wj, wl);
                     const int wslot = __shfl_sync(FULL, wsl, wl);
-                    if ((wsm & 0xFFFFu) == NO_SNAP) {
-                        // allocate a free slot (not referenced by a live entry nor by p)
-                        int slot = -1;
-#pragma unroll
-                        for (int w = 0; w < SLOTS; w++) {
-                            uint32_t used = 0;
-#pragma unroll
-                            for (int s = 0; s < SLOTS; s++) {
-                                const uint32_t sn = s_sm[s] & 0xFFFFu;
-                                if (s_ser[s] != EMPTY && sn != NO_SNAP && (int)(sn >> 5) == w) used |= 1u << (sn & 31);
-                            }
-                            used = __reduce_or_sync(FULL, used);
-                            const uint32_t ps = p_sm & 0xFFFFu;
-                            if (ps != NO_SNAP && (int)(ps >> 5) == w) used |= 1u << (ps & 31);
-                            const int lim = D - w * 32;
-                            uint32_t freem = ~used;
-                            if (lim < 32) freem &= (1u << lim) - 1u;
-                            if (slot < 0 && freem) slot = w * 32 + __ffs(freem) - 1;
-                        }
+                    if (jsm_snap(wj) == SNAP_NONE) {
+                        const int slot = alloc_snapshot<SLOTS>(s_ser, s_jsm, D, -1, 0, jsm_snap(p_jsm), lane);
                         uint32_t *dst = snap + (size_t)slot * sstride;
                         const int nwords = (work_pl + 31) >> 5;
                         for (int w = lane; w < nwords; w += 32) dst[w] = beta[w];
                         if (lane == wl) {
 #pragma unroll
-                            for (int s = 0; s < SLOTS; s++) if (s == wslot) s_sm[s] = (uint32_t)slot;
+                            for (int s = 0; s < SLOTS; s++)
+                                if (s == wslot) s_jsm[s] = jsm_make(jsm_j(wj), (uint32_t)slot, 0);
                         }
                     }
                 }
-                // restore p's beta: fork snapshot + flip descriptor
-                const uint32_t ps = p_sm & 0xFFFFu, rel = p_sm >> 16;
-                const uint32_t nop = ops[p_k - 1];
-                const int nk = (int)op_kind(nop), nl = (int)op_lam(nop), nphi = (int)op_phi(nop);
-                const int p_pl = (nphi + 1) << nl;
+                // restore p's beta (fork snapshot), locating the first bit d where it
+                // differs from the beta the alpha memory was computed from
+                const uint32_t ps = jsm_snap(p_jsm), rel = jsm_mask(p_jsm);
                 const uint32_t *src = snap + (size_t)ps * sstride;
-                const int nwords = (p_pl + 31) >> 5;
-                for (int w = lane; w < nwords; w += 32) beta[w] = SNAP_SMEM ? src[w] : __ldcg(src + w);
+                const int nwords = (pl + 31) >> 5;
+                int d = 0x7FFFFFFF;
+                for (int w0 = 0; w0 < nwords; w0 += 32) {
+                    const int w = w0 + lane;
+                    uint32_t x = 0;
+                    if (w < nwords) {
+                        const uint32_t nv = SNAP_SMEM ? src[w] : __ldcg(src + w);
+                        x = nv ^ beta[w];
+                        if (w == nwords - 1 && (pl & 31)) x &= (1u << (pl & 31)) - 1u;
+                        beta[w] = nv;
+                    }
+                    const uint32_t b = __ballot_sync(FULL, x != 0);
+                    if (b && d == 0x7FFFFFFF) {
+                        const int fl = __ffs(b) - 1;
+                        const uint32_t xv = __shfl_sync(FULL, x, fl);
+                        d = 32 * (w0 + fl) + __ffs(xv) - 1;
+                    }
+                }
+                if (pl > d) s_d = bitlen((uint32_t)pl ^ (uint32_t)d);
                 __syncwarp();
                 if (rel != 0u) {
-                    const int seg = nphi << nl, Lam = 1 << nl;
-                    if (nk == OP_REP) {
+                    const int seg = pphi << plam, Lam = 1 << plam;
+                    if (pkind == OP_REP) {
                         if (Lam >= 32) {
                             for (int t = lane; t < (Lam >> 5); t += 32) beta[(seg >> 5) + t] ^= FULL;
                         } else if (lane == 0) {
-                            beta[seg >> 5] ^= ((Lam == 32) ? FULL : ((1u << Lam) - 1u)) << (seg & 31);
+                            beta[seg >> 5] ^= ((1u << Lam) - 1u) << (seg & 31);
                         }
                     } else if (lane == 0) {
                         const uint32_t h0 = SNAP_SMEM ? src[nw] : __ldcg(src + nw);
@@ -291,29 +335,19 @@ fsscs_decode_kernel(const DecodeParams P) {
                     __syncwarp();
                 }
                 work = p_ser;
-                work_pl = p_pl;
-                dirty = true;
+            }
+            work_pl = pl;
+
+            // ---- pending BETA ops of p: climb from its
+            // last node while it is a right child
+            int l = n;
+            if (j > 0) {
+                int ph = pphi;
+                l = plam;
+                while (ph & 1) { beta_op(beta, l, ph, lane); ph >>= 1; l++; }
             }
 
-            // ---- continue the schedule from the stored progress
-            int k = p_k;
-            for (; k < nops; k++) {
-                const uint32_t op = ops[k];
-                const uint32_t kind = op_kind(op);
-                if (kind >= OP_R0) break;
-                const int lam = (int)op_lam(op), phi = (int)op_phi(op);
-                if (kind == OP_BETA) {
-                    beta_op(beta, lam, phi, lane);
-                } else {
-                    if (dirty) {                      // Alg. 4: spine from the root
-                        for (int s = n - 1; s > lam; s--) alpha_stage(chan, alpha, beta, n, s, phi >> (s - lam), lane);
-                        dirty = false;
-                    }
-                    alpha_stage(chan, alpha, beta, n, lam, phi, lane);
-                }
-            }
-
-            if (k == nops) {
+            if (j == M) {
                 // ---- complete path: CRC on the systematic bits
                 bool ok = true;
                 if (P.c > 0) {
@@ -335,9 +369,19 @@ fsscs_decode_kernel(const DecodeParams P) {
                 continue;
             }
 
+            // ---- ALPHA ops down to node j (Eq. 4, Alg. 1 / Alg. 4): stage s
+            // holds node (s, pl >> s); stages >= s_min are still valid
+            const uint32_t nd = nodes[j];
+            const int kind = (int)op_kind(nd), lam = (int)op_lam(nd), phi = (int)op_phi(nd);
+            {
+                int s_min = max(max(lev_mem, bitlen((uint32_t)(pos_mem ^ pl))), max(s_d, l + 1));
+                s_min = min(s_min, n);
+                for (int s = s_min - 1; s >= lam; s--) alpha_stage(chan, alpha, beta, n, s, pl >> s, lane);
+                pos_mem = pl;
+                lev_mem = lam + 1;
+            }
+
             // ---- decision node ----------
-            const uint32_t op = ops[k];
-            const int kind = (int)op_kind(op), lam = (int)op_lam(op), phi = (int)op_phi(op);
             const int Lam = 1 << lam;
             const int seg = phi << lam;
             float *a = (lam == n) ? chan : alpha + Lam;
@@ -347,12 +391,10 @@ fsscs_decode_kernel(const DecodeParams P) {
                 __syncwarp();
                 a = alpha;
             }
-            float dpm[8];
-            int msk[8];
-            int nc = 1;
+            // candidate t lives in lane t: (dpm, mask) and its rank in (dPM, mask) order
+            float my_dpm = 0.f;
+            int my_mask = 0, my_rank = 0, nc = 1;
             uint32_t mi[4] = {0, 0, 0, 0};
-#pragma unroll
-            for (int t = 0; t < 8; t++) { dpm[t] = 0.f; msk[t] = t; }
 
             if (kind == OP_R0 || kind == OP_REP) {
                 // tree-order sums T(neg(a)) and T(pos(a)) (reading R3)
@@ -389,11 +431,13 @@ fsscs_decode_kernel(const DecodeParams P) {
                 vn = __shfl_sync(FULL, vn, 0);
                 vp = __shfl_sync(FULL, vp, 0);
                 if (!rep) {
-                    nc = 1; dpm[0] = vn; msk[0] = 0;
+                    nc = 1; my_dpm = vn;
                 } else {
                     nc = 2;
-                    if (vp < vn) { dpm[0] = vp; msk[0] = 1; dpm[1] = vn; msk[1] = 0; }
-                    else         { dpm[0] = vn; msk[0] = 0; dpm[1] = vp; msk[1] = 1; }
+                    my_dpm = (lane == 0) ? vn : vp;
+                    my_mask = lane & 1;
+                    const bool ones_first = vp < vn;           // ties: zeros first
+                    my_rank = (lane == 0) ? (ones_first ? 1 : 0) : (ones_first ? 0 : 1);
                 }
             } else {
                 // R1 / SPC: hard-decision word, parity, least reliable positions
@@ -419,9 +463,7 @@ fsscs_decode_kernel(const DecodeParams P) {
                 par &= 1u;
                 float A[4] = {0.f, 0.f, 0.f, 0.f};
                 if (Lam == 1) {
-                    // R1 at Lambda = 1: HD and its flip (reading R6)
-                    A[0] = fabsf(a[0]);
-                    mi[0] = 0;
+                    A[0] = fabsf(a[0]);                       // R1 at Lambda = 1 (reading R6)
                 } else {
 #pragma unroll
                     for (int r = 0; r < 4; r++) {
@@ -436,54 +478,53 @@ fsscs_decode_kernel(const DecodeParams P) {
                 }
                 if (kind == OP_R1) {
                     if (Lam == 1) {
-                        nc = 2; dpm[0] = 0.f; msk[0] = 0; dpm[1] = A[0]; msk[1] = 1;
+                        nc = 2; my_mask = lane & 1; my_dpm = (lane == 1) ? A[0] : 0.f; my_rank = lane;
                     } else {
-                        nc = 4;   // Chase-II: order (0, m1, m2, m1+m2) is already sorted
-                        dpm[0] = 0.f; msk[0] = 0;
-                        dpm[1] = A[0]; msk[1] = 1;
-                        dpm[2] = A[1]; msk[2] = 2;
-                        dpm[3] = A[0] + A[1]; msk[3] = 3;
+                        // Chase-II: (0, m1, m2, m1+m2) is already in (dPM, mask) order
+                        nc = 4; my_mask = lane & 3; my_rank = lane;
+                        my_dpm = (my_mask == 0) ? 0.f : (my_mask == 1) ? A[0] : (my_mask == 2) ? A[1] : A[0] + A[1];
                     }
                 } else {
-                    // SPC: the 8 flip sets S of {m1..m4} with |S| = parity (mod 2), mask order
+                    // SPC: the 8 flip sets S of {m1..m4} with |S| = parity (mod 2)
                     nc = 8;
-                    constexpr int kEven[8] = {0, 3, 5, 6, 9, 10, 12, 15};
-                    constexpr int kOdd[8] = {1, 2, 4, 7, 8, 11, 13, 14};
+                    const uint32_t table = par ? 0xEDB87421u : 0xFCA96530u;   // masks in ascending order
+                    my_mask = (int)((table >> (4 * (lane & 7))) & 15u);
+                    float dsum = 0.f;
+                    bool first = true;
 #pragma unroll
-                    for (int t = 0; t < 8; t++) {
-                        const int s = par ? kOdd[t] : kEven[t];
-                        float d = 0.f;
-                        bool first = true;
+                    for (int q = 0; q < 4; q++)
+                        if ((my_mask >> q) & 1) { dsum = first ? A[q] : dsum + A[q]; first = false; }
+                    my_dpm = dsum;
+                    // rank = #{u : (dpm_u, mask_u) < (dpm_t, mask_t)}: pairwise compares, 32 per round
+                    const int u = lane & 7;
+                    const float du = __shfl_sync(FULL, my_dpm, u);
+                    const int mu = __shfl_sync(FULL, my_mask, u);
+                    uint32_t bal[2];
 #pragma unroll
-                        for (int q = 0; q < 4; q++)
-                            if ((s >> q) & 1) { d = first ? A[q] : d + A[q]; first = false; }
-                        dpm[t] = d;
-                        msk[t] = s;
+                    for (int rnd = 0; rnd < 2; rnd++) {
+                        const int t = (lane >> 3) + 4 * rnd;
+                        const float dt_ = __shfl_sync(FULL, my_dpm, t);
+                        const int mt_ = __shfl_sync(FULL, my_mask, t);
+                        bal[rnd] = __ballot_sync(FULL, du < dt_ || (du == dt_ && mu < mt_));
                     }
-                    // stable sort by dPM (ties keep mask order)
-#pragma unroll
-                    for (int i = 0; i < 7; i++)
-#pragma unroll
-                        for (int j = 0; j < 7 - i; j++)
-                            if (dpm[j] > dpm[j + 1]) {
-                                const float td = dpm[j]; dpm[j] = dpm[j + 1]; dpm[j + 1] = td;
-                                const int tm = msk[j]; msk[j] = msk[j + 1]; msk[j + 1] = tm;
-                            }
+                    const uint32_t bb = (lane < 4) ? bal[0] : bal[1];
+                    my_rank = __popc((bb >> (8 * (lane & 3))) & 0xFFu);
                 }
-                if (Lam < 32) {
-                    // HD word of the node (Lam < 32 bits) into beta, c1's flips applied below
-                    if (lane == 0) {
-                        const uint32_t lm = (1u << Lam) - 1u;
-                        const int w = seg >> 5, o = seg & 31;
-                        beta[w] = (beta[w] & ~(lm << o)) | ((hdw & lm) << o);
-                    }
+                if (Lam < 32 && lane == 0) {
+                    // HD word of the node (Lam < 32 bits) into beta; c1's flips applied below
+                    const uint32_t lm = (1u << Lam) - 1u;
+                    const int w = seg >> 5, o = seg & 31;
+                    beta[w] = (beta[w] & ~(lm << o)) | ((hdw & lm) << o);
                 }
                 __syncwarp();
             }
+            const bool is_cand = lane < nc;
 
             // ---- c1 continues in the working memory ------------------------
+            const int c1l = __ffs(__ballot_sync(FULL, is_cand && my_rank == 0)) - 1;
+            const float dpm1 = __shfl_sync(FULL, my_dpm, c1l);
+            const int m0 = __shfl_sync(FULL, my_mask, c1l);
             {
-                const int m0 = msk[0];
                 if (kind == OP_R0 || kind == OP_REP) {
                     const uint32_t fill = (kind == OP_REP && m0) ? FULL : 0u;
                     if (Lam >= 32) {
@@ -502,10 +543,9 @@ fsscs_decode_kernel(const DecodeParams P) {
                 }
                 __syncwarp();
             }
-            const int kn = k + 1, jn = p_j + 1, pl = (phi + 1) << lam;
+            const int jn = j + 1, npl = (phi + 1) << lam;
             const uint32_t ser0 = next_serial;
             next_serial += (uint32_t)nc;
-            const uint32_t kj_new = (uint32_t)kn | ((uint32_t)jn << 16);
 
             // insert c1 into a free entry (p's was freed, reading R8)
             int c1_lane = 0, c1_slot = 0;
@@ -517,22 +557,23 @@ fsscs_decode_kernel(const DecodeParams P) {
                     if (!placed && fb) {
                         c1_lane = __ffs(fb) - 1; c1_slot = s; placed = true;
                         if (lane == c1_lane) {
-                            s_pm[s] = __float_as_uint(p_pm + dpm[0]); s_ser[s] = ser0; s_kj[s] = kj_new; s_sm[s] = NO_SNAP;
+                            s_pm[s] = __float_as_uint(p_pm + dpm1); s_ser[s] = ser0; s_jsm[s] = jsm_make(jn, SNAP_NONE, 0);
                         }
                     }
                 }
                 nS++;
             }
             work = ser0;
-            work_pl = pl;
+            work_pl = npl;
 
-            // siblings c2..: insert if room, else replace the least reliable iff
-            // strictly better; they share one fork snapshot.
+            // siblings in rank order: insert if room, else replace the least
+            // reliable iff strictly better.  Ranks ascend, so the
+            // first one dropped ends the loop.  They share one fork snapshot.
             int fslot = -1;
-            for (int t = 1; t < nc; t++) {
-                float dt = 0.f; int mt = 0;
-#pragma unroll
-                for (int q = 1; q < 8; q++) if (q == t) { dt = dpm[q]; mt = msk[q]; }
+            for (int r = 1; r < nc; r++) {
+                const int ol = __ffs(__ballot_sync(FULL, is_cand && my_rank == r)) - 1;
+                const float dt = __shfl_sync(FULL, my_dpm, ol);
+                const int mt = __shfl_sync(FULL, my_mask, ol);
                 const uint32_t cpm = __float_as_uint(p_pm + dt);
                 int tl = -1, ts = 0;
                 if (nS < D) {
@@ -549,34 +590,16 @@ fsscs_decode_kernel(const DecodeParams P) {
                     for (int s = 0; s < SLOTS; s++)
                         if (s_ser[s] != EMPTY && (s_pm[s] > xpm || (s_pm[s] == xpm && s_ser[s] >= xser))) { xpm = s_pm[s]; xser = s_ser[s]; xs = s; }
                     const uint32_t Mpm = __reduce_max_sync(FULL, xpm);
+                    if (cpm >= Mpm) break;                      // dropped, and so are the rest
                     const uint32_t Mser = __reduce_max_sync(FULL, xpm == Mpm ? xser : 0u);
-                    if (cpm < Mpm) {
-                        tl = __ffs(__ballot_sync(FULL, xpm == Mpm && xser == Mser)) - 1;
-                        ts = __shfl_sync(FULL, xs, tl);
-                    }
+                    tl = __ffs(__ballot_sync(FULL, xpm == Mpm && xser == Mser)) - 1;
+                    ts = __shfl_sync(FULL, xs, tl);
                 }
-                if (tl < 0) continue;                    // dropped
                 if (fslot < 0) {
-                    // fork snapshot: beta prefix [0, pl) with c1's segment + m1..m4
-                    int slot = -1;
-#pragma unroll
-                    for (int w = 0; w < SLOTS; w++) {
-                        uint32_t used = 0;
-#pragma unroll
-                        for (int s = 0; s < SLOTS; s++) {
-                            const uint32_t sn = s_sm[s] & 0xFFFFu;
-                            const bool victim = (lane == tl && s == ts);
-                            if (s_ser[s] != EMPTY && !victim && sn != NO_SNAP && (int)(sn >> 5) == w) used |= 1u << (sn & 31);
-                        }
-                        used = __reduce_or_sync(FULL, used);
-                        const int lim = D - w * 32;
-                        uint32_t freem = ~used;
-                        if (lim < 32) freem &= (1u << lim) - 1u;
-                        if (slot < 0 && freem) slot = w * 32 + __ffs(freem) - 1;
-                    }
-                    fslot = slot;
-                    uint32_t *dst = snap + (size_t)slot * sstride;
-                    const int nwords = (pl + 31) >> 5;
+                    // fork snapshot: beta prefix [0, npl) with c1's segment + m1..m4
+                    fslot = alloc_snapshot<SLOTS>(s_ser, s_jsm, D, tl, ts, SNAP_NONE, lane);
+                    uint32_t *dst = snap + (size_t)fslot * sstride;
+                    const int nwords = (npl + 31) >> 5;
                     for (int w = lane; w < nwords; w += 32) dst[w] = beta[w];
                     if (lane == 0) {
                         dst[nw] = mi[0] | (mi[1] << 16);
@@ -587,14 +610,14 @@ fsscs_decode_kernel(const DecodeParams P) {
 #pragma unroll
                     for (int s = 0; s < SLOTS; s++)
                         if (s == ts) {
-                            s_pm[s] = cpm; s_ser[s] = ser0 + (uint32_t)t; s_kj[s] = kj_new;
-                            s_sm[s] = (uint32_t)fslot | ((uint32_t)(mt ^ msk[0]) << 16);
+                            s_pm[s] = cpm; s_ser[s] = ser0 + (uint32_t)r;
+                            s_jsm[s] = jsm_make(jn, (uint32_t)fslot, (uint32_t)(mt ^ m0));
                         }
                 }
             }
             if (fslot >= 0 && lane == c1_lane) {
 #pragma unroll
-                for (int s = 0; s < SLOTS; s++) if (s == c1_slot) s_sm[s] = (uint32_t)fslot;
+                for (int s = 0; s < SLOTS; s++) if (s == c1_slot) s_jsm[s] = jsm_make(jn, (uint32_t)fslot, 0);
             }
         }
 

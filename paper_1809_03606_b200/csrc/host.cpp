@@ -116,7 +116,9 @@ int build_host_code(int N, int K, const uint8_t *frozen, uint32_t crc_poly, bool
         }
     } rec{hc, node_kind};
     rec(n, 0);
-    if (hc.ops.size() > 65535) return POLAR_EINVAL;
+    if (hc.ops.size() > 65535 || hc.M > 8191) return POLAR_EINVAL;
+    for (uint32_t op : hc.ops)
+        if (op_kind(op) >= OP_R0) hc.nodes.push_back(op);
 
     // CRC syndrome table: block bit k < P = K-c is the
     // payload coefficient of x^(P-1-k); its contribution to the remainder of

@@ -28,7 +28,7 @@ struct CodeTables {
     int N = 0, n = 0, K = 0, c = 0, M = 0;
     uint32_t crc_poly = 0;
     bool systematic_ok = false;
-    uint32_t *ops = nullptr;  int nops = 0;     // schedule
+    uint32_t *nodes = nullptr;  int nops = 0;   // decision nodes (kind, lambda, phi) in schedule order
     uint16_t *info = nullptr;                   // A ascending, [K]
     uint32_t *crc_tab = nullptr;                // [K] syndrome contribution of block bit k
     uint32_t *info_words = nullptr;             // [max(1,N/32)] bit i set iff i in A
@@ -42,15 +42,15 @@ struct DecodeParams {
     float *pm;
     uint32_t *pops, *switches;
     uint8_t *status;
-    const uint32_t *ops;
+    const uint32_t *nodes;      // [M] node records; the BETA/ALPHA walk between them is implied
     const uint16_t *info;
     const uint32_t *crc_tab;
     unsigned long long *queue;
     uint32_t *snap_global;      // arena when snapshots live in global memory
-    int N, n, K, c, D, L, M, nops;
+    int N, n, K, c, D, L, M;
     int nw;                     // beta words = max(1, N/32)
     int snap_stride;            // words per snapshot slot = nw + 2 (header: m1..m4)
-    int sched_words;            // schedule words staged in shared memory (0 = read global)
+    int sched_words;            // node-table words staged in shared memory (0 = read global)
     int warp_words;             // shared-memory words per warp
     int cnt_words;              // words of the per-length counters (u16 each)
 };
@@ -98,7 +98,8 @@ struct HostCode {
     int N = 0, n = 0, K = 0, c = 0, M = 0;
     uint32_t crc_poly = 0;
     bool systematic_ok = false;
-    std::vector<uint32_t> ops;
+    std::vector<uint32_t> ops;      // full FSSC schedule (ALPHA/BETA/nodes), Fig. 5
+    std::vector<uint32_t> nodes;    // its decision nodes only
     std::vector<uint16_t> info;
     std::vector<uint32_t> crc_tab;
     std::vector<uint32_t> info_words;
