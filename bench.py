@@ -48,6 +48,9 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--snap-global", action="store_true")
+    ap.add_argument("--snap-smem", action="store_true")
+    ap.add_argument("--chan-global", action="store_true")
+    ap.add_argument("--chan-smem", action="store_true")
     return ap.parse_args()
 
 
@@ -197,7 +200,8 @@ def run_ours(args, cfg, c):
     npts = len(c["ebno"])
     frames = nf * npts
     fr = P.bhattacharyya_mask(c["N"], c["K"], c["design_db"])
-    dec = P.PolarSCS(fr, c["D"], c["L"], c["crc_poly"], snap_global=args.snap_global)
+    dec = P.PolarSCS(fr, c["D"], c["L"], c["crc_poly"], snap_global=args.snap_global, snap_smem=args.snap_smem,
+                     chan_global=args.chan_global, chan_smem=args.chan_smem)
     K, N = c["K"], c["N"]
 
     # inputs: device generator, each rank its own frame range; all points share
@@ -331,7 +335,8 @@ def run_ours(args, cfg, c):
         "config": {"workload": workload_name(cfg, c), "frames_per_step_per_gpu": frames,
                    "l2": f"inputs {frames * N * 4 / 1e9:.2f} GB per step > 126 MB L2 (no flush needed)",
                    "launch": {"ctas": info["ctas"], "warps_per_cta": info["warps_per_cta"],
-                              "smem_per_cta": info["smem_per_cta"], "snap_in_smem": info["snap_in_smem"]}},
+                              "smem_per_cta": info["smem_per_cta"], "snap_in_smem": info["snap_in_smem"],
+                              "chan_in_smem": info["chan_in_smem"]}},
         "frames_per_s": world * frames / (ms_per_step / 1e3),
         "frames_per_s_per_gpu": fps_rank,
         "roofline": roofline,

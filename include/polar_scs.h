@@ -46,6 +46,10 @@ extern "C" {
                                           */
 #define POLAR_FLAG_SNAP_GLOBAL  0x2u  /* force the path-snapshot arena into
                                          global memory (L2) instead of shared */
+#define POLAR_FLAG_CHAN_GLOBAL  0x4u  /* read the channel LLR row through L1/L2
+                                         instead of staging it in shared memory */
+#define POLAR_FLAG_SNAP_SMEM    0x8u  /* force snapshots into shared memory */
+#define POLAR_FLAG_CHAN_SMEM    0x10u /* force channel staging in shared memory */
 
 typedef struct polar_scs_s *polar_scs_t;
 
@@ -56,6 +60,7 @@ typedef struct {
     int32_t num_nodes;        /* M = decision nodes in the schedule               */
     int32_t warps_per_cta, ctas, smem_per_cta;  /* decode launch configuration   */
     int32_t snap_in_smem;     /* 1: path snapshots in shared memory, 0: global    */
+    int32_t chan_in_smem;     /* 1: channel row staged in shared memory           */
     int32_t systematic_ok;    /* 1 if the mask is systematic-encodable            */
     uint32_t flags;
 } polar_scs_info_t;

@@ -12,8 +12,9 @@
 #include "internal.h"
 
 namespace polar {
-cudaError_t launch_decode(const DecodeParams &p, int slots, bool snap_smem, int ctas, int smem, cudaStream_t st);
-cudaError_t decode_occupancy(int slots, bool snap_smem, int smem, int *blocks_per_sm);
+cudaError_t launch_decode(const DecodeParams &p, int slots, bool snap_smem, bool chan_smem, int ctas, int smem,
+                          cudaStream_t st);
+cudaError_t decode_occupancy(int slots, bool snap_smem, bool chan_smem, int smem, int *blocks_per_sm);
 cudaError_t launch_crc_attach(const CodecParams &p, cudaStream_t st);
 cudaError_t launch_encode(const CodecParams &p, cudaStream_t st);
 cudaError_t launch_modulate(const CodecParams &p, cudaStream_t st);
@@ -72,7 +73,8 @@ int decode_impl(polar_scs_t h, const float *llr, int64_t n, uint8_t *bits, float
     p.pm = pm; p.pops = pops; p.switches = sw; p.status = status;
     cudaError_t e = cudaMemsetAsync(h->d_queue, 0, sizeof(unsigned long long), st);
     if (e != cudaSuccess) return cuda_status(e);
-    return cuda_status(launch_decode(p, slots_for(h->D), h->snap_in_smem != 0, h->ctas, h->smem_per_cta, st));
+    return cuda_status(launch_decode(p, slots_for(h->D), h->snap_in_smem != 0, h->chan_in_smem != 0, h->ctas,
+                                     h->smem_per_cta, st));
 }
 
 }  // namespace
@@ -94,7 +96,11 @@ int polar_scs_create_ex(polar_scs_t *out, int32_t N, int32_t K, const uint8_t *f
                         uint32_t crc_poly, uint32_t flags) {
     if (!out) return POLAR_EINVAL;
     *out = nullptr;
-    if (D < 1 || D > kMaxD || L < 1 || (flags & ~(POLAR_FLAG_BIT_LEVEL | POLAR_FLAG_SNAP_GLOBAL))) return POLAR_EINVAL;
+    const uint32_t known = POLAR_FLAG_BIT_LEVEL | POLAR_FLAG_SNAP_GLOBAL | POLAR_FLAG_CHAN_GLOBAL |
+                           POLAR_FLAG_SNAP_SMEM | POLAR_FLAG_CHAN_SMEM;
+    if (D < 1 || D > kMaxD || L < 1 || (flags & ~known)) return POLAR_EINVAL;
+    if ((flags & POLAR_FLAG_SNAP_GLOBAL) && (flags & POLAR_FLAG_SNAP_SMEM)) return POLAR_EINVAL;
+    if ((flags & POLAR_FLAG_CHAN_GLOBAL) && (flags & POLAR_FLAG_CHAN_SMEM)) return POLAR_EINVAL;
     HostCode hc;
     int rc = build_host_code(N, K, frozen_mask, crc_poly, (flags & POLAR_FLAG_BIT_LEVEL) != 0, hc);
     if (rc != POLAR_OK) return rc;
@@ -123,7 +129,6 @@ int polar_scs_create_ex(polar_scs_t *out, int32_t N, int32_t K, const uint8_t *f
     const int nw = std::max(1, N / 32);
     const int cnt_words = ((t.M + 1) * 2 + 3) / 4;
     const int sstride = nw + 2;
-    const int base_words = 2 * N + 2 * nw + cnt_words;
     const int sched_words = (t.M * 4 <= 16384) ? round4(t.M) : 0;
     const int slots = slots_for(D);
 
@@ -132,26 +137,38 @@ int polar_scs_create_ex(polar_scs_t *out, int32_t N, int32_t K, const uint8_t *f
     p.N = N; p.n = t.n; p.K = K; p.c = t.c; p.D = D; p.L = h->L; p.M = t.M;
     p.nw = nw; p.snap_stride = sstride; p.sched_words = sched_words; p.cnt_words = cnt_words;
 
-    int occ = 0;
-    bool use_smem = false;
-    if (!(flags & POLAR_FLAG_SNAP_GLOBAL)) {
-        const int ww = round4(base_words + D * sstride);
-        const int smem = 4 * (sched_words + kDecodeWarps * ww);
-        if (smem <= optin && decode_occupancy(slots, true, smem, &occ) == cudaSuccess && occ * kDecodeWarps >= 16) {
-            use_smem = true;
-            p.warp_words = ww;
-            h->smem_per_cta = smem;
+    // Layout choice: per warp, alpha stages >= 6 (N floats incl. scratch), flat
+    // beta, best-effort beta and counters always live in shared memory; the
+    // channel row and the snapshot arena go to shared memory or L1/L2.  Among
+    // the allowed placements take the one with the most resident warps per SM;
+    // ties prefer shared memory.
+    int best_occ = -1, best_smem = 0, best_ww = 0;
+    bool best_snap = false, best_chan = false;
+    for (int ci = 0; ci < 2; ci++) {
+        const bool chan_smem = (ci == 0);
+        if (chan_smem && (flags & POLAR_FLAG_CHAN_GLOBAL)) continue;
+        if (!chan_smem && (flags & POLAR_FLAG_CHAN_SMEM)) continue;
+        for (int si = 0; si < 2; si++) {
+            const bool snap_smem = (si == 0);
+            if (snap_smem && (flags & POLAR_FLAG_SNAP_GLOBAL)) continue;
+            if (!snap_smem && (flags & POLAR_FLAG_SNAP_SMEM)) continue;
+            const int ww = round4((chan_smem ? N : 0) + N + 2 * nw + cnt_words + (snap_smem ? D * sstride : 0));
+            const int smem = 4 * (sched_words + kDecodeWarps * ww);
+            if (smem > optin) continue;
+            int occ = 0;
+            if (decode_occupancy(slots, snap_smem, chan_smem, smem, &occ) != cudaSuccess || occ < 1) continue;
+            if (occ > best_occ) {
+                best_occ = occ; best_smem = smem; best_ww = ww; best_snap = snap_smem; best_chan = chan_smem;
+            }
         }
     }
-    if (!use_smem) {
-        const int ww = round4(base_words);
-        const int smem = 4 * (sched_words + kDecodeWarps * ww);
-        if (smem > optin) { free_handle(h); return POLAR_EINVAL; }
-        e = decode_occupancy(slots, false, smem, &occ);
-        if (e != cudaSuccess || occ < 1) { free_handle(h); return e != cudaSuccess ? cuda_status(e) : POLAR_EINVAL; }
-        p.warp_words = ww;
-        h->smem_per_cta = smem;
-    }
+    cudaGetLastError();
+    if (best_occ < 1) { free_handle(h); return POLAR_EINVAL; }
+    const int occ = best_occ;
+    const bool use_smem = best_snap;
+    p.warp_words = best_ww;
+    h->smem_per_cta = best_smem;
+    h->chan_in_smem = best_chan ? 1 : 0;
     cudaGetLastError();
     h->snap_in_smem = use_smem ? 1 : 0;
     h->warps_per_cta = kDecodeWarps;
@@ -182,7 +199,7 @@ int polar_scs_get_info(polar_scs_t h, polar_scs_info_t *o) {
     o->N = h->t.N; o->n = h->t.n; o->K = h->t.K; o->crc_bits = h->t.c; o->D = h->D; o->L = h->L;
     o->num_ops = h->t.nops; o->num_nodes = h->t.M;
     o->warps_per_cta = h->warps_per_cta; o->ctas = h->ctas; o->smem_per_cta = h->smem_per_cta;
-    o->snap_in_smem = h->snap_in_smem; o->systematic_ok = h->t.systematic_ok ? 1 : 0; o->flags = h->flags;
+    o->snap_in_smem = h->snap_in_smem; o->chan_in_smem = h->chan_in_smem; o->systematic_ok = h->t.systematic_ok ? 1 : 0; o->flags = h->flags;
     return POLAR_OK;
 }
 

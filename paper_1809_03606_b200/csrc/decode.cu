@@ -39,32 +39,49 @@ __device__ __forceinline__ float g_exact(float lo, float hi, uint32_t bit) {
 __device__ __forceinline__ float negpart(float x) { return x < 0.f ? -x : 0.f; }
 __device__ __forceinline__ float pospart(float x) { return x < 0.f ? 0.f : x; }
 
-// ALPHA(s, psi): alpha_s from alpha_{s+1} (Eq. 4, Alg. 1).  Stage s lives at
-// alpha[2^s, 2^{s+1}); stage n is the channel row.
+// ALPHA(s, psi): alpha_s from alpha_{s+1} (Eq. 4, Alg. 1) for stages s >= 6
+// (Lambda >= 64) held in shared memory at alpha[2^s, 2^{s+1}).  Stage n is the
+// channel row: shared memory (CHAN_SMEM) or the LLR input read through L1/L2.
+template <bool CHAN_SMEM>
+__device__ __forceinline__ float4 ld4(const float *p, bool top) {
+    if (!CHAN_SMEM && top) return __ldg(reinterpret_cast<const float4 *>(p));
+    return *reinterpret_cast<const float4 *>(p);
+}
+template <bool CHAN_SMEM>
+__device__ __forceinline__ float ld1(const float *p, bool top) {
+    if (!CHAN_SMEM && top) return __ldg(p);
+    return *p;
+}
+
+template <bool CHAN_SMEM>
 __device__ __forceinline__ void alpha_stage(const float *chan, float *alpha, const uint32_t *beta,
                                             int n, int s, int psi, int lane) {
     const int Ls = 1 << s;
-    const float *src = (s + 1 == n) ? chan : alpha + (2 << s);
+    const bool top = (s + 1 == n);
+    const float *src = top ? chan : alpha + (2 << s);
     float *dst = alpha + Ls;
     if ((psi & 1) == 0) {
         if (Ls >= 128) {
+            #pragma unroll 1
             for (int i = lane * 4; i < Ls; i += 128) {
-                const float4 lo = *reinterpret_cast<const float4 *>(src + i);
-                const float4 hi = *reinterpret_cast<const float4 *>(src + Ls + i);
+                const float4 lo = ld4<CHAN_SMEM>(src + i, top);
+                const float4 hi = ld4<CHAN_SMEM>(src + Ls + i, top);
                 float4 o;
                 o.x = f_minsum(lo.x, hi.x); o.y = f_minsum(lo.y, hi.y);
                 o.z = f_minsum(lo.z, hi.z); o.w = f_minsum(lo.w, hi.w);
                 *reinterpret_cast<float4 *>(dst + i) = o;
             }
         } else {
-            for (int i = lane; i < Ls; i += 32) dst[i] = f_minsum(src[i], src[i + Ls]);
+            #pragma unroll 1
+            for (int i = lane; i < Ls; i += 32) dst[i] = f_minsum(ld1<CHAN_SMEM>(src + i, top), ld1<CHAN_SMEM>(src + i + Ls, top));
         }
     } else {
         const int boff = (psi - 1) * Ls;            // left sibling's segment of the flat beta
         if (Ls >= 128) {
+            #pragma unroll 1
             for (int i = lane * 4; i < Ls; i += 128) {
-                const float4 lo = *reinterpret_cast<const float4 *>(src + i);
-                const float4 hi = *reinterpret_cast<const float4 *>(src + Ls + i);
+                const float4 lo = ld4<CHAN_SMEM>(src + i, top);
+                const float4 hi = ld4<CHAN_SMEM>(src + Ls + i, top);
                 const uint32_t b = beta[(boff + i) >> 5] >> ((boff + i) & 31);
                 float4 o;
                 o.x = g_exact(lo.x, hi.x, b & 1); o.y = g_exact(lo.y, hi.y, (b >> 1) & 1);
@@ -72,9 +89,10 @@ __device__ __forceinline__ void alpha_stage(const float *chan, float *alpha, con
                 *reinterpret_cast<float4 *>(dst + i) = o;
             }
         } else {
+            #pragma unroll 1
             for (int i = lane; i < Ls; i += 32) {
                 const int p = boff + i;
-                dst[i] = g_exact(src[i], src[i + Ls], (beta[p >> 5] >> (p & 31)) & 1);
+                dst[i] = g_exact(ld1<CHAN_SMEM>(src + i, top), ld1<CHAN_SMEM>(src + i + Ls, top), (beta[p >> 5] >> (p & 31)) & 1);
             }
         }
     }
@@ -86,6 +104,7 @@ __device__ __forceinline__ void beta_op(uint32_t *beta, int lam, int phi, int la
     const int Lam = 1 << lam;
     if (Lam >= 32) {
         const int wd = ((phi - 1) * Lam) >> 5, ws = (phi * Lam) >> 5, nwd = Lam >> 5;
+        #pragma unroll 1
         for (int t = lane; t < nwd; t += 32) beta[wd + t] ^= beta[ws + t];
     } else if (lane == 0) {
         const int p = (phi - 1) * Lam;             // 2*Lam bits inside one word
@@ -153,8 +172,8 @@ __device__ __forceinline__ int alloc_snapshot(const uint32_t (&s_ser)[SLOTS], co
     return slot;
 }
 
-template <int SLOTS, bool SNAP_SMEM>
-__global__ void __launch_bounds__(kDecodeWarps * 32)
+template <int SLOTS, bool SNAP_SMEM, bool CHAN_SMEM>
+__global__ void __launch_bounds__(kDecodeWarps * 32, SLOTS == 4 ? kDecodeMinBlocks - 2 : kDecodeMinBlocks)
 fsscs_decode_kernel(const DecodeParams P) {
     extern __shared__ __align__(16) uint32_t smem[];
     const int lane = threadIdx.x & 31;
@@ -165,13 +184,14 @@ fsscs_decode_kernel(const DecodeParams P) {
     // shared memory when it fits: the schedule walk is derived from it
     const uint32_t *nodes = P.nodes;
     if (P.sched_words > 0) {
+        #pragma unroll 1
         for (int i = threadIdx.x; i < M; i += blockDim.x) smem[i] = P.nodes[i];
         __syncthreads();
         nodes = smem;
     }
     uint32_t *wb = smem + P.sched_words + warp * P.warp_words;
-    float *chan = reinterpret_cast<float *>(wb);
-    float *alpha = chan + N;
+    float *chan_s = reinterpret_cast<float *>(wb);                 // channel row (CHAN_SMEM)
+    float *alpha = CHAN_SMEM ? chan_s + N : chan_s;                // stages >= 6 (+ scratch)
     uint32_t *beta = reinterpret_cast<uint32_t *>(alpha + N);
     uint32_t *best = beta + nw;
     uint16_t *cnt = reinterpret_cast<uint16_t *>(best + nw);
@@ -180,22 +200,38 @@ fsscs_decode_kernel(const DecodeParams P) {
     else snap = P.snap_global + (size_t)(blockIdx.x * kDecodeWarps + warp) * (size_t)D * P.snap_stride;
     const int sstride = P.snap_stride;
 
-    unsigned long long f = 0;
-    if (lane == 0) f = atomicAdd(P.queue, 1ull);
+    // frame queue: each warp holds the frame it decodes and the next one it
+    // claimed, whose LLR row is prefetched into L2 meanwhile
+    unsigned long long f = 0, fnext = 0;
+    if (lane == 0) { f = atomicAdd(P.queue, 1ull); fnext = atomicAdd(P.queue, 1ull); }
     f = __shfl_sync(FULL, f, 0);
+    fnext = __shfl_sync(FULL, fnext, 0);
+    const unsigned long long nfr = (unsigned long long)P.n_frames;
 
-    while (f < (unsigned long long)P.n_frames) {
-        unsigned long long fnext = 0;
-        if (lane == 0) fnext = atomicAdd(P.queue, 1ull);
-
-        // ---- stage the channel row (the only mandatory HBM read) ----------
-        const float *row = P.llr + (size_t)f * N;
-        if (N >= 4) {
-            for (int i = lane * 4; i < N; i += 128)
-                *reinterpret_cast<float4 *>(chan + i) = __ldcs(reinterpret_cast<const float4 *>(row + i));
-        } else if (lane < N) {
-            chan[lane] = row[lane];
+    #pragma unroll 1
+    while (f < nfr) {
+        if (fnext < nfr) {
+            const char *nr = reinterpret_cast<const char *>(P.llr + (size_t)fnext * N);
+            #pragma unroll 1
+            for (int b = lane * 128; b < N * 4; b += 32 * 128)
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(nr + b));
         }
+        unsigned long long fnext2 = 0;
+        if (lane == 0) fnext2 = atomicAdd(P.queue, 1ull);
+
+        // ---- the channel row (the only mandatory HBM read) -----------------
+        const float *row = P.llr + (size_t)f * N;
+        const float *chan = CHAN_SMEM ? chan_s : row;
+        if (CHAN_SMEM) {
+            if (N >= 4) {
+                #pragma unroll 1
+                for (int i = lane * 4; i < N; i += 128)
+                    *reinterpret_cast<float4 *>(chan_s + i) = __ldcs(reinterpret_cast<const float4 *>(row + i));
+            } else if (lane < N) {
+                chan_s[lane] = row[lane];
+            }
+        }
+        #pragma unroll 1
         for (int i = lane; i < P.cnt_words; i += 32) reinterpret_cast<uint32_t *>(cnt)[i] = 0;
         __syncwarp();
 
@@ -210,12 +246,16 @@ fsscs_decode_kernel(const DecodeParams P) {
         // alpha memory content: stages s >= lev_mem hold the node (s, pos_mem >> s)
         // for the working path's beta (partial-spine reuse, reading R12)
         int pos_mem = 0, lev_mem = n;
+        float r[6];                       // alpha stages 0..5 (Lambda <= 32): element i in lane i
+#pragma unroll
+        for (int t = 0; t < 6; t++) r[t] = 0.f;
         bool have_best = false;
         float best_pm = 0.f, out_pm = 0.f;
         int status = 0;
         bool from_best = false;
         const uint32_t pop_cap = (uint32_t)P.L * (uint32_t)(M + 1);
 
+        #pragma unroll 1
         for (;;) {
             if (nS == 0) { from_best = true; out_pm = best_pm; status = 1; break; }   // reading R13
             if (pops >= pop_cap) { status = 2; out_pm = -1.f; break; }   // watchdog: cannot happen (cnt[j] <= L)
@@ -281,6 +321,7 @@ fsscs_decode_kernel(const DecodeParams P) {
                         const int slot = alloc_snapshot<SLOTS>(s_ser, s_jsm, D, -1, 0, jsm_snap(p_jsm), lane);
                         uint32_t *dst = snap + (size_t)slot * sstride;
                         const int nwords = (work_pl + 31) >> 5;
+                        #pragma unroll 1
                         for (int w = lane; w < nwords; w += 32) dst[w] = beta[w];
                         if (lane == wl) {
 #pragma unroll
@@ -295,6 +336,7 @@ fsscs_decode_kernel(const DecodeParams P) {
                 const uint32_t *src = snap + (size_t)ps * sstride;
                 const int nwords = (pl + 31) >> 5;
                 int d = 0x7FFFFFFF;
+                #pragma unroll 1
                 for (int w0 = 0; w0 < nwords; w0 += 32) {
                     const int w = w0 + lane;
                     uint32_t x = 0;
@@ -317,6 +359,7 @@ fsscs_decode_kernel(const DecodeParams P) {
                     const int seg = pphi << plam, Lam = 1 << plam;
                     if (pkind == OP_REP) {
                         if (Lam >= 32) {
+                            #pragma unroll 1
                             for (int t = lane; t < (Lam >> 5); t += 32) beta[(seg >> 5) + t] ^= FULL;
                         } else if (lane == 0) {
                             beta[seg >> 5] ^= ((1u << Lam) - 1u) << (seg & 31);
@@ -344,6 +387,7 @@ fsscs_decode_kernel(const DecodeParams P) {
             if (j > 0) {
                 int ph = pphi;
                 l = plam;
+                #pragma unroll 1
                 while (ph & 1) { beta_op(beta, l, ph, lane); ph >>= 1; l++; }
             }
 
@@ -352,6 +396,7 @@ fsscs_decode_kernel(const DecodeParams P) {
                 bool ok = true;
                 if (P.c > 0) {
                     uint32_t syn = 0;
+                    #pragma unroll 1
                     for (int q = lane; q < K; q += 32) {
                         const int idx = P.info[q];
                         if ((beta[idx >> 5] >> (idx & 31)) & 1u) syn ^= P.crc_tab[q];
@@ -361,6 +406,7 @@ fsscs_decode_kernel(const DecodeParams P) {
                 }
                 if (ok) { out_pm = p_pm; status = 0; break; }
                 if (!have_best) {
+                    #pragma unroll 1
                     for (int w = lane; w < nw; w += 32) best[w] = beta[w];
                     __syncwarp();
                     have_best = true;
@@ -376,7 +422,35 @@ fsscs_decode_kernel(const DecodeParams P) {
             {
                 int s_min = max(max(lev_mem, bitlen((uint32_t)(pos_mem ^ pl))), max(s_d, l + 1));
                 s_min = min(s_min, n);
-                for (int s = s_min - 1; s >= lam; s--) alpha_stage(chan, alpha, beta, n, s, pl >> s, lane);
+                const int s_hi = s_min - 1;
+                #pragma unroll 1
+                for (int s = s_hi; s >= max(lam, 6); s--) alpha_stage<CHAN_SMEM>(chan, alpha, beta, n, s, pl >> s, lane);
+                // register stages: lo = element i, hi = element i + Lambda by shuffle
+#pragma unroll
+                for (int t = 5; t >= 0; t--) {
+                    if (t <= s_hi && t >= lam) {
+                        const int Lt = 1 << t;
+                        float lo, hi;
+                        if (t + 1 == n) {
+                            lo = (lane < Lt) ? ld1<CHAN_SMEM>(chan + lane, true) : 0.f;
+                            hi = (lane < Lt) ? ld1<CHAN_SMEM>(chan + Lt + lane, true) : 0.f;
+                        } else if (t == 5) {
+                            lo = alpha[64 + lane];
+                            hi = alpha[96 + lane];
+                        } else {
+                            lo = r[t + 1];
+                            hi = __shfl_down_sync(FULL, r[t + 1], Lt);
+                        }
+                        const int psi = pl >> t;
+                        if (psi & 1) {
+                            const int boff = (psi - 1) << t;
+                            const uint32_t bit = (beta[boff >> 5] >> (((boff & 31) + lane) & 31)) & 1u;
+                            r[t] = g_exact(lo, hi, bit);
+                        } else {
+                            r[t] = f_minsum(lo, hi);
+                        }
+                    }
+                }
                 pos_mem = pl;
                 lev_mem = lam + 1;
             }
@@ -384,68 +458,83 @@ fsscs_decode_kernel(const DecodeParams P) {
             // ---- decision node ----------
             const int Lam = 1 << lam;
             const int seg = phi << lam;
-            float *a = (lam == n) ? chan : alpha + Lam;
-            if (lam == n && (kind == OP_R0 || kind == OP_REP)) {
+            float *a = alpha + Lam;           // node alpha in shared memory (Lambda > 32)
+            float xr = 0.f;                    // node alpha element of this lane (Lambda <= 32)
+            if (Lam <= 32) {
+                if (lam == n) {
+                    xr = (lane < Lam) ? ld1<CHAN_SMEM>(chan + lane, true) : 0.f;
+                } else {
+#pragma unroll
+                    for (int t = 0; t < 6; t++) if (t == lam) xr = r[t];
+                    if (lane >= Lam) xr = 0.f;
+                }
+            } else if (lam == n) {
                 // whole code is one node: copy the channel so the sums can work in place
-                for (int i = lane; i < N; i += 32) alpha[i] = chan[i];
+                #pragma unroll 1
+                for (int i = lane; i < N; i += 32) alpha[i] = ld1<CHAN_SMEM>(chan + i, true);
                 __syncwarp();
                 a = alpha;
             }
-            // candidate t lives in lane t: (dpm, mask) and its rank in (dPM, mask) order
-            float my_dpm = 0.f;
-            int my_mask = 0, my_rank = 0, nc = 1;
+            // Candidates in (dPM, mask) order (reading R7).  With
+            // A0 <= A1 <= A2 <= A3 the order is fixed up to one comparison, because
+            // round-to-nearest addition of non-negative values is monotone:
+            //   R1:          masks 0, 1, 2, 3          (0, A0, A1, A0+A1)
+            //   SPC, even:   0, 3, 5, 6|9, 9|6, 10, 12, 15  (6 = A1+A2, 9 = A0+A3)
+            //   SPC, odd:    1, 2, 4, 7|8, 8|7, 11, 13, 14  (7 = A0+A1+A2, 8 = A3)
+            // clist holds the masks in that order, 4 bits each.
+            uint32_t clist = 0;
+            int nc = 1;
+            float vn = 0.f, vp = 0.f;
+            float A[4] = {0.f, 0.f, 0.f, 0.f};
             uint32_t mi[4] = {0, 0, 0, 0};
+            const bool sum_kind = (kind == OP_R0 || kind == OP_REP);
 
-            if (kind == OP_R0 || kind == OP_REP) {
+            if (sum_kind) {
                 // tree-order sums T(neg(a)) and T(pos(a)) (reading R3)
                 const bool rep = (kind == OP_REP);
-                float vn, vp;
                 if (Lam > 32) {
                     const int R = Lam >> 5, H = R >> 1;
+                    #pragma unroll 1
                     for (int t = 0; t < H; t++) {        // first level, in place, lane-private columns
                         const float x = a[32 * t + lane], y = a[32 * (t + H) + lane];
                         a[32 * t + lane] = negpart(x) + negpart(y);
                         a[32 * (t + H) + lane] = pospart(x) + pospart(y);
                     }
+                    #pragma unroll 1
                     for (int h = H >> 1; h >= 1; h >>= 1)
+                        #pragma unroll 1
                         for (int t = 0; t < h; t++) {
                             a[32 * t + lane] += a[32 * (t + h) + lane];
                             if (rep) a[32 * (H + t) + lane] += a[32 * (H + t + h) + lane];
                         }
                     vn = a[lane];
                     vp = a[32 * H + lane];
+                    #pragma unroll 1
                     for (int h = 16; h >= 1; h >>= 1) {
                         vn += __shfl_down_sync(FULL, vn, h);
                         vp += __shfl_down_sync(FULL, vp, h);
                     }
                     __syncwarp();
                 } else {
-                    const float x = (lane < Lam) ? a[lane] : 0.f;
-                    vn = negpart(x);
-                    vp = pospart(x);
+                    vn = negpart(xr);
+                    vp = pospart(xr);
+                    #pragma unroll 1
                     for (int h = Lam >> 1; h >= 1; h >>= 1) {
                         vn += __shfl_down_sync(FULL, vn, h);
-                        vp += __shfl_down_sync(FULL, vp, h);
+                        if (rep) vp += __shfl_down_sync(FULL, vp, h);
                     }
                 }
                 vn = __shfl_sync(FULL, vn, 0);
                 vp = __shfl_sync(FULL, vp, 0);
-                if (!rep) {
-                    nc = 1; my_dpm = vn;
-                } else {
-                    nc = 2;
-                    my_dpm = (lane == 0) ? vn : vp;
-                    my_mask = lane & 1;
-                    const bool ones_first = vp < vn;           // ties: zeros first
-                    my_rank = (lane == 0) ? (ones_first ? 1 : 0) : (ones_first ? 0 : 1);
-                }
+                if (rep) { nc = 2; clist = (vp < vn) ? 0x01u : 0x10u; }   // ties: zeros first
             } else {
                 // R1 / SPC: hard-decision word, parity, least reliable positions
                 const int need = (kind == OP_SPC) ? 4 : 2;
-                unsigned long long t0 = ~0ull, t1 = ~0ull, t2 = ~0ull, t3 = ~0ull;
-                uint32_t par = 0, hdw = 0;
-                if (Lam >= 32) {
+                uint32_t par = 0;
+                if (Lam > 32) {
+                    unsigned long long t0 = ~0ull, t1 = ~0ull, t2 = ~0ull, t3 = ~0ull;
                     const int R = Lam >> 5;
+                    #pragma unroll 1
                     for (int t = 0; t < R; t++) {
                         const float x = a[32 * t + lane];
                         const uint32_t b = __ballot_sync(FULL, x < 0.f);
@@ -454,17 +543,6 @@ fsscs_decode_kernel(const DecodeParams P) {
                         top4_insert(((unsigned long long)__float_as_uint(fabsf(x)) << 32) | (uint32_t)(32 * t + lane),
                                     t0, t1, t2, t3);
                     }
-                } else {
-                    const float x = (lane < Lam) ? a[lane] : 0.f;
-                    hdw = __ballot_sync(FULL, lane < Lam && x < 0.f);
-                    par = (uint32_t)__popc(hdw);
-                    if (lane < Lam) t0 = ((unsigned long long)__float_as_uint(fabsf(x)) << 32) | (uint32_t)lane;
-                }
-                par &= 1u;
-                float A[4] = {0.f, 0.f, 0.f, 0.f};
-                if (Lam == 1) {
-                    A[0] = fabsf(a[0]);                       // R1 at Lambda = 1 (reading R6)
-                } else {
 #pragma unroll
                     for (int r = 0; r < 4; r++) {
                         if (r < need) {
@@ -475,59 +553,59 @@ fsscs_decode_kernel(const DecodeParams P) {
                             if ((uint32_t)t0 == ml && (uint32_t)(t0 >> 32) == mh) { t0 = t1; t1 = t2; t2 = t3; t3 = ~0ull; }
                         }
                     }
-                }
-                if (kind == OP_R1) {
-                    if (Lam == 1) {
-                        nc = 2; my_mask = lane & 1; my_dpm = (lane == 1) ? A[0] : 0.f; my_rank = lane;
-                    } else {
-                        // Chase-II: (0, m1, m2, m1+m2) is already in (dPM, mask) order
-                        nc = 4; my_mask = lane & 3; my_rank = lane;
-                        my_dpm = (my_mask == 0) ? 0.f : (my_mask == 1) ? A[0] : (my_mask == 2) ? A[1] : A[0] + A[1];
-                    }
                 } else {
-                    // SPC: the 8 flip sets S of {m1..m4} with |S| = parity (mod 2)
-                    nc = 8;
-                    const uint32_t table = par ? 0xEDB87421u : 0xFCA96530u;   // masks in ascending order
-                    my_mask = (int)((table >> (4 * (lane & 7))) & 15u);
-                    float dsum = 0.f;
-                    bool first = true;
-#pragma unroll
-                    for (int q = 0; q < 4; q++)
-                        if ((my_mask >> q) & 1) { dsum = first ? A[q] : dsum + A[q]; first = false; }
-                    my_dpm = dsum;
-                    // rank = #{u : (dpm_u, mask_u) < (dpm_t, mask_t)}: pairwise compares, 32 per round
-                    const int u = lane & 7;
-                    const float du = __shfl_sync(FULL, my_dpm, u);
-                    const int mu = __shfl_sync(FULL, my_mask, u);
-                    uint32_t bal[2];
-#pragma unroll
-                    for (int rnd = 0; rnd < 2; rnd++) {
-                        const int t = (lane >> 3) + 4 * rnd;
-                        const float dt_ = __shfl_sync(FULL, my_dpm, t);
-                        const int mt_ = __shfl_sync(FULL, my_mask, t);
-                        bal[rnd] = __ballot_sync(FULL, du < dt_ || (du == dt_ && mu < mt_));
+                    const uint32_t hdw = __ballot_sync(FULL, lane < Lam && xr < 0.f);
+                    par = (uint32_t)__popc(hdw);
+                    if (lane == 0) {
+                        // HD word of the node (Lam <= 32 bits) into beta; c1's flips applied below
+                        const uint32_t lm = (Lam == 32) ? FULL : (1u << Lam) - 1u;
+                        const int w = seg >> 5, o = seg & 31;
+                        beta[w] = (beta[w] & ~(lm << o)) | ((hdw & lm) << o);
                     }
-                    const uint32_t bb = (lane < 4) ? bal[0] : bal[1];
-                    my_rank = __popc((bb >> (8 * (lane & 3))) & 0xFFu);
+                    // least reliable: the lane is the index, so ties go to the lowest lane
+                    uint32_t key = (lane < Lam) ? __float_as_uint(fabsf(xr)) : 0xFFFFFFFFu;
+#pragma unroll
+                    for (int r = 0; r < 4; r++) {
+                        if (r < need && r < Lam) {
+                            const uint32_t mh = __reduce_min_sync(FULL, key);
+                            const int ml = __ffs(__ballot_sync(FULL, key == mh)) - 1;
+                            mi[r] = (uint32_t)ml;
+                            A[r] = __uint_as_float(mh);
+                            if (lane == ml) key = 0xFFFFFFFFu;
+                        }
+                    }
                 }
-                if (Lam < 32 && lane == 0) {
-                    // HD word of the node (Lam < 32 bits) into beta; c1's flips applied below
-                    const uint32_t lm = (1u << Lam) - 1u;
-                    const int w = seg >> 5, o = seg & 31;
-                    beta[w] = (beta[w] & ~(lm << o)) | ((hdw & lm) << o);
+                par &= 1u;
+                if (kind == OP_R1) {
+                    nc = (Lam == 1) ? 2 : 4;                // Lambda = 1: HD and its flip (reading R6)
+                    clist = 0x3210u;
+                } else {
+                    nc = 8;
+                    if (par == 0) clist = ((A[0] + A[3]) < (A[1] + A[2])) ? 0xFCA69530u : 0xFCA96530u;
+                    else          clist = (A[3] < (A[0] + A[1]) + A[2]) ? 0xEDB78421u : 0xEDB87421u;
                 }
                 __syncwarp();
             }
-            const bool is_cand = lane < nc;
+            // dPM of a candidate mask: R0/REP tree sums, else the flipped |alpha|s
+            // summed in order m1, m2, m3, m4
+            auto dpm_of = [&](uint32_t msk) -> float {
+                if (sum_kind) return msk ? vp : vn;
+                float d = 0.f;
+                bool first = true;
+#pragma unroll
+                for (int q = 0; q < 4; q++)
+                    if ((msk >> q) & 1u) { d = first ? A[q] : d + A[q]; first = false; }
+                return d;
+            };
 
             // ---- c1 continues in the working memory ------------------------
-            const int c1l = __ffs(__ballot_sync(FULL, is_cand && my_rank == 0)) - 1;
-            const float dpm1 = __shfl_sync(FULL, my_dpm, c1l);
-            const int m0 = __shfl_sync(FULL, my_mask, c1l);
+            const int m0 = (int)(clist & 15u);
+            const float dpm1 = dpm_of((uint32_t)m0);
             {
-                if (kind == OP_R0 || kind == OP_REP) {
+                if (sum_kind) {
                     const uint32_t fill = (kind == OP_REP && m0) ? FULL : 0u;
                     if (Lam >= 32) {
+                        #pragma unroll 1
                         for (int t = lane; t < (Lam >> 5); t += 32) beta[(seg >> 5) + t] = fill;
                     } else if (lane == 0) {
                         const uint32_t lm = ((1u << Lam) - 1u) << (seg & 31);
@@ -570,10 +648,10 @@ fsscs_decode_kernel(const DecodeParams P) {
             // reliable iff strictly better.  Ranks ascend, so the
             // first one dropped ends the loop.  They share one fork snapshot.
             int fslot = -1;
+            #pragma unroll 1
             for (int r = 1; r < nc; r++) {
-                const int ol = __ffs(__ballot_sync(FULL, is_cand && my_rank == r)) - 1;
-                const float dt = __shfl_sync(FULL, my_dpm, ol);
-                const int mt = __shfl_sync(FULL, my_mask, ol);
+                const int mt = (int)((clist >> (4 * r)) & 15u);
+                const float dt = dpm_of((uint32_t)mt);
                 const uint32_t cpm = __float_as_uint(p_pm + dt);
                 int tl = -1, ts = 0;
                 if (nS < D) {
@@ -600,6 +678,7 @@ fsscs_decode_kernel(const DecodeParams P) {
                     fslot = alloc_snapshot<SLOTS>(s_ser, s_jsm, D, tl, ts, SNAP_NONE, lane);
                     uint32_t *dst = snap + (size_t)fslot * sstride;
                     const int nwords = (npl + 31) >> 5;
+                    #pragma unroll 1
                     for (int w = lane; w < nwords; w += 32) dst[w] = beta[w];
                     if (lane == 0) {
                         dst[nw] = mi[0] | (mi[1] << 16);
@@ -625,6 +704,7 @@ fsscs_decode_kernel(const DecodeParams P) {
         {
             const uint32_t *bsrc = from_best ? best : beta;
             uint8_t *ob = P.out_bits + (size_t)f * K;
+            #pragma unroll 1
             for (int q = lane; q < K; q += 32) {
                 const int idx = P.info[q];
                 ob[q] = (uint8_t)((bsrc[idx >> 5] >> (idx & 31)) & 1u);
@@ -637,48 +717,49 @@ fsscs_decode_kernel(const DecodeParams P) {
             }
             __syncwarp();
         }
-        f = __shfl_sync(FULL, fnext, 0);
+        f = fnext;
+        fnext = __shfl_sync(FULL, fnext2, 0);
     }
 }
 
-template <int SLOTS, bool SM>
+template <int SLOTS, bool SM, bool CS>
 static cudaError_t launch_t(const DecodeParams &p, int ctas, int smem, cudaStream_t st) {
-    auto kern = fsscs_decode_kernel<SLOTS, SM>;
+    auto kern = fsscs_decode_kernel<SLOTS, SM, CS>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     kern<<<ctas, kDecodeWarps * 32, smem, st>>>(p);
     return cudaGetLastError();
 }
 
-cudaError_t launch_decode(const DecodeParams &p, int slots, bool snap_smem, int ctas, int smem, cudaStream_t st) {
-    if (snap_smem) {
-        if (slots == 1) return launch_t<1, true>(p, ctas, smem, st);
-        if (slots == 2) return launch_t<2, true>(p, ctas, smem, st);
-        return launch_t<4, true>(p, ctas, smem, st);
-    }
-    if (slots == 1) return launch_t<1, false>(p, ctas, smem, st);
-    if (slots == 2) return launch_t<2, false>(p, ctas, smem, st);
-    return launch_t<4, false>(p, ctas, smem, st);
+template <bool SM, bool CS>
+static cudaError_t launch_s(const DecodeParams &p, int slots, int ctas, int smem, cudaStream_t st) {
+    if (slots == 1) return launch_t<1, SM, CS>(p, ctas, smem, st);
+    if (slots == 2) return launch_t<2, SM, CS>(p, ctas, smem, st);
+    return launch_t<4, SM, CS>(p, ctas, smem, st);
 }
 
-cudaError_t decode_occupancy(int slots, bool snap_smem, int smem, int *blocks_per_sm) {
-    cudaError_t e;
-#define OCC(S, B)                                                                                       \
-    do {                                                                                                \
-        e = cudaFuncSetAttribute(fsscs_decode_kernel<S, B>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); \
-        if (e != cudaSuccess) return e;                                                                 \
-        return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, fsscs_decode_kernel<S, B>,   \
-                                                             kDecodeWarps * 32, smem);                  \
-    } while (0)
-    if (snap_smem) {
-        if (slots == 1) OCC(1, true);
-        if (slots == 2) OCC(2, true);
-        OCC(4, true);
-    }
-    if (slots == 1) OCC(1, false);
-    if (slots == 2) OCC(2, false);
-    OCC(4, false);
-#undef OCC
+cudaError_t launch_decode(const DecodeParams &p, int slots, bool snap_smem, bool chan_smem, int ctas, int smem,
+                          cudaStream_t st) {
+    if (snap_smem) return chan_smem ? launch_s<true, true>(p, slots, ctas, smem, st) : launch_s<true, false>(p, slots, ctas, smem, st);
+    return chan_smem ? launch_s<false, true>(p, slots, ctas, smem, st) : launch_s<false, false>(p, slots, ctas, smem, st);
+}
+
+template <int S, bool B, bool C>
+static cudaError_t occ_t(int smem, int *blocks) {
+    cudaError_t e = cudaFuncSetAttribute(fsscs_decode_kernel<S, B, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, fsscs_decode_kernel<S, B, C>, kDecodeWarps * 32, smem);
+}
+template <bool B, bool C>
+static cudaError_t occ_s(int slots, int smem, int *blocks) {
+    if (slots == 1) return occ_t<1, B, C>(smem, blocks);
+    if (slots == 2) return occ_t<2, B, C>(smem, blocks);
+    return occ_t<4, B, C>(smem, blocks);
+}
+
+cudaError_t decode_occupancy(int slots, bool snap_smem, bool chan_smem, int smem, int *blocks_per_sm) {
+    if (snap_smem) return chan_smem ? occ_s<true, true>(slots, smem, blocks_per_sm) : occ_s<true, false>(slots, smem, blocks_per_sm);
+    return chan_smem ? occ_s<false, true>(slots, smem, blocks_per_sm) : occ_s<false, false>(slots, smem, blocks_per_sm);
 }
 
 }  // namespace polar

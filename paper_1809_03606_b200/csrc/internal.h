@@ -21,6 +21,7 @@ __host__ __device__ inline uint32_t op_phi(uint32_t op) { return op >> 8; }
 constexpr int kMaxN = 4096;
 constexpr int kMaxD = 128;
 constexpr int kDecodeWarps = 4;      // warps (frames in flight) per decode CTA
+constexpr int kDecodeMinBlocks = 8;  // launch bound: 32 resident warps/SM => <= 64 registers
 constexpr int kCodecWarps = 4;       // warps per CTA of the generator/encoder kernels
 
 // Host-side compiled code description (host.cpp)
@@ -82,6 +83,7 @@ struct polar_scs_s {
     uint32_t *d_snap = nullptr;     // global snapshot arena (or null)
     size_t snap_bytes = 0;
     int snap_in_smem = 0;
+    int chan_in_smem = 0;
     int warps_per_cta = 0, ctas = 0, smem_per_cta = 0;
     polar::DecodeParams base{};     // prefilled params
     // host-staging for polar_scs_decode_host (lazily allocated)

@@ -121,18 +121,31 @@ def test_decode_parity(cfg, ebno, n):
     assert np.array_equal(dec.decode(gl).cpu().numpy(), ref["bits"])
 
 
-@pytest.mark.parametrize("cfg", ["C2", "C5"])
-def test_decode_parity_snapshots_in_global(cfg):
+PLACEMENTS = [dict(snap_smem=True, chan_smem=True), dict(snap_global=True, chan_smem=True),
+              dict(snap_smem=True, chan_global=True), dict(snap_global=True, chan_global=True)]
+
+
+@pytest.mark.parametrize("cfg", ["C1", "C2", "C4", "C5"])
+@pytest.mark.parametrize("place", range(4))
+def test_decode_parity_memory_placements(cfg, place):
+    """Snapshots and the channel row in shared memory or L1/L2: same results."""
     c, fr = _mk(cfg)
-    dec = P.PolarSCS(fr, c["D"], c["L"], c["crc_poly"], snap_global=True)
-    assert dec.info["snap_in_smem"] == 0
+    kw = PLACEMENTS[place]
+    try:
+        dec = P.PolarSCS(fr, c["D"], c["L"], c["crc_poly"], **kw)
+    except P.PolarError as e:
+        if e.code == P.POLAR_EINVAL and kw.get("snap_smem"):
+            pytest.skip("snapshot arena does not fit in shared memory for this code")
+        raise
+    assert dec.info["snap_in_smem"] == int(bool(kw.get("snap_smem")))
+    assert dec.info["chan_in_smem"] == int(bool(kw.get("chan_smem")))
     n = 100
     pay = ig.payload_bits(7, 0, n, c["K"] - dec.c)
     nz = ig.unit_normals(7, 0, n, c["N"])
     _, _, gl = _gpu_llr(dec, pay, nz, c["ebno"][0] - 0.5)
     _, _, ol = _oracle_llr(fr, c["crc_poly"], pay, nz, c["ebno"][0] - 0.5)
     ref = O.SCSDecoder(fr, c["D"], c["L"], c["crc_poly"]).decode(ol, threads=8)
-    _compare(dec.decode_stats(gl), ref, cfg)
+    _compare(dec.decode_stats(gl), ref, f"{cfg} {kw}")
 
 
 @pytest.mark.parametrize("N,K,D,L,crc,bit_level", [
