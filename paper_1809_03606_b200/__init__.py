@@ -17,7 +17,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_SO = os.path.join(_HERE, "libpolarscs.so")
+_SO = os.environ.get("POLAR_SCS_LIB") or os.path.join(_HERE, "libpolarscs.so")   # override: A/B builds
 
 if not os.path.exists(_SO):
     raise ImportError(f"libpolarscs.so not built ({_SO}); run `python -m paper_1809_03606_b200.build` "
