@@ -387,6 +387,20 @@ fsscs_decode_kernel(const DecodeParams P) {
             if (j > 0) {
                 int ph = pphi;
                 l = plam;
+                if ((ph & 1) && l < 5) {
+                    // every BETA with 2*Lambda <= 32 acts inside one word: one RMW
+                    const int w = ((ph - 1) << l) >> 5;
+                    uint32_t x = beta[w];
+                    #pragma unroll 1
+                    while ((ph & 1) && l < 5) {
+                        const int o = ((ph - 1) << l) & 31, Lm = 1 << l;
+                        x ^= ((x >> (o + Lm)) & ((1u << Lm) - 1u)) << o;
+                        ph >>= 1;
+                        l++;
+                    }
+                    if (lane == 0) beta[w] = x;
+                    __syncwarp();
+                }
                 #pragma unroll 1
                 while (ph & 1) { beta_op(beta, l, ph, lane); ph >>= 1; l++; }
             }
@@ -419,13 +433,15 @@ fsscs_decode_kernel(const DecodeParams P) {
             // holds node (s, pl >> s); stages >= s_min are still valid
             const uint32_t nd = nodes[j];
             const int kind = (int)op_kind(nd), lam = (int)op_lam(nd), phi = (int)op_phi(nd);
+            float xr = 0.f;                    // node alpha element of this lane (Lambda <= 32)
             {
                 int s_min = max(max(lev_mem, bitlen((uint32_t)(pos_mem ^ pl))), max(s_d, l + 1));
                 s_min = min(s_min, n);
                 const int s_hi = s_min - 1;
                 #pragma unroll 1
                 for (int s = s_hi; s >= max(lam, 6); s--) alpha_stage<CHAN_SMEM>(chan, alpha, beta, n, s, pl >> s, lane);
-                // register stages: lo = element i, hi = element i + Lambda by shuffle
+                // register stages: lo = element i, hi = element i + Lambda by shuffle;
+                // the last one computed is the node's own stage
 #pragma unroll
                 for (int t = 5; t >= 0; t--) {
                     if (t <= s_hi && t >= lam) {
@@ -449,6 +465,7 @@ fsscs_decode_kernel(const DecodeParams P) {
                         } else {
                             r[t] = f_minsum(lo, hi);
                         }
+                        xr = r[t];
                     }
                 }
                 pos_mem = pl;
@@ -459,15 +476,9 @@ fsscs_decode_kernel(const DecodeParams P) {
             const int Lam = 1 << lam;
             const int seg = phi << lam;
             float *a = alpha + Lam;           // node alpha in shared memory (Lambda > 32)
-            float xr = 0.f;                    // node alpha element of this lane (Lambda <= 32)
             if (Lam <= 32) {
-                if (lam == n) {
-                    xr = (lane < Lam) ? ld1<CHAN_SMEM>(chan + lane, true) : 0.f;
-                } else {
-#pragma unroll
-                    for (int t = 0; t < 6; t++) if (t == lam) xr = r[t];
-                    if (lane >= Lam) xr = 0.f;
-                }
+                if (lam == n) xr = ld1<CHAN_SMEM>(chan + (lane & (Lam - 1)), true);
+                if (lane >= Lam) xr = 0.f;
             } else if (lam == n) {
                 // whole code is one node: copy the channel so the sums can work in place
                 #pragma unroll 1
@@ -586,21 +597,21 @@ fsscs_decode_kernel(const DecodeParams P) {
                 }
                 __syncwarp();
             }
-            // dPM of a candidate mask: R0/REP tree sums, else the flipped |alpha|s
-            // summed in order m1, m2, m3, m4
-            auto dpm_of = [&](uint32_t msk) -> float {
-                if (sum_kind) return msk ? vp : vn;
-                float d = 0.f;
+            // lane r computes candidate r's mask and dPM (R0/REP: tree sums; R1/SPC:
+            // the flipped |alpha|s summed in order m1, m2, m3, m4)
+            const uint32_t my_m = (clist >> (4 * (lane & 7))) & 15u;
+            float my_d = 0.f;
+            if (sum_kind) {
+                my_d = my_m ? vp : vn;
+            } else {
                 bool first = true;
 #pragma unroll
                 for (int q = 0; q < 4; q++)
-                    if ((msk >> q) & 1u) { d = first ? A[q] : d + A[q]; first = false; }
-                return d;
-            };
+                    if ((my_m >> q) & 1u) { my_d = first ? A[q] : my_d + A[q]; first = false; }
+            }
 
             // ---- c1 continues in the working memory ------------------------
             const int m0 = (int)(clist & 15u);
-            const float dpm1 = dpm_of((uint32_t)m0);
             {
                 if (sum_kind) {
                     const uint32_t fill = (kind == OP_REP && m0) ? FULL : 0u;
@@ -625,66 +636,67 @@ fsscs_decode_kernel(const DecodeParams P) {
             const uint32_t ser0 = next_serial;
             next_serial += (uint32_t)nc;
 
-            // insert c1 into a free entry (p's was freed, reading R8)
+            // c1 and the siblings that fit take free entries, in rank order, in one
+            // step (p's entry was freed, so c1 always fits: reading R8).  The
+            // siblings share one fork snapshot: beta prefix [0, npl) with c1's
+            // segment, plus m1..m4 for the flip descriptors.
+            int fslot = -1;
+            const int nfit = min(nc, D - nS);
+            auto write_fork_snapshot = [&](int victim_lane, int victim_slot) {
+                fslot = alloc_snapshot<SLOTS>(s_ser, s_jsm, D, victim_lane, victim_slot, SNAP_NONE, lane);
+                uint32_t *dst = snap + (size_t)fslot * sstride;
+                const int nwords = (npl + 31) >> 5;
+                #pragma unroll 1
+                for (int w = lane; w < nwords; w += 32) dst[w] = beta[w];
+                if (lane == 0) {
+                    dst[nw] = mi[0] | (mi[1] << 16);
+                    dst[nw + 1] = mi[2] | (mi[3] << 16);
+                }
+            };
+            if (nfit > 1) write_fork_snapshot(-1, 0);
             int c1_lane = 0, c1_slot = 0;
             {
-                bool placed = false;
+                int base = 0;
+                bool c1_found = false;
 #pragma unroll
                 for (int s = 0; s < SLOTS; s++) {
-                    const uint32_t fb = __ballot_sync(FULL, s_ser[s] == EMPTY);
-                    if (!placed && fb) {
-                        c1_lane = __ffs(fb) - 1; c1_slot = s; placed = true;
-                        if (lane == c1_lane) {
-                            s_pm[s] = __float_as_uint(p_pm + dpm1); s_ser[s] = ser0; s_jsm[s] = jsm_make(jn, SNAP_NONE, 0);
-                        }
+                    const bool fr = (s_ser[s] == EMPTY);
+                    const uint32_t fb = __ballot_sync(FULL, fr);
+                    const int k = base + __popc(fb & ((1u << lane) - 1u));    // rank among free entries
+                    const float dk = __shfl_sync(FULL, my_d, k & 7);
+                    if (fr && k < nfit) {
+                        const uint32_t mk = (clist >> (4 * k)) & 15u;
+                        s_pm[s] = __float_as_uint(p_pm + dk);
+                        s_ser[s] = ser0 + (uint32_t)k;
+                        s_jsm[s] = jsm_make(jn, (k == 0 && nfit == 1) ? SNAP_NONE : (uint32_t)fslot, mk ^ (uint32_t)m0);
                     }
+                    const uint32_t b0 = __ballot_sync(FULL, fr && k == 0);
+                    if (!c1_found && b0) { c1_found = true; c1_lane = __ffs(b0) - 1; c1_slot = s; }
+                    base += __popc(fb);
                 }
-                nS++;
+                nS += nfit;
             }
             work = ser0;
             work_pl = npl;
 
-            // siblings in rank order: insert if room, else replace the least
-            // reliable iff strictly better.  Ranks ascend, so the
-            // first one dropped ends the loop.  They share one fork snapshot.
-            int fslot = -1;
+            // the rest (stack full): replace the least reliable iff strictly better
+            // (PAPER.md:L599).  Ranks ascend, so the first one dropped ends the loop.
             #pragma unroll 1
-            for (int r = 1; r < nc; r++) {
+            for (int r = nfit; r < nc; r++) {
                 const int mt = (int)((clist >> (4 * r)) & 15u);
-                const float dt = dpm_of((uint32_t)mt);
+                const float dt = __shfl_sync(FULL, my_d, r);
                 const uint32_t cpm = __float_as_uint(p_pm + dt);
-                int tl = -1, ts = 0;
-                if (nS < D) {
+                uint32_t xpm = 0, xser = 0;
+                int xs = 0;
 #pragma unroll
-                    for (int s = 0; s < SLOTS; s++) {
-                        const uint32_t fb = __ballot_sync(FULL, s_ser[s] == EMPTY);
-                        if (tl < 0 && fb) { tl = __ffs(fb) - 1; ts = s; }
-                    }
-                    nS++;
-                } else {
-                    uint32_t xpm = 0, xser = 0;
-                    int xs = 0;
-#pragma unroll
-                    for (int s = 0; s < SLOTS; s++)
-                        if (s_ser[s] != EMPTY && (s_pm[s] > xpm || (s_pm[s] == xpm && s_ser[s] >= xser))) { xpm = s_pm[s]; xser = s_ser[s]; xs = s; }
-                    const uint32_t Mpm = __reduce_max_sync(FULL, xpm);
-                    if (cpm >= Mpm) break;                      // dropped, and so are the rest
-                    const uint32_t Mser = __reduce_max_sync(FULL, xpm == Mpm ? xser : 0u);
-                    tl = __ffs(__ballot_sync(FULL, xpm == Mpm && xser == Mser)) - 1;
-                    ts = __shfl_sync(FULL, xs, tl);
-                }
-                if (fslot < 0) {
-                    // fork snapshot: beta prefix [0, npl) with c1's segment + m1..m4
-                    fslot = alloc_snapshot<SLOTS>(s_ser, s_jsm, D, tl, ts, SNAP_NONE, lane);
-                    uint32_t *dst = snap + (size_t)fslot * sstride;
-                    const int nwords = (npl + 31) >> 5;
-                    #pragma unroll 1
-                    for (int w = lane; w < nwords; w += 32) dst[w] = beta[w];
-                    if (lane == 0) {
-                        dst[nw] = mi[0] | (mi[1] << 16);
-                        dst[nw + 1] = mi[2] | (mi[3] << 16);
-                    }
-                }
+                for (int s = 0; s < SLOTS; s++)
+                    if (s_ser[s] != EMPTY && (s_pm[s] > xpm || (s_pm[s] == xpm && s_ser[s] >= xser))) { xpm = s_pm[s]; xser = s_ser[s]; xs = s; }
+                const uint32_t Mpm = __reduce_max_sync(FULL, xpm);
+                if (cpm >= Mpm) break;                      // dropped, and so are the rest
+                const uint32_t Mser = __reduce_max_sync(FULL, xpm == Mpm ? xser : 0u);
+                const int tl = __ffs(__ballot_sync(FULL, xpm == Mpm && xser == Mser)) - 1;
+                const int ts = __shfl_sync(FULL, xs, tl);
+                if (fslot < 0) write_fork_snapshot(tl, ts);
                 if (lane == tl) {
 #pragma unroll
                     for (int s = 0; s < SLOTS; s++)
