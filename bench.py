@@ -195,6 +195,7 @@ def run_ours(args, cfg, c):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_1809_03606_b200 as P
+    from paper_1809_03606_b200 import shard
 
     nf = args.frames or c["frames"]
     npts = len(c["ebno"])
@@ -206,7 +207,7 @@ def run_ours(args, cfg, c):
 
     # inputs: device generator, each rank its own frame range; all points share
     # the draws (common random numbers)
-    first = rank * nf
+    first = shard.frame_range(rank, world, nf)[0]
     llr = torch.empty((frames, N), dtype=torch.float32, device="cuda")
     blocks = None
     tg0 = time.perf_counter()
@@ -248,10 +249,7 @@ def run_ours(args, cfg, c):
         barrier()
     t_ms = ev0.elapsed_time(ev1)
     launch_ms = [a.elapsed_time(b) for a, b in per_launch]
-    if dist is not None:
-        tt = torch.tensor([t_ms], device="cuda")
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_ms = float(tt.item())
+    t_ms = shard.max_over_ranks(t_ms, device="cuda")
     ms_per_step = t_ms / args.steps
     fps_rank = frames / (ms_per_step / 1e3)
     value = world * frames * K / (ms_per_step / 1e3) / 1e6
@@ -261,8 +259,9 @@ def run_ours(args, cfg, c):
     torch.cuda.synchronize()
     fer = []
     for p in range(npts):
-        errs = (stats["bits"][p * nf:(p + 1) * nf] != blocks).any(1).float().mean().item()
-        fer.append(errs)
+        errs = int((stats["bits"][p * nf:(p + 1) * nf] != blocks).any(1).sum().item())
+        tot = shard.reduce_counters({"frames": nf, "frame_errors": errs}, device="cuda")
+        fer.append(tot["frame_errors"] / tot["frames"])
     pops_mean = [float(stats["pops"][p * nf:(p + 1) * nf].float().mean().item()) for p in range(npts)]
     sw_mean = [float(stats["switches"][p * nf:(p + 1) * nf].float().mean().item()) for p in range(npts)]
     assert torch.equal(stats["bits"], out), "decode and decode_stats disagree"
@@ -281,10 +280,7 @@ def run_ours(args, cfg, c):
             dec.decode_host(host_llr, host_out)
         barrier()
         e2e_s = (time.perf_counter() - t0) / reps
-        if dist is not None:
-            tt = torch.tensor([e2e_s], device="cuda")
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-            e2e_s = float(tt.item())
+        e2e_s = shard.max_over_ranks(e2e_s, device="cuda")
         assert torch.equal(host_out, out.cpu()), "host-path decode differs"
         e2e = {"value": world * frames * K / e2e_s / 1e6, "unit": "Mbps",
                "h2d_bytes_per_step": frames * N * 4, "d2h_bytes_per_step": frames * K,
