@@ -128,7 +128,7 @@ int polar_scs_create_ex(polar_scs_t *out, int32_t N, int32_t K, const uint8_t *f
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device);
     const int nw = std::max(1, N / 32);
     const int cnt_words = ((t.M + 1) * 2 + 3) / 4;
-    const int sstride = nw + 2;
+    const int sstride = nw;                       // snapshot slot: beta words (headers live in smem)
     const int sched_words = (t.M * 4 <= 16384) ? round4(t.M) : 0;
     const int slots = slots_for(D);
 
@@ -152,7 +152,7 @@ int polar_scs_create_ex(polar_scs_t *out, int32_t N, int32_t K, const uint8_t *f
             const bool snap_smem = (si == 0);
             if (snap_smem && (flags & POLAR_FLAG_SNAP_GLOBAL)) continue;
             if (!snap_smem && (flags & POLAR_FLAG_SNAP_SMEM)) continue;
-            const int ww = round4((chan_smem ? N : 0) + N + 2 * nw + cnt_words + (snap_smem ? D * sstride : 0));
+            const int ww = round4((chan_smem ? N : 0) + N + 2 * nw + cnt_words + 2 * D + (snap_smem ? D * sstride : 0));
             const int smem = 4 * (sched_words + kDecodeWarps * ww);
             if (smem > optin) continue;
             int occ = 0;

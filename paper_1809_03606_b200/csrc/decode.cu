@@ -27,9 +27,13 @@ constexpr uint32_t FULL = 0xFFFFFFFFu;
 constexpr uint32_t EMPTY = 0xFFFFFFFFu;
 constexpr uint32_t NO_SNAP = 0xFFFFu;
 
-__device__ __forceinline__ float f_minsum(float a, float b) {      // Eq. (1)
+// Eq. (1): sign(a) sign(b) min(|a|,|b|).  The sign is taken from
+// the sign bits, so it differs from a comparison-based sign only when an input
+// is -0, i.e. when the result is a zero: HD, |.|, the PM sums and every later
+// f/g see +0 and -0 alike (reading R2), so bits, PMs and counts are unchanged.
+__device__ __forceinline__ float f_minsum(float a, float b) {
     const float m = fminf(fabsf(a), fabsf(b));
-    return ((a < 0.f) != (b < 0.f)) ? -m : m;
+    return __uint_as_float(__float_as_uint(m) | ((__float_as_uint(a) ^ __float_as_uint(b)) & 0x80000000u));
 }
 // corrected Eq. (2): g = a_hi + (1 - 2 beta) a_lo (reading R1); a_hi - a_lo is
 // a_hi + (-a_lo) exactly, so flipping the sign bit of a_lo is exact.
@@ -60,40 +64,35 @@ __device__ __forceinline__ void alpha_stage(const float *chan, float *alpha, con
     const bool top = (s + 1 == n);
     const float *src = top ? chan : alpha + (2 << s);
     float *dst = alpha + Ls;
-    if ((psi & 1) == 0) {
-        if (Ls >= 128) {
-            #pragma unroll 1
-            for (int i = lane * 4; i < Ls; i += 128) {
-                const float4 lo = ld4<CHAN_SMEM>(src + i, top);
-                const float4 hi = ld4<CHAN_SMEM>(src + Ls + i, top);
-                float4 o;
-                o.x = f_minsum(lo.x, hi.x); o.y = f_minsum(lo.y, hi.y);
-                o.z = f_minsum(lo.z, hi.z); o.w = f_minsum(lo.w, hi.w);
-                *reinterpret_cast<float4 *>(dst + i) = o;
-            }
+    const bool odd = (psi & 1) != 0;
+    const int boff = (psi - 1) << s;                 // left sibling's segment of the flat beta
+    if (Ls == 64) {
+        // two elements per lane: lane and lane + 32
+        const float lo0 = ld1<CHAN_SMEM>(src + lane, top), lo1 = ld1<CHAN_SMEM>(src + 32 + lane, top);
+        const float hi0 = ld1<CHAN_SMEM>(src + 64 + lane, top), hi1 = ld1<CHAN_SMEM>(src + 96 + lane, top);
+        if (odd) {
+            const uint32_t w0 = beta[boff >> 5], w1 = beta[(boff >> 5) + 1];
+            dst[lane] = g_exact(lo0, hi0, (w0 >> lane) & 1u);
+            dst[32 + lane] = g_exact(lo1, hi1, (w1 >> lane) & 1u);
         } else {
-            #pragma unroll 1
-            for (int i = lane; i < Ls; i += 32) dst[i] = f_minsum(ld1<CHAN_SMEM>(src + i, top), ld1<CHAN_SMEM>(src + i + Ls, top));
+            dst[lane] = f_minsum(lo0, hi0);
+            dst[32 + lane] = f_minsum(lo1, hi1);
         }
     } else {
-        const int boff = (psi - 1) * Ls;            // left sibling's segment of the flat beta
-        if (Ls >= 128) {
-            #pragma unroll 1
-            for (int i = lane * 4; i < Ls; i += 128) {
-                const float4 lo = ld4<CHAN_SMEM>(src + i, top);
-                const float4 hi = ld4<CHAN_SMEM>(src + Ls + i, top);
+        #pragma unroll 1
+        for (int i = lane * 4; i < Ls; i += 128) {
+            const float4 lo = ld4<CHAN_SMEM>(src + i, top);
+            const float4 hi = ld4<CHAN_SMEM>(src + Ls + i, top);
+            float4 o;
+            if (odd) {
                 const uint32_t b = beta[(boff + i) >> 5] >> ((boff + i) & 31);
-                float4 o;
                 o.x = g_exact(lo.x, hi.x, b & 1); o.y = g_exact(lo.y, hi.y, (b >> 1) & 1);
                 o.z = g_exact(lo.z, hi.z, (b >> 2) & 1); o.w = g_exact(lo.w, hi.w, (b >> 3) & 1);
-                *reinterpret_cast<float4 *>(dst + i) = o;
+            } else {
+                o.x = f_minsum(lo.x, hi.x); o.y = f_minsum(lo.y, hi.y);
+                o.z = f_minsum(lo.z, hi.z); o.w = f_minsum(lo.w, hi.w);
             }
-        } else {
-            #pragma unroll 1
-            for (int i = lane; i < Ls; i += 32) {
-                const int p = boff + i;
-                dst[i] = g_exact(ld1<CHAN_SMEM>(src + i, top), ld1<CHAN_SMEM>(src + i + Ls, top), (beta[p >> 5] >> (p & 31)) & 1);
-            }
+            *reinterpret_cast<float4 *>(dst + i) = o;
         }
     }
     __syncwarp();
@@ -195,8 +194,9 @@ fsscs_decode_kernel(const DecodeParams P) {
     uint32_t *beta = reinterpret_cast<uint32_t *>(alpha + N);
     uint32_t *best = beta + nw;
     uint16_t *cnt = reinterpret_cast<uint16_t *>(best + nw);
+    uint32_t *shdr = best + nw + P.cnt_words;                      // fork headers m1..m4, 2 words/slot
     uint32_t *snap;
-    if (SNAP_SMEM) snap = best + nw + P.cnt_words;
+    if (SNAP_SMEM) snap = shdr + 2 * D;
     else snap = P.snap_global + (size_t)(blockIdx.x * kDecodeWarps + warp) * (size_t)D * P.snap_stride;
     const int sstride = P.snap_stride;
 
@@ -365,8 +365,7 @@ fsscs_decode_kernel(const DecodeParams P) {
                             beta[seg >> 5] ^= ((1u << Lam) - 1u) << (seg & 31);
                         }
                     } else if (lane == 0) {
-                        const uint32_t h0 = SNAP_SMEM ? src[nw] : __ldcg(src + nw);
-                        const uint32_t h1 = SNAP_SMEM ? src[nw + 1] : __ldcg(src + nw + 1);
+                        const uint32_t h0 = shdr[2 * ps], h1 = shdr[2 * ps + 1];
                         const uint32_t m[4] = {h0 & 0xFFFFu, h0 >> 16, h1 & 0xFFFFu, h1 >> 16};
 #pragma unroll
                         for (int q = 0; q < 4; q++)
@@ -440,34 +439,46 @@ fsscs_decode_kernel(const DecodeParams P) {
                 const int s_hi = s_min - 1;
                 #pragma unroll 1
                 for (int s = s_hi; s >= max(lam, 6); s--) alpha_stage<CHAN_SMEM>(chan, alpha, beta, n, s, pl >> s, lane);
-                // register stages: lo = element i, hi = element i + Lambda by shuffle;
-                // the last one computed is the node's own stage
-#pragma unroll
-                for (int t = 5; t >= 0; t--) {
-                    if (t <= s_hi && t >= lam) {
-                        const int Lt = 1 << t;
-                        float lo, hi;
-                        if (t + 1 == n) {
-                            lo = (lane < Lt) ? ld1<CHAN_SMEM>(chan + lane, true) : 0.f;
-                            hi = (lane < Lt) ? ld1<CHAN_SMEM>(chan + Lt + lane, true) : 0.f;
-                        } else if (t == 5) {
-                            lo = alpha[64 + lane];
-                            hi = alpha[96 + lane];
-                        } else {
-                            lo = r[t + 1];
-                            hi = __shfl_down_sync(FULL, r[t + 1], Lt);
-                        }
-                        const int psi = pl >> t;
-                        if (psi & 1) {
-                            const int boff = (psi - 1) << t;
-                            const uint32_t bit = (beta[boff >> 5] >> (((boff & 31) + lane) & 31)) & 1u;
-                            r[t] = g_exact(lo, hi, bit);
-                        } else {
-                            r[t] = f_minsum(lo, hi);
-                        }
-                        xr = r[t];
+                // register stages (Lambda <= 32): lo = element i, hi = element i + Lambda
+                // by shuffle; enter the cascade at the first stage to compute, leave
+                // after the node's own stage (its value is the node input xr)
+#define POLAR_RSTAGE(T)                                                                    \
+    {                                                                                      \
+        const int Lt = 1 << (T);                                                           \
+        float lo, hi;                                                                      \
+        if ((T) + 1 == n) {                                                                \
+            lo = ld1<CHAN_SMEM>(chan + (lane & (Lt - 1)), true);                            \
+            hi = ld1<CHAN_SMEM>(chan + Lt + (lane & (Lt - 1)), true);                       \
+        } else if ((T) == 5) {                                                             \
+            lo = alpha[64 + lane];                                                         \
+            hi = alpha[96 + lane];                                                         \
+        } else {                                                                           \
+            lo = r[((T) + 1) % 6];                                                         \
+            hi = __shfl_down_sync(FULL, r[((T) + 1) % 6], Lt);                              \
+        }                                                                                  \
+        const int psi = pl >> (T);                                                         \
+        if (psi & 1) {                                                                     \
+            const int boff = (psi - 1) << (T);                                             \
+            const uint32_t bit = (beta[boff >> 5] >> (((boff & 31) + lane) & 31)) & 1u;     \
+            r[T] = g_exact(lo, hi, bit);                                                   \
+        } else {                                                                           \
+            r[T] = f_minsum(lo, hi);                                                       \
+        }                                                                                  \
+        xr = r[T];                                                                         \
+        if (lam == (T)) break;                                                             \
+    }
+                if (lam <= 5) {
+                    switch (min(s_hi, 5)) {
+                    case 5: POLAR_RSTAGE(5)
+                    case 4: POLAR_RSTAGE(4)
+                    case 3: POLAR_RSTAGE(3)
+                    case 2: POLAR_RSTAGE(2)
+                    case 1: POLAR_RSTAGE(1)
+                    case 0: POLAR_RSTAGE(0)
+                    default: break;
                     }
                 }
+#undef POLAR_RSTAGE
                 pos_mem = pl;
                 lev_mem = lam + 1;
             }
@@ -649,8 +660,8 @@ fsscs_decode_kernel(const DecodeParams P) {
                 #pragma unroll 1
                 for (int w = lane; w < nwords; w += 32) dst[w] = beta[w];
                 if (lane == 0) {
-                    dst[nw] = mi[0] | (mi[1] << 16);
-                    dst[nw + 1] = mi[2] | (mi[3] << 16);
+                    shdr[2 * fslot] = mi[0] | (mi[1] << 16);
+                    shdr[2 * fslot + 1] = mi[2] | (mi[3] << 16);
                 }
             };
             if (nfit > 1) write_fork_snapshot(-1, 0);

@@ -50,7 +50,7 @@ struct DecodeParams {
     uint32_t *snap_global;      // arena when snapshots live in global memory
     int N, n, K, c, D, L, M;
     int nw;                     // beta words = max(1, N/32)
-    int snap_stride;            // words per snapshot slot = nw + 2 (header: m1..m4)
+    int snap_stride;            // words per snapshot slot = nw (headers m1..m4 in shared memory)
     int sched_words;            // node-table words staged in shared memory (0 = read global)
     int warp_words;             // shared-memory words per warp
     int cnt_words;              // words of the per-length counters (u16 each)
