@@ -195,10 +195,14 @@ fsscs_decode_kernel(const DecodeParams P) {
     uint32_t *best = beta + nw;
     uint16_t *cnt = reinterpret_cast<uint16_t *>(best + nw);
     uint32_t *shdr = best + nw + P.cnt_words;                      // fork headers m1..m4, 2 words/slot
-    uint32_t *snap;
-    if (SNAP_SMEM) snap = shdr + 2 * D;
-    else snap = P.snap_global + (size_t)(blockIdx.x * kDecodeWarps + warp) * (size_t)D * P.snap_stride;
+    // snapshot slot k of this warp: shared memory, or global slot index snap0 + k
+    uint32_t *snap_s = shdr + 2 * D;
+    const uint32_t snap0 = (uint32_t)(blockIdx.x * kDecodeWarps + warp) * (uint32_t)D;
     const int sstride = P.snap_stride;
+    auto snap_slot = [&](int k) -> uint32_t * {
+        if (SNAP_SMEM) return snap_s + k * sstride;
+        return P.snap_global + (size_t)(snap0 + (uint32_t)k) * (size_t)sstride;
+    };
 
     // frame queue: each warp holds the frame it decodes and the next one it
     // claimed, whose LLR row is prefetched into L2 meanwhile
@@ -257,8 +261,11 @@ fsscs_decode_kernel(const DecodeParams P) {
 
         #pragma unroll 1
         for (;;) {
-            if (nS == 0) { from_best = true; out_pm = best_pm; status = 1; break; }   // reading R13
-            if (pops >= pop_cap) { status = 2; out_pm = -1.f; break; }   // watchdog: cannot happen (cnt[j] <= L)
+            if (nS == 0 || pops >= pop_cap) {
+                if (nS == 0) { from_best = true; out_pm = best_pm; status = 1; }   // reading R13
+                else { status = 2; out_pm = -1.f; }        // watchdog: cannot happen (cnt[j] <= L)
+                break;
+            }
             // ---- select: min (PM, serial) (reading R7)
             uint32_t lpm = EMPTY, lser = EMPTY, ljsm = 0;
             int ls = 0;
@@ -319,7 +326,7 @@ fsscs_decode_kernel(const DecodeParams P) {
                     const int wslot = __shfl_sync(FULL, wsl, wl);
                     if (jsm_snap(wj) == SNAP_NONE) {
                         const int slot = alloc_snapshot<SLOTS>(s_ser, s_jsm, D, -1, 0, jsm_snap(p_jsm), lane);
-                        uint32_t *dst = snap + (size_t)slot * sstride;
+                        uint32_t *dst = snap_slot(slot);
                         const int nwords = (work_pl + 31) >> 5;
                         #pragma unroll 1
                         for (int w = lane; w < nwords; w += 32) dst[w] = beta[w];
@@ -333,7 +340,7 @@ fsscs_decode_kernel(const DecodeParams P) {
                 // restore p's beta (fork snapshot), locating the first bit d where it
                 // differs from the beta the alpha memory was computed from
                 const uint32_t ps = jsm_snap(p_jsm), rel = jsm_mask(p_jsm);
-                const uint32_t *src = snap + (size_t)ps * sstride;
+                const uint32_t *src = snap_slot((int)ps);
                 const int nwords = (pl + 31) >> 5;
                 int d = 0x7FFFFFFF;
                 #pragma unroll 1
@@ -586,9 +593,10 @@ fsscs_decode_kernel(const DecodeParams P) {
                     }
                     // least reliable: the lane is the index, so ties go to the lowest lane
                     uint32_t key = (lane < Lam) ? __float_as_uint(fabsf(xr)) : 0xFFFFFFFFu;
+                    const int rounds = min(need, Lam);
 #pragma unroll
                     for (int r = 0; r < 4; r++) {
-                        if (r < need && r < Lam) {
+                        if (r < rounds) {
                             const uint32_t mh = __reduce_min_sync(FULL, key);
                             const int ml = __ffs(__ballot_sync(FULL, key == mh)) - 1;
                             mi[r] = (uint32_t)ml;
@@ -615,10 +623,10 @@ fsscs_decode_kernel(const DecodeParams P) {
             if (sum_kind) {
                 my_d = my_m ? vp : vn;
             } else {
-                bool first = true;
+                // 0 + x = x and d + 0 = d exactly (all terms >= +0), so this equals the
+                // ordered sum of the flipped terms
 #pragma unroll
-                for (int q = 0; q < 4; q++)
-                    if ((my_m >> q) & 1u) { my_d = first ? A[q] : my_d + A[q]; first = false; }
+                for (int q = 0; q < 4; q++) my_d = my_d + (((my_m >> q) & 1u) ? A[q] : 0.f);
             }
 
             // ---- c1 continues in the working memory ------------------------
@@ -655,7 +663,7 @@ fsscs_decode_kernel(const DecodeParams P) {
             const int nfit = min(nc, D - nS);
             auto write_fork_snapshot = [&](int victim_lane, int victim_slot) {
                 fslot = alloc_snapshot<SLOTS>(s_ser, s_jsm, D, victim_lane, victim_slot, SNAP_NONE, lane);
-                uint32_t *dst = snap + (size_t)fslot * sstride;
+                uint32_t *dst = snap_slot(fslot);
                 const int nwords = (npl + 31) >> 5;
                 #pragma unroll 1
                 for (int w = lane; w < nwords; w += 32) dst[w] = beta[w];
@@ -669,6 +677,7 @@ fsscs_decode_kernel(const DecodeParams P) {
             {
                 int base = 0;
                 bool c1_found = false;
+                const uint32_t jbase = jsm_make(jn, (nfit == 1) ? SNAP_NONE : (uint32_t)fslot, 0);
 #pragma unroll
                 for (int s = 0; s < SLOTS; s++) {
                     const bool fr = (s_ser[s] == EMPTY);
@@ -679,7 +688,7 @@ fsscs_decode_kernel(const DecodeParams P) {
                         const uint32_t mk = (clist >> (4 * k)) & 15u;
                         s_pm[s] = __float_as_uint(p_pm + dk);
                         s_ser[s] = ser0 + (uint32_t)k;
-                        s_jsm[s] = jsm_make(jn, (k == 0 && nfit == 1) ? SNAP_NONE : (uint32_t)fslot, mk ^ (uint32_t)m0);
+                        s_jsm[s] = jbase | ((mk ^ (uint32_t)m0) << 21);
                     }
                     const uint32_t b0 = __ballot_sync(FULL, fr && k == 0);
                     if (!c1_found && b0) { c1_found = true; c1_lane = __ffs(b0) - 1; c1_slot = s; }
