@@ -130,7 +130,7 @@ int polar_scs_decode_stats(polar_scs_t h, const float *llr, int64_t n_frames, ui
  * End-to-end decode from HOST buffers: copies llr_host ([n][N] float32) to the
  * device in chunks, decodes, and copies the bits back to out_bits_host
  * ([n][K] uint8), overlapping the copies of one chunk with the decode of the
- * other on three internal streams (H2D, decode, D2H).  Blocking: returns when out_bits_host is
+ * other on internal streams (H2D, two decode slots, D2H).  Blocking: returns when out_bits_host is
  * complete.  Pinned host memory gives full PCIe/C2C speed.  `stream` orders
  * the call after prior work on it.
  */

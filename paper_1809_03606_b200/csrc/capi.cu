@@ -48,7 +48,8 @@ void free_handle(polar_scs_t h) {
         if (h->ev_d2h[b]) cudaEventDestroy(h->ev_d2h[b]);
     }
     if (h->s_h2d) cudaStreamDestroy(h->s_h2d);
-    if (h->s_comp) cudaStreamDestroy(h->s_comp);
+    for (int b = 0; b < 2; b++)
+        if (h->s_comp[b]) cudaStreamDestroy(h->s_comp[b]);
     if (h->s_d2h) cudaStreamDestroy(h->s_d2h);
     delete h;
 }
@@ -66,12 +67,16 @@ CodecParams codec_params(polar_scs_t h, int64_t n) {
 
 int cuda_status(cudaError_t e) { return e == cudaSuccess ? POLAR_OK : (e == cudaErrorMemoryAllocation ? POLAR_ENOMEM : POLAR_ECUDA); }
 
+// slot: which frame-queue counter / snapshot arena the launch uses; two slots
+// let the host pipeline overlap one chunk's decode with the next one's
 int decode_impl(polar_scs_t h, const float *llr, int64_t n, uint8_t *bits, float *pm, uint32_t *pops,
-                uint32_t *sw, uint8_t *status, cudaStream_t st) {
+                uint32_t *sw, uint8_t *status, cudaStream_t st, int slot = 0) {
     DecodeParams p = h->base;
     p.llr = llr; p.n_frames = n; p.out_bits = bits;
     p.pm = pm; p.pops = pops; p.switches = sw; p.status = status;
-    cudaError_t e = cudaMemsetAsync(h->d_queue, 0, sizeof(unsigned long long), st);
+    p.queue = h->d_queue + slot;
+    if (h->d_snap) p.snap_global = h->d_snap + (h->snap_bytes / 4) * (size_t)slot;
+    cudaError_t e = cudaMemsetAsync(p.queue, 0, sizeof(unsigned long long), st);
     if (e != cudaSuccess) return cuda_status(e);
     return cuda_status(launch_decode(p, slots_for(h->D), h->snap_in_smem != 0, h->chan_in_smem != 0, h->ctas,
                                      h->smem_per_cta, st));
@@ -119,7 +124,7 @@ int polar_scs_create_ex(polar_scs_t *out, int32_t N, int32_t K, const uint8_t *f
     if (e == cudaSuccess) e = upload(&t.info, hc.info);
     if (e == cudaSuccess) e = upload(&t.crc_tab, hc.crc_tab);
     if (e == cudaSuccess) e = upload(&t.info_words, hc.info_words);
-    if (e == cudaSuccess) e = cudaMalloc(&h->d_queue, sizeof(unsigned long long));
+    if (e == cudaSuccess) e = cudaMalloc(&h->d_queue, 2 * sizeof(unsigned long long));
     if (e != cudaSuccess) { free_handle(h); return cuda_status(e); }
 
     // ---- decode launch layout (per-warp shared memory)
@@ -175,7 +180,7 @@ int polar_scs_create_ex(polar_scs_t *out, int32_t N, int32_t K, const uint8_t *f
     h->ctas = occ * sms;
     if (!use_smem) {
         h->snap_bytes = (size_t)h->ctas * kDecodeWarps * (size_t)D * sstride * 4;
-        e = cudaMalloc(&h->d_snap, h->snap_bytes);
+        e = cudaMalloc(&h->d_snap, 2 * h->snap_bytes);
         if (e != cudaSuccess) { free_handle(h); return cuda_status(e); }
         p.snap_global = h->d_snap;
     }
@@ -222,9 +227,11 @@ int polar_scs_decode_host(polar_scs_t h, const float *llr_host, int64_t n, uint8
     if (!llr_host || !bits_host) return POLAR_EINVAL;
     const int N = h->t.N, K = h->t.K;
     cudaError_t e = cudaSuccess;
-    if (!h->s_comp) {
-        // chunk of about 128 MiB of LLRs, double-buffered
-        h->stage_frames = std::max<int64_t>(1, (int64_t)(128ll << 20) / (4ll * N));
+    if (!h->s_comp[0]) {
+        // chunks of about 256 MiB of LLRs, double-buffered; consecutive chunks
+        // decode on two streams with separate queue/arena slots, so the next
+        // chunk's CTAs fill the SMs while the previous chunk's last frames finish
+        h->stage_frames = std::max<int64_t>(1, (int64_t)(256ll << 20) / (4ll * N));
         for (int b = 0; b < 2 && e == cudaSuccess; b++) {
             e = cudaMalloc(&h->d_stage_llr[b], (size_t)h->stage_frames * N * 4);
             if (e == cudaSuccess) e = cudaMalloc(&h->d_stage_bits[b], (size_t)h->stage_frames * K);
@@ -233,7 +240,7 @@ int polar_scs_decode_host(polar_scs_t h, const float *llr_host, int64_t n, uint8
             if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_d2h[b], cudaEventDisableTiming);
         }
         if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->s_h2d, cudaStreamNonBlocking);
-        if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->s_comp, cudaStreamNonBlocking);
+        for (int b = 0; b < 2 && e == cudaSuccess; b++) e = cudaStreamCreateWithFlags(&h->s_comp[b], cudaStreamNonBlocking);
         if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->s_d2h, cudaStreamNonBlocking);
         if (e != cudaSuccess) return cuda_status(e);
     }
@@ -242,7 +249,8 @@ int polar_scs_decode_host(polar_scs_t h, const float *llr_host, int64_t n, uint8
     if (e != cudaSuccess) return cuda_status(e);
     cudaEventRecord(start, static_cast<cudaStream_t>(stream));
     cudaStreamWaitEvent(h->s_h2d, start, 0);
-    cudaStreamWaitEvent(h->s_comp, start, 0);
+    cudaStreamWaitEvent(h->s_comp[0], start, 0);
+    cudaStreamWaitEvent(h->s_comp[1], start, 0);
     int rc = POLAR_OK;
     int64_t i = 0;
     for (int64_t off = 0; off < n && rc == POLAR_OK; off += h->stage_frames, i++) {
@@ -252,10 +260,11 @@ int polar_scs_decode_host(polar_scs_t h, const float *llr_host, int64_t n, uint8
         e = cudaMemcpyAsync(h->d_stage_llr[b], llr_host + off * N, (size_t)cnt * N * 4, cudaMemcpyHostToDevice, h->s_h2d);
         if (e != cudaSuccess) { rc = cuda_status(e); break; }
         cudaEventRecord(h->ev_h2d[b], h->s_h2d);
-        cudaStreamWaitEvent(h->s_comp, h->ev_h2d[b], 0);
-        cudaStreamWaitEvent(h->s_comp, h->ev_d2h[b], 0);      // bits buffer b has been copied out
-        rc = decode_impl(h, h->d_stage_llr[b], cnt, h->d_stage_bits[b], nullptr, nullptr, nullptr, nullptr, h->s_comp);
-        cudaEventRecord(h->ev_dec[b], h->s_comp);
+        cudaStreamWaitEvent(h->s_comp[b], h->ev_h2d[b], 0);
+        cudaStreamWaitEvent(h->s_comp[b], h->ev_d2h[b], 0);   // bits buffer b has been copied out
+        rc = decode_impl(h, h->d_stage_llr[b], cnt, h->d_stage_bits[b], nullptr, nullptr, nullptr, nullptr,
+                         h->s_comp[b], b);
+        cudaEventRecord(h->ev_dec[b], h->s_comp[b]);
         cudaStreamWaitEvent(h->s_d2h, h->ev_dec[b], 0);
         e = cudaMemcpyAsync(bits_host + off * K, h->d_stage_bits[b], (size_t)cnt * K, cudaMemcpyDeviceToHost, h->s_d2h);
         if (e != cudaSuccess) { rc = cuda_status(e); break; }
@@ -263,7 +272,10 @@ int polar_scs_decode_host(polar_scs_t h, const float *llr_host, int64_t n, uint8
     }
     e = cudaStreamSynchronize(h->s_d2h);
     if (rc == POLAR_OK && e != cudaSuccess) rc = cuda_status(e);
-    e = cudaStreamSynchronize(h->s_comp);
+    for (int b = 0; b < 2; b++) {
+        const cudaError_t e2 = cudaStreamSynchronize(h->s_comp[b]);
+        if (e == cudaSuccess) e = e2;
+    }
     if (rc == POLAR_OK && e != cudaSuccess) rc = cuda_status(e);
     cudaEventDestroy(start);
     return rc;

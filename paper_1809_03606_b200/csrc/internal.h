@@ -79,15 +79,15 @@ struct polar_scs_s {
     uint32_t flags = 0;
     int D = 0, L = 0;
     polar::CodeTables t;            // device pointers
-    unsigned long long *d_queue = nullptr;
-    uint32_t *d_snap = nullptr;     // global snapshot arena (or null)
-    size_t snap_bytes = 0;
+    unsigned long long *d_queue = nullptr;  // [2] frame-queue counters (slot 0: decode API; 0/1: host pipeline)
+    uint32_t *d_snap = nullptr;     // global snapshot arena, 2 slots (or null)
+    size_t snap_bytes = 0;          // bytes per slot
     int snap_in_smem = 0;
     int chan_in_smem = 0;
     int warps_per_cta = 0, ctas = 0, smem_per_cta = 0;
     polar::DecodeParams base{};     // prefilled params
     // host-staging for polar_scs_decode_host (lazily allocated)
-    cudaStream_t s_h2d = nullptr, s_comp = nullptr, s_d2h = nullptr;
+    cudaStream_t s_h2d = nullptr, s_comp[2] = {nullptr, nullptr}, s_d2h = nullptr;
     float *d_stage_llr[2] = {nullptr, nullptr};
     uint8_t *d_stage_bits[2] = {nullptr, nullptr};
     cudaEvent_t ev_h2d[2] = {nullptr, nullptr}, ev_dec[2] = {nullptr, nullptr}, ev_d2h[2] = {nullptr, nullptr};
