@@ -14,7 +14,7 @@
 namespace polar {
 cudaError_t launch_decode(const DecodeParams &p, int slots, bool snap_smem, bool chan_smem, int ctas, int smem,
                           cudaStream_t st);
-cudaError_t decode_occupancy(int slots, bool snap_smem, bool chan_smem, int smem, int *blocks_per_sm);
+cudaError_t decode_occupancy(int n, int slots, bool snap_smem, bool chan_smem, int smem, int *blocks_per_sm);
 cudaError_t launch_crc_attach(const CodecParams &p, cudaStream_t st);
 cudaError_t launch_encode(const CodecParams &p, cudaStream_t st);
 cudaError_t launch_modulate(const CodecParams &p, cudaStream_t st);
@@ -161,7 +161,7 @@ int polar_scs_create_ex(polar_scs_t *out, int32_t N, int32_t K, const uint8_t *f
             const int smem = 4 * (sched_words + kDecodeWarps * ww);
             if (smem > optin) continue;
             int occ = 0;
-            if (decode_occupancy(slots, snap_smem, chan_smem, smem, &occ) != cudaSuccess || occ < 1) continue;
+            if (decode_occupancy(t.n, slots, snap_smem, chan_smem, smem, &occ) != cudaSuccess || occ < 1) continue;
             if (occ > best_occ) {
                 best_occ = occ; best_smem = smem; best_ww = ww; best_snap = snap_smem; best_chan = chan_smem;
             }

@@ -171,13 +171,18 @@ __device__ __forceinline__ int alloc_snapshot(const uint32_t (&s_ser)[SLOTS], co
     return slot;
 }
 
-template <int SLOTS, bool SNAP_SMEM, bool CHAN_SMEM>
+// NL > 0: compile-time code length 2^NL (stage sizes and shifts fold to
+// constants); NL = 0: any N at run time.
+template <int SLOTS, bool SNAP_SMEM, bool CHAN_SMEM, int NL = 0>
 __global__ void __launch_bounds__(kDecodeWarps * 32, SLOTS == 4 ? kDecodeMinBlocks - 2 : kDecodeMinBlocks)
 fsscs_decode_kernel(const DecodeParams P) {
     extern __shared__ __align__(16) uint32_t smem[];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
-    const int N = P.N, n = P.n, K = P.K, D = P.D, nw = P.nw, M = P.M;
+    const int n = (NL > 0) ? NL : P.n;
+    const int N = 1 << n;
+    const int nw = (NL > 0) ? (NL >= 5 ? (1 << NL) / 32 : 1) : P.nw;
+    const int K = P.K, D = P.D, M = P.M;
 
     // node table (kind, lambda, phi of every decision node, schedule order) in
     // shared memory when it fits: the schedule walk is derived from it
@@ -445,7 +450,28 @@ fsscs_decode_kernel(const DecodeParams P) {
                 s_min = min(s_min, n);
                 const int s_hi = s_min - 1;
                 #pragma unroll 1
-                for (int s = s_hi; s >= max(lam, 6); s--) alpha_stage<CHAN_SMEM>(chan, alpha, beta, n, s, pl >> s, lane);
+                if constexpr (NL > 0) {
+                    // shared-memory stages with compile-time sizes: enter at s_hi
+#define POLAR_SSTAGE(T)                                                                       \
+    if constexpr ((T) < NL && (T) >= 6) {                                                     \
+        if ((T) < lam) break;                                                                 \
+        alpha_stage<CHAN_SMEM>(chan, alpha, beta, n, (T), pl >> (T), lane);                   \
+    }
+                    switch (s_hi) {
+                    case 12: POLAR_SSTAGE(12)
+                    case 11: POLAR_SSTAGE(11)
+                    case 10: POLAR_SSTAGE(10)
+                    case 9: POLAR_SSTAGE(9)
+                    case 8: POLAR_SSTAGE(8)
+                    case 7: POLAR_SSTAGE(7)
+                    case 6: POLAR_SSTAGE(6)
+                    default: break;
+                    }
+#undef POLAR_SSTAGE
+                } else {
+                    #pragma unroll 1
+                    for (int s = s_hi; s >= max(lam, 6); s--) alpha_stage<CHAN_SMEM>(chan, alpha, beta, n, s, pl >> s, lane);
+                }
                 // register stages (Lambda <= 32): lo = element i, hi = element i + Lambda
                 // by shuffle; enter the cascade at the first stage to compute, leave
                 // after the node's own stage (its value is the node input xr)
@@ -754,9 +780,9 @@ fsscs_decode_kernel(const DecodeParams P) {
     }
 }
 
-template <int SLOTS, bool SM, bool CS>
+template <int SLOTS, bool SM, bool CS, int NL = 0>
 static cudaError_t launch_t(const DecodeParams &p, int ctas, int smem, cudaStream_t st) {
-    auto kern = fsscs_decode_kernel<SLOTS, SM, CS>;
+    auto kern = fsscs_decode_kernel<SLOTS, SM, CS, NL>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     kern<<<ctas, kDecodeWarps * 32, smem, st>>>(p);
@@ -770,17 +796,34 @@ static cudaError_t launch_s(const DecodeParams &p, int slots, int ctas, int smem
     return launch_t<4, SM, CS>(p, ctas, smem, st);
 }
 
+// code-length-specialised instantiations: the BASELINE configs in the
+// placements create() picks for them
+int specialised_nl(int n, int slots, bool snap_smem, bool chan_smem) {
+    if (n == 7 && slots == 1 && snap_smem && chan_smem) return 7;
+    if (n == 10 && slots == 1 && !snap_smem && !chan_smem) return 10;
+    if (n == 11 && slots == 2 && !snap_smem && !chan_smem) return 11;
+    if (n == 12 && slots == 4 && !snap_smem && !chan_smem) return 12;
+    return 0;
+}
+
 cudaError_t launch_decode(const DecodeParams &p, int slots, bool snap_smem, bool chan_smem, int ctas, int smem,
                           cudaStream_t st) {
+    switch (specialised_nl(p.n, slots, snap_smem, chan_smem)) {
+    case 7: return launch_t<1, true, true, 7>(p, ctas, smem, st);
+    case 10: return launch_t<1, false, false, 10>(p, ctas, smem, st);
+    case 11: return launch_t<2, false, false, 11>(p, ctas, smem, st);
+    case 12: return launch_t<4, false, false, 12>(p, ctas, smem, st);
+    default: break;
+    }
     if (snap_smem) return chan_smem ? launch_s<true, true>(p, slots, ctas, smem, st) : launch_s<true, false>(p, slots, ctas, smem, st);
     return chan_smem ? launch_s<false, true>(p, slots, ctas, smem, st) : launch_s<false, false>(p, slots, ctas, smem, st);
 }
 
-template <int S, bool B, bool C>
+template <int S, bool B, bool C, int NL = 0>
 static cudaError_t occ_t(int smem, int *blocks) {
-    cudaError_t e = cudaFuncSetAttribute(fsscs_decode_kernel<S, B, C>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaError_t e = cudaFuncSetAttribute(fsscs_decode_kernel<S, B, C, NL>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, fsscs_decode_kernel<S, B, C>, kDecodeWarps * 32, smem);
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, fsscs_decode_kernel<S, B, C, NL>, kDecodeWarps * 32, smem);
 }
 template <bool B, bool C>
 static cudaError_t occ_s(int slots, int smem, int *blocks) {
@@ -789,7 +832,14 @@ static cudaError_t occ_s(int slots, int smem, int *blocks) {
     return occ_t<4, B, C>(smem, blocks);
 }
 
-cudaError_t decode_occupancy(int slots, bool snap_smem, bool chan_smem, int smem, int *blocks_per_sm) {
+cudaError_t decode_occupancy(int n, int slots, bool snap_smem, bool chan_smem, int smem, int *blocks_per_sm) {
+    switch (specialised_nl(n, slots, snap_smem, chan_smem)) {
+    case 7: return occ_t<1, true, true, 7>(smem, blocks_per_sm);
+    case 10: return occ_t<1, false, false, 10>(smem, blocks_per_sm);
+    case 11: return occ_t<2, false, false, 11>(smem, blocks_per_sm);
+    case 12: return occ_t<4, false, false, 12>(smem, blocks_per_sm);
+    default: break;
+    }
     if (snap_smem) return chan_smem ? occ_s<true, true>(slots, smem, blocks_per_sm) : occ_s<true, false>(slots, smem, blocks_per_sm);
     return chan_smem ? occ_s<false, true>(slots, smem, blocks_per_sm) : occ_s<false, false>(slots, smem, blocks_per_sm);
 }
