@@ -132,7 +132,7 @@ int polar_scs_create_ex(polar_scs_t *out, int32_t N, int32_t K, const uint8_t *f
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, h->device);
     cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, h->device);
     const int nw = std::max(1, N / 32);
-    const int cnt_words = ((t.M + 1) * 2 + 3) / 4;
+    const int cnt_words = (((t.M + 1) * 2 + 3) / 4 + 1) & ~1;   // even: the fork headers that follow are uint2
     const int sstride = nw;                       // snapshot slot: beta words (headers live in smem)
     const int sched_words = (t.M * 4 <= 16384) ? round4(t.M) : 0;
     const int slots = slots_for(D);

@@ -203,7 +203,7 @@ fsscs_decode_kernel(const DecodeParams P) {
     // snapshot slot k of this warp: shared memory, or global slot index snap0 + k
     uint32_t *snap_s = shdr + 2 * D;
     const uint32_t snap0 = (uint32_t)(blockIdx.x * kDecodeWarps + warp) * (uint32_t)D;
-    const int sstride = P.snap_stride;
+    const int sstride = (NL > 0) ? nw : P.snap_stride;
     auto snap_slot = [&](int k) -> uint32_t * {
         if (SNAP_SMEM) return snap_s + k * sstride;
         return P.snap_global + (size_t)(snap0 + (uint32_t)k) * (size_t)sstride;
@@ -377,7 +377,8 @@ fsscs_decode_kernel(const DecodeParams P) {
                             beta[seg >> 5] ^= ((1u << Lam) - 1u) << (seg & 31);
                         }
                     } else if (lane == 0) {
-                        const uint32_t h0 = shdr[2 * ps], h1 = shdr[2 * ps + 1];
+                        const uint2 hh = reinterpret_cast<const uint2 *>(shdr)[ps];
+                        const uint32_t h0 = hh.x, h1 = hh.y;
                         const uint32_t m[4] = {h0 & 0xFFFFu, h0 >> 16, h1 & 0xFFFFu, h1 >> 16};
 #pragma unroll
                         for (int q = 0; q < 4; q++)
@@ -542,6 +543,7 @@ fsscs_decode_kernel(const DecodeParams P) {
             float vn = 0.f, vp = 0.f;
             float A[4] = {0.f, 0.f, 0.f, 0.f};
             uint32_t mi[4] = {0, 0, 0, 0};
+            uint32_t hdw_node = 0;             // HD word of a Lambda <= 32 R1/SPC node
             const bool sum_kind = (kind == OP_R0 || kind == OP_REP);
 
             if (sum_kind) {
@@ -609,27 +611,24 @@ fsscs_decode_kernel(const DecodeParams P) {
                         }
                     }
                 } else {
-                    const uint32_t hdw = __ballot_sync(FULL, lane < Lam && xr < 0.f);
-                    par = (uint32_t)__popc(hdw);
-                    if (lane == 0) {
-                        // HD word of the node (Lam <= 32 bits) into beta; c1's flips applied below
-                        const uint32_t lm = (Lam == 32) ? FULL : (1u << Lam) - 1u;
-                        const int w = seg >> 5, o = seg & 31;
-                        beta[w] = (beta[w] & ~(lm << o)) | ((hdw & lm) << o);
-                    }
+                    hdw_node = __ballot_sync(FULL, lane < Lam && xr < 0.f);   // written with c1's flips below
+                    par = (uint32_t)__popc(hdw_node);
                     // least reliable: the lane is the index, so ties go to the lowest lane
                     uint32_t key = (lane < Lam) ? __float_as_uint(fabsf(xr)) : 0xFFFFFFFFu;
-                    const int rounds = min(need, Lam);
-#pragma unroll
-                    for (int r = 0; r < 4; r++) {
-                        if (r < rounds) {
-                            const uint32_t mh = __reduce_min_sync(FULL, key);
-                            const int ml = __ffs(__ballot_sync(FULL, key == mh)) - 1;
-                            mi[r] = (uint32_t)ml;
-                            A[r] = __uint_as_float(mh);
-                            if (lane == ml) key = 0xFFFFFFFFu;
-                        }
+#define POLAR_LR_ROUND(R)                                                       \
+    {                                                                           \
+        const uint32_t mh = __reduce_min_sync(FULL, key);                       \
+        const int ml = __ffs(__ballot_sync(FULL, key == mh)) - 1;               \
+        mi[R] = (uint32_t)ml;                                                   \
+        A[R] = __uint_as_float(mh);                                             \
+        if (lane == ml) key = 0xFFFFFFFFu;                                      \
+    }
+                    POLAR_LR_ROUND(0)
+                    if (Lam > 1) {
+                        POLAR_LR_ROUND(1)
+                        if (kind == OP_SPC) { POLAR_LR_ROUND(2) POLAR_LR_ROUND(3) }
                     }
+#undef POLAR_LR_ROUND
                 }
                 par &= 1u;
                 if (kind == OP_R1) {
@@ -667,6 +666,16 @@ fsscs_decode_kernel(const DecodeParams P) {
                         const uint32_t lm = ((1u << Lam) - 1u) << (seg & 31);
                         beta[seg >> 5] = (beta[seg >> 5] & ~lm) | (fill & lm);
                     }
+                } else if (Lam <= 32) {
+                    if (lane == 0) {                      // HD word with c1's flips, one RMW
+                        uint32_t wv = hdw_node;
+#pragma unroll
+                        for (int q = 0; q < 4; q++)
+                            if ((m0 >> q) & 1) wv ^= 1u << mi[q];
+                        const uint32_t lm = (Lam == 32) ? FULL : (1u << Lam) - 1u;
+                        const int w = seg >> 5, o = seg & 31;
+                        beta[w] = (beta[w] & ~(lm << o)) | ((wv & lm) << o);
+                    }
                 } else if (lane == 0 && m0) {
 #pragma unroll
                     for (int q = 0; q < 4; q++)
@@ -694,8 +703,7 @@ fsscs_decode_kernel(const DecodeParams P) {
                 #pragma unroll 1
                 for (int w = lane; w < nwords; w += 32) dst[w] = beta[w];
                 if (lane == 0) {
-                    shdr[2 * fslot] = mi[0] | (mi[1] << 16);
-                    shdr[2 * fslot + 1] = mi[2] | (mi[3] << 16);
+                    reinterpret_cast<uint2 *>(shdr)[fslot] = make_uint2(mi[0] | (mi[1] << 16), mi[2] | (mi[3] << 16));
                 }
             };
             if (nfit > 1) write_fork_snapshot(-1, 0);
