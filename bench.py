@@ -51,6 +51,8 @@ def parse():
     ap.add_argument("--snap-smem", action="store_true")
     ap.add_argument("--chan-global", action="store_true")
     ap.add_argument("--chan-smem", action="store_true")
+    ap.add_argument("--bit-level", action="store_true",
+                    help="bit-level SCS-RM (leaf-only schedule; the paper's SCS-RM comparator, PAPER.md:L797-813)")
     return ap.parse_args()
 
 
@@ -63,7 +65,8 @@ def dist_env():
 
 def workload_name(cfg, c):
     crc = {0: "no CRC", 0x11021: "CRC-16 0x1021", 0x107: "CRC-8 0x07"}[c["crc_poly"]]
-    return (f"{cfg}: PC({c['N']},{c['K']}) Bhattacharyya@{c['design_db']}dB, {crc}, D={c['D']}, L={c['L']}, "
+    mode = "bit-level SCS-RM" if c.get("bit_level") else "FSSCS-RM"
+    return (f"{cfg}: {mode} PC({c['N']},{c['K']}) Bhattacharyya@{c['design_db']}dB, {crc}, D={c['D']}, L={c['L']}, "
             f"{c['frames']} frames x Eb/N0 {c['ebno']} dB, BPSK-AWGN float32 LLRs, seed {c['seed']}")
 
 
@@ -127,7 +130,7 @@ def oracle_sample(cfg, c, seconds, rank=0):
     import oracle as O
     threads = os.cpu_count() or 1
     fr = O.bhattacharyya_mask(c["N"], c["K"], c["design_db"])
-    dec = O.SCSDecoder(fr, c["D"], c["L"], c["crc_poly"])
+    dec = O.SCSDecoder(fr, c["D"], c["L"], c["crc_poly"], bit_level=bool(c.get("bit_level")))
     cc = O.crc_degree(c["crc_poly"]) if c["crc_poly"] else 0
     # calibrate on a small prefix, then size the sample for ~`seconds` of work
     per_point = max(threads, 64)
@@ -144,13 +147,13 @@ def oracle_sample(cfg, c, seconds, rank=0):
             dec.decode(l, threads=threads)
         dt = time.perf_counter() - t0
         rounds += 1
-        if dt > 0.2 * seconds or rounds >= 6:
+        if dt > 0.2 * seconds or rounds >= 6 or nf >= c["frames"]:
             total_frames, total_t = nf * len(c["ebno"]), dt
-            if dt < 0.8 * seconds and rounds < 6:
-                per_point = int(per_point * max(1.5, 0.9 * seconds / max(dt, 1e-3)))
+            if dt < 0.8 * seconds and rounds < 6 and nf < c["frames"]:
+                per_point = min(c["frames"], int(per_point * max(1.5, 0.9 * seconds / max(dt, 1e-3))))
                 continue
             break
-        per_point = int(per_point * min(8.0, max(2.0, 0.5 * seconds / max(dt, 1e-3))))
+        per_point = min(c["frames"], int(per_point * min(8.0, max(2.0, 0.5 * seconds / max(dt, 1e-3)))))
     fps = total_frames / total_t
     return {
         "value": fps * c["K"] / 1e6, "unit": "Mbps", "cores": threads, "kind": "oracle",
@@ -201,7 +204,8 @@ def run_ours(args, cfg, c):
     npts = len(c["ebno"])
     frames = nf * npts
     fr = P.bhattacharyya_mask(c["N"], c["K"], c["design_db"])
-    dec = P.PolarSCS(fr, c["D"], c["L"], c["crc_poly"], snap_global=args.snap_global, snap_smem=args.snap_smem,
+    dec = P.PolarSCS(fr, c["D"], c["L"], c["crc_poly"], bit_level=bool(c.get("bit_level")),
+                     snap_global=args.snap_global, snap_smem=args.snap_smem,
                      chan_global=args.chan_global, chan_smem=args.chan_smem)
     K, N = c["K"], c["N"]
 
@@ -298,8 +302,13 @@ def run_ours(args, cfg, c):
     kern_s = statistics.median(launch_ms) / 1e3
     alg_bytes = frames * (4 * N + K)
     achieved_gbs = alg_bytes / kern_s / 1e9
+    traffic = None
+    tfile = os.path.join(ROOT, "profiles", f"decode_traffic_{cfg}.json")
+    if os.path.exists(tfile) and not c.get("bit_level"):
+        with open(tfile) as fh:
+            traffic = json.load(fh)["bytes_per_frame"] * frames     # ncu dram bytes, scaled to this launch
     roofline_hbm = {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm_peak, "unit": "GB/s",
-                    "frac": achieved_gbs / hbm_peak, "traffic": None,
+                    "frac": achieved_gbs / hbm_peak, "traffic": traffic, "algorithmic_bytes": alg_bytes,
                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6.65 TB/s"}
     # ALU roofline: algorithmic lane-ops per frame counted by the oracle (O10) on
     # a sample of the same workload, scaled to the batch; peak = 148 SMs x 128
@@ -312,7 +321,7 @@ def run_ours(args, cfg, c):
             alu_peak = 148 * 128 * sm_max * 1e6 / 1e12       # Tops/s
             achieved_alu = ops_per_frame * frames / kern_s / 1e12
             roofline_alu = {"bound": "alu", "achieved": achieved_alu, "peak": alu_peak, "unit": "Tops/s",
-                            "frac": achieved_alu / alu_peak, "traffic": None,
+                            "frac": achieved_alu / alu_peak, "traffic": traffic,
                             "ops_per_frame": ops_per_frame,
                             "peak_source": "148 SM x 128 lanes x sm_max_mhz (MEASURED_PEAKS.json)"}
             roofline = roofline_alu if roofline_alu["frac"] > roofline_hbm["frac"] else roofline_hbm
@@ -358,7 +367,7 @@ def oracle_ops_per_frame(c, npts, n_sample=64):
     stack key compares (D per pop and per candidate insert)."""
     import oracle as O
     fr = O.bhattacharyya_mask(c["N"], c["K"], c["design_db"])
-    dec = O.SCSDecoder(fr, c["D"], c["L"], c["crc_poly"])
+    dec = O.SCSDecoder(fr, c["D"], c["L"], c["crc_poly"], bit_level=bool(c.get("bit_level")))
     cc = O.crc_degree(c["crc_poly"]) if c["crc_poly"] else 0
     pay = ig.payload_bits(c["seed"], 0, n_sample, c["K"] - cc)
     nz = ig.unit_normals(c["seed"], 0, n_sample, c["N"])
@@ -378,6 +387,8 @@ def main():
     c = dict(ig.CONFIGS[cfg])
     if args.frames:
         c["frames"] = args.frames
+    if args.bit_level:
+        c["bit_level"] = True
     if args.impl == "reference":
         run_reference(args, cfg, c)
     else:
