@@ -39,7 +39,7 @@ int round4(int w) { return (w + 3) & ~3; }
 
 void free_handle(polar_scs_t h) {
     if (!h) return;
-    cudaFree(h->t.nodes); cudaFree(h->t.info); cudaFree(h->t.crc_tab); cudaFree(h->t.info_words);
+    cudaFree(h->t.nodes); cudaFree(h->t.info); cudaFree(h->t.crc_tab); cudaFree(h->t.crc_bytes); cudaFree(h->t.info_words);
     cudaFree(h->d_queue); cudaFree(h->d_snap);
     for (int b = 0; b < 2; b++) {
         cudaFree(h->d_stage_llr[b]); cudaFree(h->d_stage_bits[b]);
@@ -123,6 +123,7 @@ int polar_scs_create_ex(polar_scs_t *out, int32_t N, int32_t K, const uint8_t *f
     if (e == cudaSuccess) e = upload(&t.nodes, hc.nodes);
     if (e == cudaSuccess) e = upload(&t.info, hc.info);
     if (e == cudaSuccess) e = upload(&t.crc_tab, hc.crc_tab);
+    if (e == cudaSuccess) e = upload(&t.crc_bytes, hc.crc_bytes);
     if (e == cudaSuccess) e = upload(&t.info_words, hc.info_words);
     if (e == cudaSuccess) e = cudaMalloc(&h->d_queue, 2 * sizeof(unsigned long long));
     if (e != cudaSuccess) { free_handle(h); return cuda_status(e); }
@@ -138,7 +139,7 @@ int polar_scs_create_ex(polar_scs_t *out, int32_t N, int32_t K, const uint8_t *f
     const int slots = slots_for(D);
 
     DecodeParams &p = h->base;
-    p.nodes = t.nodes; p.info = t.info; p.crc_tab = t.crc_tab; p.queue = h->d_queue;
+    p.nodes = t.nodes; p.info = t.info; p.crc_tab = t.crc_tab; p.crc_bytes = t.crc_bytes; p.queue = h->d_queue;
     p.N = N; p.n = t.n; p.K = K; p.c = t.c; p.D = D; p.L = h->L; p.M = t.M;
     p.nw = nw; p.snap_stride = sstride; p.sched_words = sched_words; p.cnt_words = cnt_words;
 
@@ -157,7 +158,7 @@ int polar_scs_create_ex(polar_scs_t *out, int32_t N, int32_t K, const uint8_t *f
             const bool snap_smem = (si == 0);
             if (snap_smem && (flags & POLAR_FLAG_SNAP_GLOBAL)) continue;
             if (!snap_smem && (flags & POLAR_FLAG_SNAP_SMEM)) continue;
-            const int ww = round4((chan_smem ? N : 0) + N + 2 * nw + cnt_words + 2 * D + (snap_smem ? D * sstride : 0));
+            const int ww = round4((chan_smem ? N : 0) + N + 2 * nw + cnt_words + 2 * D + 4 + (snap_smem ? D * sstride : 0));
             const int smem = 4 * (sched_words + kDecodeWarps * ww);
             if (smem > optin) continue;
             int occ = 0;

@@ -173,8 +173,54 @@ __device__ __forceinline__ int alloc_snapshot(const uint32_t (&s_ser)[SLOTS], co
 
 // NL > 0: compile-time code length 2^NL (stage sizes and shifts fold to
 // constants); NL = 0: any N at run time.
+// Snapshot-slot allocation with a conservative used-bitmap (uniform across the
+// warp): bits are set on allocation and only cleared by an exact recount from
+// the live entries, done when the bitmap has no free slot left.
+template <int SLOTS>
+__device__ __forceinline__ int alloc_snapshot_lazy(uint32_t *used, const uint32_t (&s_ser)[SLOTS],
+                                                   const uint32_t (&s_jsm)[SLOTS], int D, int skip_lane,
+                                                   int skip_slot, uint32_t extra, int lane) {
+    if (SLOTS == 1) return alloc_snapshot<SLOTS>(s_ser, s_jsm, D, skip_lane, skip_slot, extra, lane);  // 1 REDUX: exact
+    int slot = -1;
+#pragma unroll
+    for (int w = 0; w < SLOTS; w++) {
+        const int lim = D - w * 32;
+        uint32_t freem = ~used[w];
+        if (lim < 32) freem &= (lim > 0) ? ((1u << lim) - 1u) : 0u;
+        if (slot < 0 && freem) slot = w * 32 + __ffs(freem) - 1;
+    }
+    if (slot < 0) {
+#pragma unroll
+        for (int w = 0; w < SLOTS; w++) {
+            uint32_t u = 0;
+#pragma unroll
+            for (int s = 0; s < SLOTS; s++) {
+                const uint32_t sn = jsm_snap(s_jsm[s]);
+                const bool skip = (lane == skip_lane && s == skip_slot);
+                if (s_ser[s] != EMPTY && !skip && sn != SNAP_NONE && (int)(sn >> 5) == w) u |= 1u << (sn & 31);
+            }
+            u = __reduce_or_sync(FULL, u);
+            if (extra != SNAP_NONE && (int)(extra >> 5) == w) u |= 1u << (extra & 31);
+            __syncwarp();
+            if (lane == 0) used[w] = u;
+        }
+        __syncwarp();
+#pragma unroll
+        for (int w = 0; w < SLOTS; w++) {
+            const int lim = D - w * 32;
+            uint32_t freem = ~used[w];
+            if (lim < 32) freem &= (lim > 0) ? ((1u << lim) - 1u) : 0u;
+            if (slot < 0 && freem) slot = w * 32 + __ffs(freem) - 1;
+        }
+    }
+    __syncwarp();
+    if (lane == 0) used[slot >> 5] |= 1u << (slot & 31);
+    __syncwarp();
+    return slot;
+}
+
 template <int SLOTS, bool SNAP_SMEM, bool CHAN_SMEM, int NL = 0>
-__global__ void __launch_bounds__(kDecodeWarps * 32, SLOTS == 4 ? kDecodeMinBlocks - 2 : kDecodeMinBlocks)
+__global__ void __launch_bounds__(kDecodeWarps * 32, SLOTS == 4 ? 3 : (SLOTS == 2 ? 5 : kDecodeMinBlocks))
 fsscs_decode_kernel(const DecodeParams P) {
     extern __shared__ __align__(16) uint32_t smem[];
     const int lane = threadIdx.x & 31;
@@ -186,13 +232,13 @@ fsscs_decode_kernel(const DecodeParams P) {
 
     // node table (kind, lambda, phi of every decision node, schedule order) in
     // shared memory when it fits: the schedule walk is derived from it
-    const uint32_t *nodes = P.nodes;
-    if (P.sched_words > 0) {
+    const bool nodes_smem = (NL > 0) || P.sched_words > 0;   // NL kernels: always staged (M*4 <= 16 KiB)
+    if (nodes_smem) {
         #pragma unroll 1
         for (int i = threadIdx.x; i < M; i += blockDim.x) smem[i] = P.nodes[i];
         __syncthreads();
-        nodes = smem;
     }
+    auto node_rec = [&](int jj) -> uint32_t { return nodes_smem ? smem[jj] : __ldg(P.nodes + jj); };
     uint32_t *wb = smem + P.sched_words + warp * P.warp_words;
     float *chan_s = reinterpret_cast<float *>(wb);                 // channel row (CHAN_SMEM)
     float *alpha = CHAN_SMEM ? chan_s + N : chan_s;                // stages >= 6 (+ scratch)
@@ -200,8 +246,9 @@ fsscs_decode_kernel(const DecodeParams P) {
     uint32_t *best = beta + nw;
     uint16_t *cnt = reinterpret_cast<uint16_t *>(best + nw);
     uint32_t *shdr = best + nw + P.cnt_words;                      // fork headers m1..m4, 2 words/slot
+    uint32_t *snap_used = shdr + 2 * D;                            // 4 words: snapshot-slot bitmap
     // snapshot slot k of this warp: shared memory, or global slot index snap0 + k
-    uint32_t *snap_s = shdr + 2 * D;
+    uint32_t *snap_s = shdr + 2 * D + 4;
     const uint32_t snap0 = (uint32_t)(blockIdx.x * kDecodeWarps + warp) * (uint32_t)D;
     const int sstride = (NL > 0) ? nw : P.snap_stride;
     auto snap_slot = [&](int k) -> uint32_t * {
@@ -250,6 +297,7 @@ fsscs_decode_kernel(const DecodeParams P) {
         for (int s = 0; s < SLOTS; s++) { s_pm[s] = EMPTY; s_ser[s] = EMPTY; s_jsm[s] = jsm_make(0, SNAP_NONE, 0); }
         if (lane == 0) { s_pm[0] = 0u; s_ser[0] = 0u; }
         int nS = 1;
+        if (lane < 4) snap_used[lane] = 0u;      // conservative snapshot-slot bitmap (alloc_snapshot_lazy)
         uint32_t work = 0, next_serial = 1, pops = 0, switches = 0;
         int work_pl = 0;
         // alpha memory content: stages s >= lev_mem hold the node (s, pos_mem >> s)
@@ -308,7 +356,7 @@ fsscs_decode_kernel(const DecodeParams P) {
             // position after the node that created p (its path length)
             int pl = 0, plam = 0, pphi = 0, pkind = 0;
             if (j > 0) {
-                const uint32_t pn = nodes[j - 1];
+                const uint32_t pn = node_rec(j - 1);
                 pkind = (int)op_kind(pn); plam = (int)op_lam(pn); pphi = (int)op_phi(pn);
                 pl = (pphi + 1) << plam;
             }
@@ -330,7 +378,7 @@ fsscs_decode_kernel(const DecodeParams P) {
                     wj = __shfl_sync(FULL, wj, wl);
                     const int wslot = __shfl_sync(FULL, wsl, wl);
                     if (jsm_snap(wj) == SNAP_NONE) {
-                        const int slot = alloc_snapshot<SLOTS>(s_ser, s_jsm, D, -1, 0, jsm_snap(p_jsm), lane);
+                        const int slot = alloc_snapshot_lazy<SLOTS>(snap_used, s_ser, s_jsm, D, -1, 0, jsm_snap(p_jsm), lane);
                         uint32_t *dst = snap_slot(slot);
                         const int nwords = (work_pl + 31) >> 5;
                         #pragma unroll 1
@@ -421,11 +469,15 @@ fsscs_decode_kernel(const DecodeParams P) {
                 // ---- complete path: CRC on the systematic bits
                 bool ok = true;
                 if (P.c > 0) {
+                    // syndrome = XOR of the contributions of the set systematic bits,
+                    // looked up per beta byte (tables hold information positions only)
                     uint32_t syn = 0;
                     #pragma unroll 1
-                    for (int q = lane; q < K; q += 32) {
-                        const int idx = P.info[q];
-                        if ((beta[idx >> 5] >> (idx & 31)) & 1u) syn ^= P.crc_tab[q];
+                    for (int w = lane; w < nw; w += 32) {
+                        const uint32_t x = beta[w];
+                        const uint32_t *tw = P.crc_bytes + (size_t)w * 1024;
+                        syn ^= __ldg(tw + (x & 255u)) ^ __ldg(tw + 256 + ((x >> 8) & 255u)) ^
+                               __ldg(tw + 512 + ((x >> 16) & 255u)) ^ __ldg(tw + 768 + (x >> 24));
                     }
                     syn = __reduce_xor_sync(FULL, syn);
                     ok = (syn == 0);
@@ -443,7 +495,7 @@ fsscs_decode_kernel(const DecodeParams P) {
 
             // ---- ALPHA ops down to node j (Eq. 4, Alg. 1 / Alg. 4): stage s
             // holds node (s, pl >> s); stages >= s_min are still valid
-            const uint32_t nd = nodes[j];
+            const uint32_t nd = node_rec(j);
             const int kind = (int)op_kind(nd), lam = (int)op_lam(nd), phi = (int)op_phi(nd);
             float xr = 0.f;                    // node alpha element of this lane (Lambda <= 32)
             {
@@ -697,7 +749,7 @@ fsscs_decode_kernel(const DecodeParams P) {
             int fslot = -1;
             const int nfit = min(nc, D - nS);
             auto write_fork_snapshot = [&](int victim_lane, int victim_slot) {
-                fslot = alloc_snapshot<SLOTS>(s_ser, s_jsm, D, victim_lane, victim_slot, SNAP_NONE, lane);
+                fslot = alloc_snapshot_lazy<SLOTS>(snap_used, s_ser, s_jsm, D, victim_lane, victim_slot, SNAP_NONE, lane);
                 uint32_t *dst = snap_slot(fslot);
                 const int nwords = (npl + 31) >> 5;
                 #pragma unroll 1

@@ -140,6 +140,21 @@ int build_host_code(int N, int K, const uint8_t *frozen, uint32_t crc_poly, bool
             if (carry) r ^= low;
         }
         for (int k = P; k < K; k++) hc.crc_tab[k] = 1u << (K - 1 - k);
+        // per beta byte (word w, byte b, value v): XOR of the contributions of
+        // the information positions among the set bits of v
+        std::vector<int> rank(N, -1);
+        for (int k = 0; k < K; k++) rank[info[k]] = k;
+        hc.crc_bytes.assign((size_t)nw32 * 1024, 0);
+        for (int w = 0; w < nw32; w++)
+            for (int b = 0; b < 4; b++)
+                for (int v = 0; v < 256; v++) {
+                    uint32_t acc = 0;
+                    for (int bit = 0; bit < 8; bit++) {
+                        const int pos = 32 * w + 8 * b + bit;
+                        if (((v >> bit) & 1) && pos < N && rank[pos] >= 0) acc ^= hc.crc_tab[rank[pos]];
+                    }
+                    hc.crc_bytes[(size_t)w * 1024 + 256 * b + v] = acc;
+                }
     }
     return POLAR_OK;
 }

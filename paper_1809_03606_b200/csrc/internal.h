@@ -32,6 +32,7 @@ struct CodeTables {
     uint32_t *nodes = nullptr;  int nops = 0;   // decision nodes (kind, lambda, phi) in schedule order
     uint16_t *info = nullptr;                   // A ascending, [K]
     uint32_t *crc_tab = nullptr;                // [K] syndrome contribution of block bit k
+    uint32_t *crc_bytes = nullptr;              // [nw][4][256] per beta byte (CRC codes)
     uint32_t *info_words = nullptr;             // [max(1,N/32)] bit i set iff i in A
 };
 
@@ -46,6 +47,7 @@ struct DecodeParams {
     const uint32_t *nodes;      // [M] node records; the BETA/ALPHA walk between them is implied
     const uint16_t *info;
     const uint32_t *crc_tab;
+    const uint32_t *crc_bytes;  // [nw][4][256] syndrome contribution of each beta byte (CRC codes)
     unsigned long long *queue;
     uint32_t *snap_global;      // arena when snapshots live in global memory
     int N, n, K, c, D, L, M;
@@ -104,6 +106,7 @@ struct HostCode {
     std::vector<uint32_t> nodes;    // its decision nodes only
     std::vector<uint16_t> info;
     std::vector<uint32_t> crc_tab;
+    std::vector<uint32_t> crc_bytes;
     std::vector<uint32_t> info_words;
 };
 int build_host_code(int N, int K, const uint8_t *frozen, uint32_t crc_poly, bool bit_level, HostCode &hc);
