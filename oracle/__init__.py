@@ -64,6 +64,10 @@ def lib():
             L.orc_polar_transform.argtypes = [C.c_int, u8p]
             L.orc_polar_transform.restype = None
             L.orc_encode_systematic.argtypes = [C.c_int, u8p, u8p, u8p]
+            L.orc_encode_nonsystematic.argtypes = [C.c_int, u8p, u8p, u8p]
+            L.orc_mask_from_sequence.argtypes = [C.c_int, C.c_int, C.POINTER(C.c_int32), C.c_int, u8p]
+            L.orc_scs_create_ex.argtypes = [C.c_int, u8p, C.c_int, C.c_int, C.c_uint32, C.c_int, C.c_int]
+            L.orc_scs_create_ex.restype = C.c_void_p
             L.orc_crc_bits.argtypes = [u8p, C.c_int, C.c_uint32, u8p]
             L.orc_crc_degree.argtypes = [C.c_uint32]
             L.orc_sigma.argtypes = [C.c_double, C.c_double, f32p, f32p]
@@ -109,6 +113,15 @@ def bhattacharyya_mask(N: int, K: int, design_ebno_db: float) -> np.ndarray:
     return m
 
 
+def mask_from_sequence(N: int, K: int, seq) -> np.ndarray:
+    """frozen mask from a reliability sequence, least reliable first (O1b)."""
+    seq = np.ascontiguousarray(seq, dtype=np.int32)
+    m = np.zeros(N, np.uint8)
+    if lib().orc_mask_from_sequence(N, K, _p(seq, C.c_int32), seq.size, _p(m, C.c_uint8)) != 0:
+        raise ValueError("invalid sequence / sizes")
+    return m
+
+
 def polar_transform(x) -> np.ndarray:
     x = _u8(x).copy()
     for row in x.reshape(-1, x.shape[-1]):
@@ -125,6 +138,18 @@ def encode_systematic(frozen, block) -> np.ndarray:
     for r in range(b2.shape[0]):
         row = np.ascontiguousarray(b2[r])
         lib().orc_encode_systematic(N, _p(frozen, C.c_uint8), _p(row, C.c_uint8), _p(out[r], C.c_uint8))
+    return out.reshape(block.shape[:-1] + (N,))
+
+
+def encode_nonsystematic(frozen, block) -> np.ndarray:
+    frozen = _u8(frozen)
+    block = _u8(block)
+    N = frozen.size
+    b2 = block.reshape(-1, block.shape[-1])
+    out = np.zeros((b2.shape[0], N), np.uint8)
+    for r in range(b2.shape[0]):
+        row = np.ascontiguousarray(b2[r])
+        lib().orc_encode_nonsystematic(N, _p(frozen, C.c_uint8), _p(row, C.c_uint8), _p(out[r], C.c_uint8))
     return out.reshape(block.shape[:-1] + (N,))
 
 
@@ -224,12 +249,14 @@ def sc_decode(frozen, llr):
 class SCSDecoder:
     """The FSSCS-RM engine (O7).  bit_level=True gives the bit-level SCS-RM."""
 
-    def __init__(self, frozen, D: int, L: int, crc_poly: int = 0, bit_level: bool = False):
+    def __init__(self, frozen, D: int, L: int, crc_poly: int = 0, bit_level: bool = False,
+                 nonsystematic: bool = False):
         self.frozen = _u8(frozen).copy()
         self.N = int(self.frozen.size)
         self.D, self.L, self.crc_poly, self.bit_level = int(D), int(L), int(crc_poly), bool(bit_level)
-        self._h = lib().orc_scs_create(self.N, _p(self.frozen, C.c_uint8), self.D, self.L,
-                                       self.crc_poly, int(self.bit_level))
+        self.nonsystematic = bool(nonsystematic)
+        self._h = lib().orc_scs_create_ex(self.N, _p(self.frozen, C.c_uint8), self.D, self.L,
+                                          self.crc_poly, int(self.bit_level), int(self.nonsystematic))
         if not self._h:
             raise ValueError("orc_scs_create: invalid parameters")
         self.K = int(lib().orc_scs_K(self._h))

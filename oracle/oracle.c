@@ -66,6 +66,27 @@ int orc_bhattacharyya_mask(int N, int K, double design_ebno_db, uint8_t *frozen)
     return 0;
 }
 
+/* O1b  information set from a reliability sequence, least reliable first
+ * (SPEC.md:L42-44): keep the entries < N in order; the last K are A.       */
+int orc_mask_from_sequence(int N, int K, const int32_t *seq, int len, uint8_t *frozen)
+{
+    if (ilog2(N) < 0 || K < 0 || K > N || len < N || !seq) return -1;
+    uint8_t *seen = (uint8_t *)calloc((size_t)len, 1);
+    int *sub = (int *)malloc(sizeof(int) * (size_t)N);
+    int ok = seen && sub, m = 0;
+    for (int i = 0; ok && i < len; i++) {
+        if (seq[i] < 0 || seq[i] >= len || seen[seq[i]]) ok = 0;
+        else { seen[seq[i]] = 1; if (seq[i] < N) sub[m++] = seq[i]; }
+    }
+    if (ok && m != N) ok = 0;
+    if (ok) {
+        for (int i = 0; i < N; i++) frozen[i] = 1;
+        for (int r = N - K; r < N; r++) frozen[sub[r]] = 0;
+    }
+    free(seen); free(sub);
+    return ok ? 0 : -1;
+}
+
 /* ------------------------------------------------------------------------ */
 /* O2  c = u F^{(x)n}, F = [[1,0],[1,1]]: the n-stage XOR tree of Fig. 1
  * (PAPER.md:L30-36).  Stage with span h: x[i] ^= x[i+h] for (i & h) == 0.  */
@@ -85,6 +106,15 @@ int orc_encode_systematic(int N, const uint8_t *frozen, const uint8_t *block, ui
     for (int i = 0; i < N; i++) codeword[i] = frozen[i] ? 0 : (uint8_t)(block[k++] & 1);
     orc_polar_transform(N, codeword);
     for (int i = 0; i < N; i++) if (frozen[i]) codeword[i] = 0;
+    orc_polar_transform(N, codeword);
+    return 0;
+}
+
+int orc_encode_nonsystematic(int N, const uint8_t *frozen, const uint8_t *block, uint8_t *codeword)
+{
+    if (ilog2(N) < 0) return -1;
+    int k = 0;
+    for (int i = 0; i < N; i++) codeword[i] = frozen[i] ? 0 : (uint8_t)(block[k++] & 1);
     orc_polar_transform(N, codeword);
     return 0;
 }
@@ -339,7 +369,7 @@ static void apply_candidate(int kind, int Lam, const uint8_t *seg_base, const in
  * progress (L848), j = depth = decision-node ordinal, PL, beta copy (L854)},
  * and the per-length counters cnt[0..M] (L595).                              */
 struct orc_scs_s {
-    int N, n, K, D, L, c, M, nops, bit_level;
+    int N, n, K, D, L, c, M, nops, bit_level, nonsys;
     uint32_t crc_poly;
     uint8_t *frozen;
     int *info;       /* A ascending */
@@ -356,10 +386,17 @@ typedef struct {
 
 orc_scs_t *orc_scs_create(int N, const uint8_t *frozen, int D, int L, uint32_t crc_poly, int bit_level)
 {
+    return orc_scs_create_ex(N, frozen, D, L, crc_poly, bit_level, 0);
+}
+
+orc_scs_t *orc_scs_create_ex(int N, const uint8_t *frozen, int D, int L, uint32_t crc_poly, int bit_level,
+                             int nonsystematic)
+{
     int n = ilog2(N);
     if (n < 0 || D < 1 || L < 1) return NULL;
     orc_scs_t *h = (orc_scs_t *)calloc(1, sizeof(*h));
     h->N = N; h->n = n; h->D = D; h->L = L; h->crc_poly = crc_poly; h->bit_level = bit_level;
+    h->nonsys = nonsystematic ? 1 : 0;
     h->c = orc_crc_degree(crc_poly);
     h->frozen = (uint8_t *)malloc((size_t)N);
     memcpy(h->frozen, frozen, (size_t)N);
@@ -412,6 +449,19 @@ static void alpha_op(const orc_scs_t *h, float **alpha, const float *chan, const
     }
 }
 
+/* the K-bit block of a complete path: x_hat restricted to A (systematic,
+ * PAPER.md:L854), or u_hat = x_hat F^{(x)n} restricted to A */
+static void read_block(const orc_scs_t *h, const uint8_t *xhat, uint8_t *tmp, uint8_t *block)
+{
+    const uint8_t *src = xhat;
+    if (h->nonsys) {
+        memcpy(tmp, xhat, (size_t)h->N);
+        orc_polar_transform(h->N, tmp);
+        src = tmp;
+    }
+    for (int q = 0; q < h->K; q++) block[q] = src[h->info[q]];
+}
+
 static int decode_one(const orc_scs_t *h, const float *chan, uint8_t *block, uint8_t *xhat,
                       float *pm_out, uint32_t *pops_out, uint32_t *sw_out, uint8_t *st_out,
                       orc_counters_t *ct, float **alpha, entry_t *S, uint8_t *beta_work,
@@ -433,7 +483,7 @@ static int decode_one(const orc_scs_t *h, const float *chan, uint8_t *block, uin
     for (;;) {
         if (nS == 0) {
             /* every complete path failed the CRC: best effort (reading R13) */
-            if (block) for (int k = 0; k < h->K; k++) block[k] = best_beta[h->info[k]];
+            if (block) read_block(h, best_beta, seg_base, block);
             if (xhat) memcpy(xhat, best_beta, (size_t)N);
             if (pm_out) *pm_out = best_pm;
             if (pops_out) *pops_out = pops;
@@ -499,13 +549,13 @@ static int decode_one(const orc_scs_t *h, const float *chan, uint8_t *block, uin
             int ok = 1;
             if (h->c > 0) {
                 if (ct) ct->crc_checks++;
-                for (int q = 0; q < h->K; q++) seg[q] = beta_work[h->info[q]];
+                read_block(h, beta_work, seg_base, seg);
                 uint8_t rem[32];
                 orc_crc_bits(seg, h->K - h->c, h->crc_poly, rem);
                 for (int d = 0; d < h->c; d++) ok &= (rem[d] == seg[h->K - h->c + d]);
             }
             if (ok) {
-                if (block) for (int q = 0; q < h->K; q++) block[q] = beta_work[h->info[q]];
+                if (block) read_block(h, beta_work, seg_base, block);
                 if (xhat) memcpy(xhat, beta_work, (size_t)N);
                 if (pm_out) *pm_out = p.pm;
                 if (pops_out) *pops_out = pops;

@@ -31,11 +31,19 @@ enum { ORC_ALPHA = 0, ORC_BETA = 1, ORC_R0 = 2, ORC_R1 = 3, ORC_REP = 4, ORC_SPC
 /* O1 — Bhattacharyya construction (BASELINE.json configs; reading R16). */
 int orc_bhattacharyya_mask(int N, int K, double design_ebno_db, uint8_t *frozen /* [N], 1=frozen */);
 
+/* O1b — information set from a reliability sequence (least reliable first):
+ * A = the K most reliable entries < N (the paper's 3GPP
+ * sequence, is user-supplied).  -1 if seq is not a permutation
+ * of [0, len) or has fewer than N entries < N. */
+int orc_mask_from_sequence(int N, int K, const int32_t *seq, int len, uint8_t *frozen);
+
 /* O2 — x <- x F^{(x)n} in place, n butterfly stages (Fig. 1). */
 void orc_polar_transform(int N, uint8_t *x);
 /* O2 — systematic encoding: u[A]=block, u[A^c]=0, encode, zero A^c, encode
  * (SPEC.md:L67).  Returns 0, or -1 if N invalid. */
 int orc_encode_systematic(int N, const uint8_t *frozen, const uint8_t *block /* [K] */, uint8_t *codeword /* [N] */);
+/* O2 — non-systematic encoding: u[A] = block, u[A^c] = 0, c = u F^{(x)n} */
+int orc_encode_nonsystematic(int N, const uint8_t *frozen, const uint8_t *block, uint8_t *codeword);
 
 /* O3 — CRC remainder of bits * x^c mod poly (MSB first, zero init, no
  * reflection, no xorout).  poly_full includes the
@@ -83,6 +91,10 @@ typedef struct {
 } orc_counters_t;
 
 orc_scs_t *orc_scs_create(int N, const uint8_t *frozen, int D, int L, uint32_t crc_poly, int bit_level);
+/* nonsystematic = 1: the block (and the CRC check) is u_hat restricted to A,
+ * u_hat = x_hat F^{(x)n} — re-encoding the root beta */
+orc_scs_t *orc_scs_create_ex(int N, const uint8_t *frozen, int D, int L, uint32_t crc_poly, int bit_level,
+                             int nonsystematic);
 void orc_scs_destroy(orc_scs_t *h);
 int  orc_scs_num_ops(const orc_scs_t *h);
 int  orc_scs_num_nodes(const orc_scs_t *h);

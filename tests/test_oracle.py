@@ -564,3 +564,57 @@ def test_fer_monotone_and_fast_vs_bit_level():
         assert ff <= 1.5 * fb + 3 * sd + 1e-9
         fers.append(ff)
     assert fers[0] > fers[1] > fers[2]
+
+
+# ------------------------------------------------------------------ O1b, non-systematic readout
+def test_mask_from_sequence():
+    # a toy sequence whose 4 most reliable entries below 8 are {3,5,6,7}
+    seq = [0, 1, 2, 8, 4, 9, 3, 10, 5, 11, 6, 12, 7, 13, 14, 15]
+    m = O.mask_from_sequence(8, 4, seq)
+    assert list(np.nonzero(m == 0)[0]) == [3, 5, 6, 7]
+    assert not O.mask_from_sequence(2, 2, [1, 0, 2, 3]).any()
+    with pytest.raises(ValueError):
+        O.mask_from_sequence(8, 4, [0, 1, 2, 3, 4, 5, 6, 6])         # not a permutation
+    with pytest.raises(ValueError):
+        O.mask_from_sequence(8, 4, [0, 1, 2, 3, 4, 5, 6])            # too short
+    # the Bhattacharyya order written as a sequence gives the Bhattacharyya set
+    for N, K in ((128, 64), (1024, 512)):
+        fr = O.bhattacharyya_mask(N, K, 2.0)
+        # any sequence listing A last (most reliable) selects A
+        info = np.nonzero(fr == 0)[0]
+        frz = np.nonzero(fr == 1)[0]
+        seq = np.concatenate([frz, info]).astype(np.int32)
+        assert np.array_equal(O.mask_from_sequence(N, K, seq), fr)
+
+
+def test_nonsystematic_encoding_is_u_times_G():
+    fr = O.bhattacharyya_mask(16, 8, 2.0)
+    G = _kron_matrix(16)
+    for m in itertools.product([0, 1], repeat=8):
+        u = np.zeros(16, np.int64)
+        u[fr == 0] = m
+        assert np.array_equal(O.encode_nonsystematic(fr, np.array(m, np.uint8)), (u @ G) % 2)
+
+
+@pytest.mark.parametrize("bit_level", [False, True])
+def test_nonsystematic_readout(bit_level):
+    """Non-systematic mode reads u_hat = x_hat F restricted to A:
+    noiseless decodes recover the message; bit-level D=1 equals textbook SC's
+    u_hat exactly; a passing CRC holds on u_hat."""
+    c = ig.CONFIGS["C1"]
+    fr = O.bhattacharyya_mask(c["N"], c["K"], c["design_db"])
+    blk = O.crc_attach(ig.payload_bits(21, 0, 200, c["K"] - 8), 0x107)
+    cw = O.encode_nonsystematic(fr, blk)
+    dec = O.SCSDecoder(fr, c["D"], c["L"], 0x107, bit_level, nonsystematic=True)
+    r = dec.decode(4.0 * (1 - 2 * cw.astype(np.float32)))
+    assert np.array_equal(r["bits"], blk) and (r["status"] == 0).all()
+    nz = ig.unit_normals(21, 0, 200, c["N"])
+    llr = O.awgn_llr(cw, nz, 1.5, c["K"] / c["N"])
+    r = dec.decode(llr, want_xhat=True)
+    assert np.array_equal(r["bits"], O.polar_transform(r["xhat"])[:, fr == 0])
+    good = r["status"] == 0
+    assert not (O.crc_bits(r["bits"][good][:, :-8], 0x107) ^ r["bits"][good][:, -8:]).any()
+    if bit_level:
+        u_sc, _ = O.sc_decode(fr, llr)
+        r1 = O.SCSDecoder(fr, 1, c["L"], 0, True, nonsystematic=True).decode(llr)
+        assert np.array_equal(r1["bits"], u_sc[:, fr == 0])
