@@ -50,6 +50,9 @@ extern "C" {
                                          instead of staging it in shared memory */
 #define POLAR_FLAG_SNAP_SMEM    0x8u  /* force snapshots into shared memory */
 #define POLAR_FLAG_CHAN_SMEM    0x10u /* force channel staging in shared memory */
+#define POLAR_FLAG_NONSYSTEMATIC 0x40u /* non-systematic code: encoders emit c = u F,
+                                          decoders read u_hat = x_hat F restricted to A
+                                          (PAPER.md:L503); any mask is allowed */
 
 typedef struct polar_scs_s *polar_scs_t;
 
@@ -75,6 +78,15 @@ typedef struct {
  *   written 1 = frozen, 0 = information.  Returns POLAR_EINVAL on bad sizes.
  */
 int polar_construct_bhattacharyya(int32_t N, int32_t K, double design_ebno_db, uint8_t *frozen_mask);
+
+/*
+ * Information set from a user-supplied reliability sequence listed LEAST
+ * reliable first (SPEC.md:L42-44 format; e.g. the 3GPP TS 38.212 sequence the
+ * paper uses, PAPER.md:L966 — not shipped): the K most reliable entries below N
+ * carry information.  seq: host [len], a permutation of [0, len) with len >= N;
+ * frozen_mask: host [N] output.  POLAR_EINVAL on a bad sequence or sizes.
+ */
+int polar_construct_from_sequence(int32_t N, int32_t K, const int32_t *seq, int32_t len, uint8_t *frozen_mask);
 
 /*
  * Create a decoder for PC(N, K) with a stack of depth D and

@@ -30,6 +30,7 @@ POLAR_FLAG_SNAP_GLOBAL = 0x2
 POLAR_FLAG_CHAN_GLOBAL = 0x4
 POLAR_FLAG_SNAP_SMEM = 0x8
 POLAR_FLAG_CHAN_SMEM = 0x10
+POLAR_FLAG_NONSYSTEMATIC = 0x40
 
 
 class PolarInfo(C.Structure):
@@ -44,6 +45,7 @@ class PolarInfo(C.Structure):
 _vp, _i32, _i64, _u32, _u64, _dbl = C.c_void_p, C.c_int32, C.c_int64, C.c_uint32, C.c_uint64, C.c_double
 _SIGS = {
     "polar_construct_bhattacharyya": ([_i32, _i32, _dbl, _vp], C.c_int),
+    "polar_construct_from_sequence": ([_i32, _i32, _vp, _i32, _vp], C.c_int),
     "polar_scs_create": ([C.POINTER(_vp), _i32, _i32, _vp, _i32, _i32, _u32], C.c_int),
     "polar_scs_create_ex": ([C.POINTER(_vp), _i32, _i32, _vp, _i32, _i32, _u32, _u32], C.c_int),
     "polar_scs_destroy": ([_vp], None),
@@ -88,6 +90,14 @@ def bhattacharyya_mask(N: int, K: int, design_ebno_db: float) -> np.ndarray:
     return m
 
 
+def mask_from_sequence(N: int, K: int, seq) -> np.ndarray:
+    """frozen mask (uint8, 1 = frozen) from a reliability sequence, least reliable first."""
+    seq = np.ascontiguousarray(seq, dtype=np.int32)
+    m = np.zeros(N, np.uint8)
+    _check(polar_construct_from_sequence(N, K, seq.ctypes.data, seq.size, m.ctypes.data), "construct_from_sequence")
+    return m
+
+
 def _stream_ptr(stream):
     import torch
     s = stream if stream is not None else torch.cuda.current_stream()
@@ -108,13 +118,13 @@ class PolarSCS:
 
     def __init__(self, frozen_mask, D: int, L: int, crc_poly: int = 0, bit_level: bool = False,
                  snap_global: bool = False, chan_global: bool = False, snap_smem: bool = False,
-                 chan_smem: bool = False):
+                 chan_smem: bool = False, nonsystematic: bool = False):
         fm = np.ascontiguousarray(frozen_mask, dtype=np.uint8)
         self.N = int(fm.size)
         self.K = int(self.N - int(fm.sum()))
         flags = ((POLAR_FLAG_BIT_LEVEL if bit_level else 0) | (POLAR_FLAG_SNAP_GLOBAL if snap_global else 0)
                  | (POLAR_FLAG_CHAN_GLOBAL if chan_global else 0) | (POLAR_FLAG_SNAP_SMEM if snap_smem else 0)
-                 | (POLAR_FLAG_CHAN_SMEM if chan_smem else 0))
+                 | (POLAR_FLAG_CHAN_SMEM if chan_smem else 0) | (POLAR_FLAG_NONSYSTEMATIC if nonsystematic else 0))
         h = _vp()
         _check(polar_scs_create_ex(C.byref(h), self.N, self.K, fm.ctypes.data, int(D), int(L),
                                    int(crc_poly), flags), "polar_scs_create")

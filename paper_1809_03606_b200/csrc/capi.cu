@@ -62,6 +62,7 @@ CodecParams codec_params(polar_scs_t h, int64_t n) {
     p.N = h->t.N; p.n = h->t.n; p.K = h->t.K; p.c = h->t.c;
     p.nw = std::max(1, h->t.N / 32);
     p.info = h->t.info; p.crc_tab = h->t.crc_tab; p.info_words = h->t.info_words;
+    p.nonsys = (h->flags & POLAR_FLAG_NONSYSTEMATIC) ? 1 : 0;
     return p;
 }
 
@@ -102,7 +103,7 @@ int polar_scs_create_ex(polar_scs_t *out, int32_t N, int32_t K, const uint8_t *f
     if (!out) return POLAR_EINVAL;
     *out = nullptr;
     const uint32_t known = POLAR_FLAG_BIT_LEVEL | POLAR_FLAG_SNAP_GLOBAL | POLAR_FLAG_CHAN_GLOBAL |
-                           POLAR_FLAG_SNAP_SMEM | POLAR_FLAG_CHAN_SMEM;
+                           POLAR_FLAG_SNAP_SMEM | POLAR_FLAG_CHAN_SMEM | POLAR_FLAG_NONSYSTEMATIC;
     if (D < 1 || D > kMaxD || L < 1 || (flags & ~known)) return POLAR_EINVAL;
     if ((flags & POLAR_FLAG_SNAP_GLOBAL) && (flags & POLAR_FLAG_SNAP_SMEM)) return POLAR_EINVAL;
     if ((flags & POLAR_FLAG_CHAN_GLOBAL) && (flags & POLAR_FLAG_CHAN_SMEM)) return POLAR_EINVAL;
@@ -142,6 +143,7 @@ int polar_scs_create_ex(polar_scs_t *out, int32_t N, int32_t K, const uint8_t *f
     p.nodes = t.nodes; p.info = t.info; p.crc_tab = t.crc_tab; p.crc_bytes = t.crc_bytes; p.queue = h->d_queue;
     p.N = N; p.n = t.n; p.K = K; p.c = t.c; p.D = D; p.L = h->L; p.M = t.M;
     p.nw = nw; p.snap_stride = sstride; p.sched_words = sched_words; p.cnt_words = cnt_words;
+    p.nonsys = (flags & POLAR_FLAG_NONSYSTEMATIC) ? 1 : 0;
 
     // Layout choice: per warp, alpha stages >= 6 (N floats incl. scratch), flat
     // beta, best-effort beta and counters always live in shared memory; the
@@ -158,7 +160,8 @@ int polar_scs_create_ex(polar_scs_t *out, int32_t N, int32_t K, const uint8_t *f
             const bool snap_smem = (si == 0);
             if (snap_smem && (flags & POLAR_FLAG_SNAP_GLOBAL)) continue;
             if (!snap_smem && (flags & POLAR_FLAG_SNAP_SMEM)) continue;
-            const int ww = round4((chan_smem ? N : 0) + N + 2 * nw + cnt_words + 2 * D + 4 + (snap_smem ? D * sstride : 0));
+            const int ww = round4((chan_smem ? N : 0) + N + 2 * nw + cnt_words + 2 * D + 4 + nw +
+                                  (snap_smem ? D * sstride : 0));
             const int smem = 4 * (sched_words + kDecodeWarps * ww);
             if (smem > optin) continue;
             int occ = 0;
@@ -293,7 +296,7 @@ int polar_crc_attach_batch(polar_scs_t h, const uint8_t *payload, int64_t n, uin
 
 int polar_encode_batch(polar_scs_t h, const uint8_t *block, int64_t n, uint8_t *codeword, void *stream) {
     if (!h || n < 0) return POLAR_EINVAL;
-    if (!h->t.systematic_ok) return POLAR_ENOTSYS;
+    if (!h->t.systematic_ok && !(h->flags & POLAR_FLAG_NONSYSTEMATIC)) return POLAR_ENOTSYS;
     if (n == 0) return POLAR_OK;
     if (!block || !codeword) return POLAR_EINVAL;
     CodecParams p = codec_params(h, n);
@@ -317,7 +320,7 @@ int polar_modulate_batch(polar_scs_t h, const uint8_t *codeword, const float *no
 int polar_generate_batch(polar_scs_t h, uint64_t seed, double ebno_db, int64_t first_frame, int64_t n,
                          uint8_t *block, float *llr, void *stream) {
     if (!h || n < 0 || first_frame < 0) return POLAR_EINVAL;
-    if (!h->t.systematic_ok) return POLAR_ENOTSYS;
+    if (!h->t.systematic_ok && !(h->flags & POLAR_FLAG_NONSYSTEMATIC)) return POLAR_ENOTSYS;
     if (n == 0) return POLAR_OK;
     if (!llr) return POLAR_EINVAL;
     if (h->t.N >= 4 && (reinterpret_cast<uintptr_t>(llr) & 15u)) return POLAR_EINVAL;

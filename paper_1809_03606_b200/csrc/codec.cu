@@ -50,6 +50,7 @@ __device__ void transform_smem(uint32_t *w, int N, int nw, int lane) {
 // block bits (K) -> systematic codeword bits in w
 __device__ void systematic_encode_smem(uint32_t *w, const CodecParams &P, int lane) {
     transform_smem(w, P.N, P.nw, lane);
+    if (P.nonsys) return;                                 // non-systematic: c = u F
     for (int j = lane; j < P.nw; j += 32) w[j] &= P.info_words[j];
     __syncwarp();
     transform_smem(w, P.N, P.nw, lane);

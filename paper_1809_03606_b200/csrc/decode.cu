@@ -115,6 +115,28 @@ __device__ __forceinline__ void beta_op(uint32_t *beta, int lam, int phi, int la
     __syncwarp();
 }
 
+// u <- x F^{(x)n} on nw bit-packed words: the re-encoding of
+// the root beta that gives u_hat in non-systematic mode
+__device__ __forceinline__ void xform_words(uint32_t *w, int N, int nw, int lane) {
+    const uint32_t masks[5] = {0x55555555u, 0x33333333u, 0x0F0F0F0Fu, 0x00FF00FFu, 0x0000FFFFu};
+    #pragma unroll 1
+    for (int j = lane; j < nw; j += 32) {
+        uint32_t x = w[j];
+#pragma unroll
+        for (int s = 0; s < 5; s++)
+            if ((1 << s) < N) x ^= (x >> (1 << s)) & masks[s];
+        w[j] = x;
+    }
+    __syncwarp();
+    #pragma unroll 1
+    for (int H = 1; H < nw; H <<= 1) {
+        #pragma unroll 1
+        for (int j = lane; j < nw; j += 32)
+            if ((j & H) == 0) w[j] ^= w[j + H];
+        __syncwarp();
+    }
+}
+
 // Warp minimum of 64-bit keys (hi, lo) with unique lo among equal hi.
 __device__ __forceinline__ void warp_min_key(uint32_t hi, uint32_t lo, uint32_t &mh, uint32_t &ml) {
     mh = __reduce_min_sync(FULL, hi);
@@ -247,8 +269,9 @@ fsscs_decode_kernel(const DecodeParams P) {
     uint16_t *cnt = reinterpret_cast<uint16_t *>(best + nw);
     uint32_t *shdr = best + nw + P.cnt_words;                      // fork headers m1..m4, 2 words/slot
     uint32_t *snap_used = shdr + 2 * D;                            // 4 words: snapshot-slot bitmap
+    uint32_t *uhat = snap_used + 4;                                // nw words: u_hat (non-systematic)
     // snapshot slot k of this warp: shared memory, or global slot index snap0 + k
-    uint32_t *snap_s = shdr + 2 * D + 4;
+    uint32_t *snap_s = shdr + 2 * D + 4 + nw;
     const uint32_t snap0 = (uint32_t)(blockIdx.x * kDecodeWarps + warp) * (uint32_t)D;
     const int sstride = (NL > 0) ? nw : P.snap_stride;
     auto snap_slot = [&](int k) -> uint32_t * {
@@ -471,10 +494,18 @@ fsscs_decode_kernel(const DecodeParams P) {
                 if (P.c > 0) {
                     // syndrome = XOR of the contributions of the set systematic bits,
                     // looked up per beta byte (tables hold information positions only)
+                    const uint32_t *cw = beta;
+                    if (P.nonsys) {
+                        #pragma unroll 1
+                        for (int w = lane; w < nw; w += 32) uhat[w] = beta[w];
+                        __syncwarp();
+                        xform_words(uhat, N, nw, lane);
+                        cw = uhat;
+                    }
                     uint32_t syn = 0;
                     #pragma unroll 1
                     for (int w = lane; w < nw; w += 32) {
-                        const uint32_t x = beta[w];
+                        const uint32_t x = cw[w];
                         const uint32_t *tw = P.crc_bytes + (size_t)w * 1024;
                         syn ^= __ldg(tw + (x & 255u)) ^ __ldg(tw + 256 + ((x >> 8) & 255u)) ^
                                __ldg(tw + 512 + ((x >> 16) & 255u)) ^ __ldg(tw + 768 + (x >> 24));
@@ -818,9 +849,17 @@ fsscs_decode_kernel(const DecodeParams P) {
             }
         }
 
-        // ---- output: x_hat restricted to A, ascending -----
+        // ---- output: x_hat (systematic) or u_hat = x_hat F
+        // (non-systematic) restricted to A, ascending ---------
         {
             const uint32_t *bsrc = from_best ? best : beta;
+            if (P.nonsys) {
+                #pragma unroll 1
+                for (int w = lane; w < nw; w += 32) uhat[w] = bsrc[w];
+                __syncwarp();
+                xform_words(uhat, N, nw, lane);
+                bsrc = uhat;
+            }
             uint8_t *ob = P.out_bits + (size_t)f * K;
             #pragma unroll 1
             for (int q = lane; q < K; q += 32) {

@@ -161,6 +161,28 @@ int build_host_code(int N, int K, const uint8_t *frozen, uint32_t crc_poly, bool
 
 }  // namespace polar
 
+// Information set from a reliability sequence listed least reliable first
+// (e.g. the 3GPP TS 38.212 sequence of PAPER.md:L966, which the
+// user supplies): the K most reliable entries below N carry information.
+extern "C" int polar_construct_from_sequence(int32_t N, int32_t K, const int32_t *seq, int32_t len,
+                                             uint8_t *frozen_mask) {
+    if (N < 1 || N > 65536 || (N & (N - 1)) != 0 || K < 0 || K > N || !seq || !frozen_mask || len < N)
+        return POLAR_EINVAL;
+    std::vector<char> seen((size_t)len, 0);
+    std::vector<int> below;
+    below.reserve(N);
+    for (int32_t i = 0; i < len; i++) {
+        const int32_t v = seq[i];
+        if (v < 0 || v >= len || seen[v]) return POLAR_EINVAL;
+        seen[v] = 1;
+        if (v < N) below.push_back(v);
+    }
+    if ((int)below.size() != N) return POLAR_EINVAL;
+    std::memset(frozen_mask, 1, (size_t)N);
+    for (int r = N - K; r < N; r++) frozen_mask[below[r]] = 0;
+    return POLAR_OK;
+}
+
 // Bhattacharyya construction, level-by-level doubling in the log domain: at
 // each level every parameter z spawns 2z - z^2 (appended bit 0) and z^2
 // (appended bit 1); the first appended bit is the index MSB.

@@ -56,6 +56,7 @@ struct DecodeParams {
     int sched_words;            // node-table words staged in shared memory (0 = read global)
     int warp_words;             // shared-memory words per warp
     int cnt_words;              // words of the per-length counters (u16 each)
+    int nonsys;                 // 1: read u_hat = x_hat F restricted to A (non-systematic)
 };
 
 struct CodecParams {
@@ -69,6 +70,7 @@ struct CodecParams {
     uint64_t seed;
     float sigma_f, scale_f;
     int N, n, K, c, nw;
+    int nonsys;                 // 1: non-systematic encoding c = u F
     const uint16_t *info;
     const uint32_t *crc_tab;
     const uint32_t *info_words;

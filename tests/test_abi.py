@@ -92,3 +92,16 @@ def test_create_rejects_bad_arguments():
     P.polar_scs_destroy(None)                                     # no-op
     assert P.polar_scs_decode(None, None, 0, None, None) == P.POLAR_EINVAL
     assert P.polar_scs_get_info(None, None) == P.POLAR_EINVAL
+
+
+def test_sequence_constructor_equals_oracle():
+    import oracle as O
+    import paper_1809_03606_b200 as P
+    rng = np.random.default_rng(3)
+    for N, K, L in ((8, 4, 16), (128, 64, 128), (1024, 512, 2048), (64, 0, 64), (64, 64, 100)):
+        seq = rng.permutation(L).astype(np.int32)
+        assert np.array_equal(P.mask_from_sequence(N, K, seq), O.mask_from_sequence(N, K, seq))
+    bad = np.array([0, 1, 2, 2, 4, 5, 6, 7], np.int32)
+    m = np.zeros(8, np.uint8)
+    assert P.polar_construct_from_sequence(8, 4, bad.ctypes.data, 8, m.ctypes.data) == P.POLAR_EINVAL
+    assert P.polar_construct_from_sequence(8, 4, bad.ctypes.data, 7, m.ctypes.data) == P.POLAR_EINVAL

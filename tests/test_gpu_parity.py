@@ -265,3 +265,36 @@ def test_full_size_sampled_parity_device_generator(cfg):
         checked += int(same.sum())
     assert checked >= 30 * npts
     assert int((res["status"] == 2).sum()) == 0          # watchdog never fires
+
+
+def _random_mask(N, K, seed):
+    rng = np.random.default_rng(seed)
+    return P.mask_from_sequence(N, K, rng.permutation(N).astype(np.int32))
+
+
+@pytest.mark.parametrize("cfg,ebno,random_mask", [("C1", 1.5, False), ("C3", 2.0, False), ("C5", 3.0, False),
+                                                  ("C1", 2.5, True), ("C2", 2.0, True)])
+def test_nonsystematic_parity(cfg, ebno, random_mask):
+    """Non-systematic mode: c = u F on the GPU equals the oracle's
+    encoding, and the decoder's u_hat block, PM, pops, switches and status equal
+    the oracle's.  A random information set (generally not systematic-
+    encodable) exercises the mode on arbitrary masks."""
+    c = ig.CONFIGS[cfg]
+    fr = _random_mask(c["N"], c["K"], 5) if random_mask else P.bhattacharyya_mask(c["N"], c["K"], c["design_db"])
+    dec = P.PolarSCS(fr, c["D"], c["L"], c["crc_poly"], nonsystematic=True)
+    n = 200 if c["N"] <= 1024 else 40
+    pay = ig.payload_bits(31, 0, n, c["K"] - dec.c)
+    nz = ig.unit_normals(31, 0, n, c["N"])
+    blk = dec.crc_attach(torch.from_numpy(pay).cuda())
+    cw = dec.encode(blk)
+    gl = dec.modulate(cw, torch.from_numpy(nz).cuda(), ebno)
+    ob = O.crc_attach(pay, c["crc_poly"])
+    ocw = O.encode_nonsystematic(fr, ob)
+    assert np.array_equal(cw.cpu().numpy(), ocw)
+    ol = O.awgn_llr(ocw, nz, ebno, c["K"] / c["N"])
+    assert np.array_equal(gl.cpu().numpy(), ol)
+    ref = O.SCSDecoder(fr, c["D"], c["L"], c["crc_poly"], nonsystematic=True).decode(ol, threads=8)
+    _compare(dec.decode_stats(gl), ref, f"{cfg} nonsys")
+    if random_mask and not dec.info["systematic_ok"]:
+        with pytest.raises(P.PolarError):
+            P.PolarSCS(fr, c["D"], c["L"], c["crc_poly"]).encode(blk)
