@@ -92,6 +92,14 @@ def lib():
             L.orc_scs_decode.argtypes = [C.c_void_p, f32p, C.c_int64, u8p, u8p, f32p,
                                          C.POINTER(C.c_uint32), C.POINTER(C.c_uint32), u8p,
                                          C.POINTER(Counters)]
+            L.orc_scl_create.argtypes = [C.c_int, u8p, C.c_int, C.c_uint32, C.c_int, C.c_int]
+            L.orc_scl_create.restype = C.c_void_p
+            L.orc_scl_destroy.argtypes = [C.c_void_p]
+            L.orc_scl_destroy.restype = None
+            for fn in ("orc_scl_K", "orc_scl_num_nodes"):
+                getattr(L, fn).argtypes = [C.c_void_p]
+            L.orc_scl_decode.argtypes = [C.c_void_p, f32p, C.c_int64, u8p, u8p, f32p, u8p,
+                                         C.POINTER(C.c_uint32)]
             _lib = L
     return _lib
 
@@ -311,4 +319,55 @@ class SCSDecoder:
                 for k, v in ct.as_dict().items():
                     tot[k] = tot.get(k, 0) + v
             out["counters"] = tot
+        return out
+
+
+# ---------------------------------------------------------------- O11 list decoder
+class SCLDecoder:
+    """The FSSCL list decoder (O11).  bit_level=True gives SCL."""
+
+    def __init__(self, frozen, L: int, crc_poly: int = 0, bit_level: bool = False, nonsystematic: bool = False):
+        self.frozen = _u8(frozen).copy()
+        self.N = int(self.frozen.size)
+        self.L, self.crc_poly, self.bit_level = int(L), int(crc_poly), bool(bit_level)
+        self._h = lib().orc_scl_create(self.N, _p(self.frozen, C.c_uint8), self.L, self.crc_poly,
+                                       int(self.bit_level), int(bool(nonsystematic)))
+        if not self._h:
+            raise ValueError("orc_scl_create: invalid parameters")
+        self.K = int(lib().orc_scl_K(self._h))
+        self.M = int(lib().orc_scl_num_nodes(self._h))
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            lib().orc_scl_destroy(h)
+            self._h = None
+
+    def decode(self, llr, want_xhat: bool = False, threads: int = 1):
+        llr = np.ascontiguousarray(llr, dtype=np.float32).reshape(-1, self.N)
+        n = llr.shape[0]
+        out = {"bits": np.zeros((n, self.K), np.uint8), "pm": np.zeros(n, np.float32),
+               "status": np.zeros(n, np.uint8), "crc_checks": np.zeros(n, np.uint32)}
+        if want_xhat:
+            out["xhat"] = np.zeros((n, self.N), np.uint8)
+        threads = max(1, min(int(threads), n)) if n else 1
+        bounds = np.linspace(0, n, threads + 1).astype(np.int64)
+
+        def run(t):
+            a, b = int(bounds[t]), int(bounds[t + 1])
+            if b <= a:
+                return
+            sl = slice(a, b)
+            rc = lib().orc_scl_decode(self._h, _p(llr[sl], C.c_float), b - a, _p(out["bits"][sl], C.c_uint8),
+                                      _p(out["xhat"][sl], C.c_uint8) if want_xhat else None,
+                                      _p(out["pm"][sl], C.c_float), _p(out["status"][sl], C.c_uint8),
+                                      _p(out["crc_checks"][sl], C.c_uint32))
+            if rc != 0:
+                raise MemoryError("orc_scl_decode failed")
+
+        if threads == 1:
+            run(0)
+        else:
+            with ThreadPoolExecutor(threads) as ex:
+                list(ex.map(run, range(threads)))
         return out

@@ -641,6 +641,200 @@ int orc_scs_decode(const orc_scs_t *h, const float *llr, int64_t n_frames,
     return rc;
 }
 
+/* ------------------------------------------------------------------------ */
+/* O11  the FSSCL list decoder (§2.2.3-2.2.4; memory per
+ * L772-780).  L paths advance in lock-step through the FSSC schedule; at every
+ * decision node (R0 included, reading R23) each path creates its node
+ * candidates (the same rules as O7, L526-585) and the union is pruned back to
+ * the L best (L507).  Written with a naive full copy of alpha and beta per
+ * path: the lazy copy of L774-776 is a memory optimisation that must not
+ * change any result.
+ *
+ * Readings: R22 the list is kept in rank order; a candidate's key
+ * is (PM, parent rank, candidate rank in (dPM, mask) order) and the L smallest
+ * keys survive, in key order ("ties broken by lower parent path
+ * id, then lower candidate ordinal").  R24 final selection (L519): the first
+ * path in rank order whose block passes the CRC (the first path when there is
+ * no CRC); if none passes, the first path with status 1.     */
+struct orc_scl_s {
+    int N, n, K, L, c, M, nops, nonsys;
+    uint32_t crc_poly;
+    uint8_t *frozen;
+    int *info;
+    int32_t *ops;
+};
+
+typedef struct {
+    float pm;
+    float **alpha;   /* stages 0..n-1, own copy */
+    uint8_t *beta;   /* N bytes */
+} lpath_t;
+
+typedef struct { float pm; int parent, rank, mask; } lcand_t;
+
+/* (PM, parent rank, candidate rank) order (reading R22) */
+static int lcand_less(const lcand_t *a, const lcand_t *b)
+{
+    if (a->pm != b->pm) return a->pm < b->pm;
+    if (a->parent != b->parent) return a->parent < b->parent;
+    return a->rank < b->rank;
+}
+
+orc_scl_t *orc_scl_create(int N, const uint8_t *frozen, int L, uint32_t crc_poly, int bit_level, int nonsystematic)
+{
+    int n = ilog2(N);
+    if (n < 0 || L < 1) return NULL;
+    orc_scl_t *h = (orc_scl_t *)calloc(1, sizeof(*h));
+    h->N = N; h->n = n; h->L = L; h->crc_poly = crc_poly; h->nonsys = nonsystematic ? 1 : 0;
+    h->c = orc_crc_degree(crc_poly);
+    h->frozen = (uint8_t *)malloc((size_t)N);
+    memcpy(h->frozen, frozen, (size_t)N);
+    h->info = (int *)malloc(sizeof(int) * (size_t)N);
+    for (int i = 0; i < N; i++) if (!frozen[i]) h->info[h->K++] = i;
+    if (h->c >= h->K && h->c > 0) { orc_scl_destroy(h); return NULL; }
+    int need = -orc_build_schedule(N, frozen, bit_level, NULL, 0);
+    h->ops = (int32_t *)malloc(sizeof(int32_t) * (size_t)(need > 0 ? need : 1));
+    h->nops = orc_build_schedule(N, frozen, bit_level, h->ops, need);
+    for (int k = 0; k < h->nops; k++) if ((h->ops[k] & 0xff) >= ORC_R0) h->M++;
+    return h;
+}
+
+void orc_scl_destroy(orc_scl_t *h)
+{
+    if (!h) return;
+    free(h->frozen); free(h->info); free(h->ops);
+    free(h);
+}
+
+int orc_scl_K(const orc_scl_t *h) { return h->K; }
+int orc_scl_num_nodes(const orc_scl_t *h) { return h->M; }
+
+/* the CRC check of a complete path's block */
+static int scl_crc_ok(const orc_scl_t *h, const uint8_t *xhat, uint8_t *tmp, uint8_t *blk)
+{
+    if (h->c == 0) return 1;
+    const uint8_t *src = xhat;
+    if (h->nonsys) { memcpy(tmp, xhat, (size_t)h->N); orc_polar_transform(h->N, tmp); src = tmp; }
+    for (int q = 0; q < h->K; q++) blk[q] = src[h->info[q]];
+    uint8_t rem[32];
+    orc_crc_bits(blk, h->K - h->c, h->crc_poly, rem);
+    int ok = 1;
+    for (int d = 0; d < h->c; d++) ok &= (rem[d] == blk[h->K - h->c + d]);
+    return ok;
+}
+
+static void scl_copy_path(const orc_scl_t *h, lpath_t *dst, const lpath_t *src)
+{
+    dst->pm = src->pm;
+    for (int l = 0; l < h->n; l++) memcpy(dst->alpha[l], src->alpha[l], sizeof(float) * ((size_t)1 << l));
+    memcpy(dst->beta, src->beta, (size_t)h->N);
+}
+
+int orc_scl_decode(const orc_scl_t *h, const float *llr, int64_t n_frames, uint8_t *block, uint8_t *xhat,
+                   float *pm_out, uint8_t *status, uint32_t *crc_checks)
+{
+    const int N = h->N, L = h->L, n = h->n;
+    lpath_t *cur = (lpath_t *)calloc((size_t)L, sizeof(lpath_t));
+    lpath_t *nxt = (lpath_t *)calloc((size_t)L, sizeof(lpath_t));
+    lcand_t *cand = (lcand_t *)malloc(sizeof(lcand_t) * (size_t)L * 8);
+    int (*mm)[4] = (int (*)[4])malloc(sizeof(int[4]) * (size_t)L);
+    uint8_t *base = (uint8_t *)malloc((size_t)L * (size_t)N);
+    float *tmp = (float *)malloc(sizeof(float) * (size_t)N);
+    uint8_t *t1 = (uint8_t *)malloc((size_t)N), *t2 = (uint8_t *)malloc((size_t)N);
+    int ok = cur && nxt && cand && mm && base && tmp && t1 && t2;
+    for (int l = 0; ok && l < L; l++) {
+        lpath_t *ps[2] = { &cur[l], &nxt[l] };
+        for (int q = 0; q < 2 && ok; q++) {
+            ps[q]->alpha = (float **)calloc((size_t)n + 1, sizeof(float *));
+            ps[q]->beta = (uint8_t *)malloc((size_t)N);
+            ok = ps[q]->alpha && ps[q]->beta;
+            for (int s = 0; ok && s < n; s++) ok = (ps[q]->alpha[s] = (float *)malloc(sizeof(float) * ((size_t)1 << s))) != NULL;
+        }
+    }
+    for (int64_t f = 0; ok && f < n_frames; f++) {
+        const float *chan = llr + f * N;
+        int nL = 1;
+        cur[0].pm = 0.0f;
+        memset(cur[0].beta, 0, (size_t)N);
+        uint32_t checks = 0;
+        for (int k = 0; k < h->nops; k++) {
+            int kind = h->ops[k] & 0xff, lam = (h->ops[k] >> 8) & 0xff, phi = h->ops[k] >> 16;
+            int Lam = 1 << lam;
+            if (kind == ORC_BETA) {          /* in-place XOR, every path */
+                for (int l = 0; l < nL; l++)
+                    for (int i = 0; i < Lam; i++) cur[l].beta[(phi - 1) * Lam + i] ^= cur[l].beta[phi * Lam + i];
+                continue;
+            }
+            if (kind == ORC_ALPHA) {         /* Eq. (4), every path on its own memory */
+                for (int l = 0; l < nL; l++) {
+                    const float *p = (lam + 1 == n) ? chan : cur[l].alpha[lam + 1];
+                    float *v = cur[l].alpha[lam];
+                    for (int i = 0; i < Lam; i++)
+                        v[i] = (phi & 1) ? orc_g(p[i], p[i + Lam], cur[l].beta[(phi - 1) * Lam + i])
+                                         : orc_f(p[i], p[i + Lam]);
+                }
+                continue;
+            }
+            /* decision node: candidates of every path */
+            int nc_all = 0;
+            for (int l = 0; l < nL; l++) {
+                const float *a = (lam == n) ? chan : cur[l].alpha[lam];
+                cand_t c[8];
+                int nc = node_candidates(kind, a, Lam, base + (size_t)l * N, mm[l], c, tmp);
+                for (int t = 0; t < nc; t++) {
+                    cand[nc_all].pm = cur[l].pm + c[t].dpm;
+                    cand[nc_all].parent = l; cand[nc_all].rank = t; cand[nc_all].mask = c[t].mask;
+                    nc_all++;
+                }
+            }
+            /* prune to the L best (reading R22): insertion sort */
+            for (int x = 1; x < nc_all; x++) {
+                lcand_t v = cand[x];
+                int y = x - 1;
+                while (y >= 0 && lcand_less(&v, &cand[y])) { cand[y + 1] = cand[y]; y--; }
+                cand[y + 1] = v;
+            }
+            int nL2 = nc_all < L ? nc_all : L;
+            for (int r = 0; r < nL2; r++) {
+                const lcand_t *cd = &cand[r];
+                scl_copy_path(h, &nxt[r], &cur[cd->parent]);
+                nxt[r].pm = cd->pm;
+                apply_candidate(kind, Lam, base + (size_t)cd->parent * N, mm[cd->parent], cd->mask,
+                                nxt[r].beta + phi * Lam);
+            }
+            lpath_t *sw = cur; cur = nxt; nxt = sw;
+            nL = nL2;
+        }
+        /* final selection (reading R24) */
+        int sel = -1;
+        for (int r = 0; r < nL && sel < 0; r++) {
+            if (h->c > 0) checks++;
+            if (scl_crc_ok(h, cur[r].beta, t1, t2)) sel = r;
+        }
+        int st = 0;
+        if (sel < 0) { sel = 0; st = 1; }
+        if (block) {
+            const uint8_t *src = cur[sel].beta;
+            if (h->nonsys) { memcpy(t1, cur[sel].beta, (size_t)N); orc_polar_transform(N, t1); src = t1; }
+            for (int q = 0; q < h->K; q++) block[f * h->K + q] = src[h->info[q]];
+        }
+        if (xhat) memcpy(xhat + f * N, cur[sel].beta, (size_t)N);
+        if (pm_out) pm_out[f] = cur[sel].pm;
+        if (status) status[f] = (uint8_t)st;
+        if (crc_checks) crc_checks[f] = checks;
+    }
+    for (int l = 0; l < L; l++) {
+        lpath_t *ps[2] = { cur ? &cur[l] : NULL, nxt ? &nxt[l] : NULL };
+        for (int q = 0; q < 2; q++) {
+            if (!ps[q]) continue;
+            if (ps[q]->alpha) for (int s = 0; s < n; s++) free(ps[q]->alpha[s]);
+            free(ps[q]->alpha); free(ps[q]->beta);
+        }
+    }
+    free(cur); free(nxt); free(cand); free(mm); free(base); free(tmp); free(t1); free(t2);
+    return ok ? 0 : -1;
+}
+
 /* test hook: the sorted candidates of one node over a[0..Lam) — segments
  * written to segs[t*Lam .. (t+1)*Lam), dPM to dpm[t], mask to mask[t].     */
 int orc_node_candidates(int kind, const float *a, int Lam, float *dpm, int *mask, uint8_t *segs)

@@ -106,6 +106,17 @@ int orc_scs_decode(const orc_scs_t *h, const float *llr, int64_t n_frames,
                    uint8_t *block, uint8_t *xhat, float *pm, uint32_t *pops,
                    uint32_t *switches, uint8_t *status, orc_counters_t *counters);
 
+/* O11 — the FSSCL list decoder (readings R22-R24).
+ * L = list size.  bit_level = 1 gives plain SCL (leaf nodes only).  Outputs as
+ * orc_scs_decode; crc_checks[f] = complete paths CRC-checked before the pick. */
+typedef struct orc_scl_s orc_scl_t;
+orc_scl_t *orc_scl_create(int N, const uint8_t *frozen, int L, uint32_t crc_poly, int bit_level, int nonsystematic);
+void orc_scl_destroy(orc_scl_t *h);
+int  orc_scl_K(const orc_scl_t *h);
+int  orc_scl_num_nodes(const orc_scl_t *h);
+int  orc_scl_decode(const orc_scl_t *h, const float *llr, int64_t n_frames, uint8_t *block, uint8_t *xhat,
+                    float *pm, uint8_t *status, uint32_t *crc_checks);
+
 #ifdef __cplusplus
 }
 #endif
