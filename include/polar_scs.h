@@ -66,6 +66,7 @@ typedef struct {
     int32_t chan_in_smem;     /* 1: channel row staged in shared memory           */
     int32_t systematic_ok;    /* 1 if the mask is systematic-encodable            */
     uint32_t flags;
+    int32_t list_ctas, list_smem_per_cta;  /* polar_scl_decode launch (0: unsupported) */
 } polar_scs_info_t;
 
 /*
@@ -137,6 +138,28 @@ int polar_scs_decode(polar_scs_t h, const float *llr, int64_t n_frames, uint8_t 
 int polar_scs_decode_stats(polar_scs_t h, const float *llr, int64_t n_frames, uint8_t *out_bits,
                            float *pm, uint32_t *pops, uint32_t *switches, uint8_t *status,
                            void *stream);
+
+/*
+ * Decode n_frames independent frames with the FSSCL LIST decoder (PAPER.md:
+ * L505-519 SCL; L521-587 fast-simplified node path creation; L772-780 list
+ * memory with lazy copy), list size = the handle's L (the visit limit that
+ * gives the stack decoder "the same search space as SCL").
+ * With POLAR_FLAG_BIT_LEVEL the handle's leaf-only schedule gives plain SCL.
+ * At every decision node each of the <= L paths creates its node candidates
+ * and the L smallest keys (PM, parent rank, candidate rank) survive (reading
+ * R22); the output is the first path of the final list, in rank order, whose
+ * block passes the CRC (the first path without a CRC); if none passes, the
+ * first path with status 1 (reading R24).  One CTA of L warps per frame,
+ * persistent kernel with a frame queue; D is not used.
+ *   llr, out_bits: as polar_scs_decode.  pm: device [n] float32 final PM of the
+ *   output path (may be NULL); status: device [n] uint8 (may be NULL).
+ *   POLAR_ENOTSYS if L > 32 or the per-frame list memory (about 4 L N bytes
+ *   of alpha plus 8 L N/32 bytes of beta) does not fit in shared memory; the
+ *   handle's D limits do not apply.  Shares the handle's frame queue: one
+ *   in-flight call per handle, as for the stack decoder.
+ */
+int polar_scl_decode(polar_scs_t h, const float *llr, int64_t n_frames, uint8_t *out_bits,
+                     float *pm, uint8_t *status, void *stream);
 
 /*
  * End-to-end decode from HOST buffers: copies llr_host ([n][N] float32) to the

@@ -46,7 +46,7 @@ class Counters(C.Structure):
     _fields_ = [(n, C.c_uint64) for n in (
         "pops", "switches", "f_ops", "g_ops", "spine_elems", "beta_xor_bits", "node_elems",
         "node_visits", "cand_created", "cand_inserted", "cand_replaced", "cand_dropped",
-        "pruned", "crc_checks")]
+        "pruned", "crc_checks", "sel_compares")]
 
     def as_dict(self):
         return {n: int(getattr(self, n)) for n, _ in self._fields_}
@@ -99,7 +99,7 @@ def lib():
             for fn in ("orc_scl_K", "orc_scl_num_nodes"):
                 getattr(L, fn).argtypes = [C.c_void_p]
             L.orc_scl_decode.argtypes = [C.c_void_p, f32p, C.c_int64, u8p, u8p, f32p, u8p,
-                                         C.POINTER(C.c_uint32)]
+                                         C.POINTER(C.c_uint32), C.POINTER(Counters)]
             _lib = L
     return _lib
 
@@ -343,7 +343,7 @@ class SCLDecoder:
             lib().orc_scl_destroy(h)
             self._h = None
 
-    def decode(self, llr, want_xhat: bool = False, threads: int = 1):
+    def decode(self, llr, want_xhat: bool = False, threads: int = 1, counters: bool = False):
         llr = np.ascontiguousarray(llr, dtype=np.float32).reshape(-1, self.N)
         n = llr.shape[0]
         out = {"bits": np.zeros((n, self.K), np.uint8), "pm": np.zeros(n, np.float32),
@@ -352,6 +352,7 @@ class SCLDecoder:
             out["xhat"] = np.zeros((n, self.N), np.uint8)
         threads = max(1, min(int(threads), n)) if n else 1
         bounds = np.linspace(0, n, threads + 1).astype(np.int64)
+        cts = [Counters() for _ in range(threads)]
 
         def run(t):
             a, b = int(bounds[t]), int(bounds[t + 1])
@@ -361,7 +362,7 @@ class SCLDecoder:
             rc = lib().orc_scl_decode(self._h, _p(llr[sl], C.c_float), b - a, _p(out["bits"][sl], C.c_uint8),
                                       _p(out["xhat"][sl], C.c_uint8) if want_xhat else None,
                                       _p(out["pm"][sl], C.c_float), _p(out["status"][sl], C.c_uint8),
-                                      _p(out["crc_checks"][sl], C.c_uint32))
+                                      _p(out["crc_checks"][sl], C.c_uint32), C.byref(cts[t]) if counters else None)
             if rc != 0:
                 raise MemoryError("orc_scl_decode failed")
 
@@ -370,4 +371,10 @@ class SCLDecoder:
         else:
             with ThreadPoolExecutor(threads) as ex:
                 list(ex.map(run, range(threads)))
+        if counters:
+            tot = {}
+            for ct in cts:
+                for k, v in ct.as_dict().items():
+                    tot[k] = tot.get(k, 0) + v
+            out["counters"] = tot
         return out

@@ -731,7 +731,7 @@ static void scl_copy_path(const orc_scl_t *h, lpath_t *dst, const lpath_t *src)
 }
 
 int orc_scl_decode(const orc_scl_t *h, const float *llr, int64_t n_frames, uint8_t *block, uint8_t *xhat,
-                   float *pm_out, uint8_t *status, uint32_t *crc_checks)
+                   float *pm_out, uint8_t *status, uint32_t *crc_checks, orc_counters_t *ct)
 {
     const int N = h->N, L = h->L, n = h->n;
     lpath_t *cur = (lpath_t *)calloc((size_t)L, sizeof(lpath_t));
@@ -763,6 +763,7 @@ int orc_scl_decode(const orc_scl_t *h, const float *llr, int64_t n_frames, uint8
             if (kind == ORC_BETA) {          /* in-place XOR, every path */
                 for (int l = 0; l < nL; l++)
                     for (int i = 0; i < Lam; i++) cur[l].beta[(phi - 1) * Lam + i] ^= cur[l].beta[phi * Lam + i];
+                if (ct) ct->beta_xor_bits += (uint64_t)Lam * (uint64_t)nL;
                 continue;
             }
             if (kind == ORC_ALPHA) {         /* Eq. (4), every path on its own memory */
@@ -773,6 +774,7 @@ int orc_scl_decode(const orc_scl_t *h, const float *llr, int64_t n_frames, uint8
                         v[i] = (phi & 1) ? orc_g(p[i], p[i + Lam], cur[l].beta[(phi - 1) * Lam + i])
                                          : orc_f(p[i], p[i + Lam]);
                 }
+                if (ct) { if (phi & 1) ct->g_ops += (uint64_t)Lam * (uint64_t)nL; else ct->f_ops += (uint64_t)Lam * (uint64_t)nL; }
                 continue;
             }
             /* decision node: candidates of every path */
@@ -786,6 +788,11 @@ int orc_scl_decode(const orc_scl_t *h, const float *llr, int64_t n_frames, uint8
                     cand[nc_all].parent = l; cand[nc_all].rank = t; cand[nc_all].mask = c[t].mask;
                     nc_all++;
                 }
+            }
+            if (ct) {
+                ct->node_visits += (uint64_t)nL; ct->node_elems += (uint64_t)Lam * (uint64_t)nL;
+                ct->cand_created += (uint64_t)nc_all; { int lg = 0; while ((1 << lg) < nc_all) lg++; ct->sel_compares += (uint64_t)nc_all * (uint64_t)lg; }
+                ct->pruned += (uint64_t)(nc_all > L ? nc_all - L : 0);
             }
             /* prune to the L best (reading R22): insertion sort */
             for (int x = 1; x < nc_all; x++) {
@@ -822,6 +829,7 @@ int orc_scl_decode(const orc_scl_t *h, const float *llr, int64_t n_frames, uint8
         if (pm_out) pm_out[f] = cur[sel].pm;
         if (status) status[f] = (uint8_t)st;
         if (crc_checks) crc_checks[f] = checks;
+        if (ct) ct->crc_checks += checks;
     }
     for (int l = 0; l < L; l++) {
         lpath_t *ps[2] = { cur ? &cur[l] : NULL, nxt ? &nxt[l] : NULL };

@@ -88,6 +88,7 @@ typedef struct {
     uint64_t cand_created, cand_inserted, cand_replaced, cand_dropped;
     uint64_t pruned;                /* entries removed by the per-length rule */
     uint64_t crc_checks;
+    uint64_t sel_compares;          /* list decoder: prune cost, sum over nodes of T ceil(log2 T), T = candidates */
 } orc_counters_t;
 
 orc_scs_t *orc_scs_create(int N, const uint8_t *frozen, int D, int L, uint32_t crc_poly, int bit_level);
@@ -115,7 +116,7 @@ void orc_scl_destroy(orc_scl_t *h);
 int  orc_scl_K(const orc_scl_t *h);
 int  orc_scl_num_nodes(const orc_scl_t *h);
 int  orc_scl_decode(const orc_scl_t *h, const float *llr, int64_t n_frames, uint8_t *block, uint8_t *xhat,
-                    float *pm, uint8_t *status, uint32_t *crc_checks);
+                    float *pm, uint8_t *status, uint32_t *crc_checks, orc_counters_t *counters);
 
 #ifdef __cplusplus
 }

@@ -36,7 +36,8 @@ POLAR_FLAG_NONSYSTEMATIC = 0x40
 class PolarInfo(C.Structure):
     _fields_ = [(n, C.c_int32) for n in (
         "N", "n", "K", "crc_bits", "D", "L", "num_ops", "num_nodes", "warps_per_cta", "ctas",
-        "smem_per_cta", "snap_in_smem", "chan_in_smem", "systematic_ok")] + [("flags", C.c_uint32)]
+        "smem_per_cta", "snap_in_smem", "chan_in_smem", "systematic_ok")] + [("flags", C.c_uint32)] + [
+        (n, C.c_int32) for n in ("list_ctas", "list_smem_per_cta")]
 
     def as_dict(self):
         return {n: int(getattr(self, n)) for n, _ in self._fields_}
@@ -54,6 +55,7 @@ _SIGS = {
     "polar_scs_decode": ([_vp, _vp, _i64, _vp, _vp], C.c_int),
     "polar_scs_decode_stats": ([_vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp], C.c_int),
     "polar_scs_decode_host": ([_vp, _vp, _i64, _vp, _vp], C.c_int),
+    "polar_scl_decode": ([_vp, _vp, _i64, _vp, _vp, _vp, _vp], C.c_int),
     "polar_crc_attach_batch": ([_vp, _vp, _i64, _vp, _vp], C.c_int),
     "polar_encode_batch": ([_vp, _vp, _i64, _vp, _vp], C.c_int),
     "polar_modulate_batch": ([_vp, _vp, _vp, _i64, _dbl, _vp, _vp], C.c_int),
@@ -174,6 +176,18 @@ class PolarSCS:
                                       bits.data_ptr(), pm.data_ptr(), pops.data_ptr(), sw.data_ptr(),
                                       st.data_ptr(), _stream_ptr(stream)), "polar_scs_decode_stats")
         return {"bits": bits, "pm": pm, "pops": pops, "switches": sw, "status": st}
+
+    def decode_list(self, llr, stream=None):
+        """FSSCL list decoding with list size L (polar_scl_decode)."""
+        import torch
+        n = llr.shape[0]
+        dev = llr.device
+        bits = torch.empty((n, self.K), dtype=torch.uint8, device=dev)
+        pm = torch.empty(n, dtype=torch.float32, device=dev)
+        st = torch.empty(n, dtype=torch.uint8, device=dev)
+        _check(polar_scl_decode(self._h, _dev(llr, torch.float32, (n, self.N), "llr"), n, bits.data_ptr(),
+                                pm.data_ptr(), st.data_ptr(), _stream_ptr(stream)), "polar_scl_decode")
+        return {"bits": bits, "pm": pm, "status": st}
 
     def decode_host(self, llr_host, out_host=None, stream=None):
         """End-to-end from host memory (numpy array or CPU tensor, ideally pinned)."""

@@ -15,6 +15,8 @@ namespace polar {
 cudaError_t launch_decode(const DecodeParams &p, int slots, bool snap_smem, bool chan_smem, int ctas, int smem,
                           cudaStream_t st);
 cudaError_t decode_occupancy(int n, int slots, bool snap_smem, bool chan_smem, int smem, int *blocks_per_sm);
+cudaError_t launch_list(const ListParams &p, int lcap, int ctas, int smem, cudaStream_t st);
+cudaError_t list_occupancy(int lcap, int L, int smem, int *blocks_per_sm);
 cudaError_t launch_crc_attach(const CodecParams &p, cudaStream_t st);
 cudaError_t launch_encode(const CodecParams &p, cudaStream_t st);
 cudaError_t launch_modulate(const CodecParams &p, cudaStream_t st);
@@ -81,6 +83,28 @@ int decode_impl(polar_scs_t h, const float *llr, int64_t n, uint8_t *bits, float
     if (e != cudaSuccess) return cuda_status(e);
     return cuda_status(launch_decode(p, slots_for(h->D), h->snap_in_smem != 0, h->chan_in_smem != 0, h->ctas,
                                      h->smem_per_cta, st));
+}
+
+// FSSCL shared-memory layout (list.cu): offsets in 32-bit words, each area
+// 16-byte aligned.  Returns the total words.
+int list_layout(ListParams &p) {
+    const int L = p.L, N = p.N, n = p.n;
+    int o = round4(p.M);                                      // node table
+    p.o_alpha = o;
+    const int alpha_words = (p.M == 1 && n > 5) ? L * N : (n > 6 ? L * (N - 64) : 0);
+    o += round4(alpha_words);
+    p.o_beta = o;  o += round4(2 * L * p.nw);
+    p.o_reg = o;   o += 2 * L * 64;
+    p.o_clist = o; o += round4(2 * L);
+    p.o_mi = o;    o += round4(4 * L);
+    p.o_prow = o;  o += round4(4 * L);
+    p.o_cand = o;  o += round4(16 * L);
+    p.o_sel = o;   o += round4(L);
+    p.o_selpm = o; o += round4(L);
+    p.o_ok = o;    o += round4(L);
+    p.o_misc = o;  o += 4;
+    p.words = o;
+    return o;
 }
 
 }  // namespace
@@ -188,6 +212,22 @@ int polar_scs_create_ex(polar_scs_t *out, int32_t N, int32_t K, const uint8_t *f
         if (e != cudaSuccess) { free_handle(h); return cuda_status(e); }
         p.snap_global = h->d_snap;
     }
+    // ---- FSSCL launch (polar_scl_decode): one CTA of L warps per frame
+    if (h->L <= 32) {
+        ListParams &lp = h->list;
+        lp.nodes = t.nodes; lp.info = t.info; lp.crc_bytes = t.crc_bytes; lp.queue = h->d_queue;
+        lp.N = N; lp.n = t.n; lp.K = K; lp.c = t.c; lp.L = h->L; lp.M = t.M; lp.nw = nw;
+        lp.nonsys = p.nonsys;
+        const int smem = 4 * list_layout(lp);
+        const int lcap = h->L <= 8 ? 8 : (h->L <= 16 ? 16 : 32);
+        int occ = 0;
+        if (smem <= optin && list_occupancy(lcap, h->L, smem, &occ) == cudaSuccess && occ >= 1) {
+            h->list_ctas = occ * sms;
+            h->list_smem = smem;
+            h->list_lcap = lcap;
+        }
+        cudaGetLastError();
+    }
     *out = h;
     return POLAR_OK;
 }
@@ -209,6 +249,7 @@ int polar_scs_get_info(polar_scs_t h, polar_scs_info_t *o) {
     o->num_ops = h->t.nops; o->num_nodes = h->t.M;
     o->warps_per_cta = h->warps_per_cta; o->ctas = h->ctas; o->smem_per_cta = h->smem_per_cta;
     o->snap_in_smem = h->snap_in_smem; o->chan_in_smem = h->chan_in_smem; o->systematic_ok = h->t.systematic_ok ? 1 : 0; o->flags = h->flags;
+    o->list_ctas = h->list_ctas; o->list_smem_per_cta = h->list_smem;
     return POLAR_OK;
 }
 
@@ -223,6 +264,23 @@ int polar_scs_decode_stats(polar_scs_t h, const float *llr, int64_t n, uint8_t *
 
 int polar_scs_decode(polar_scs_t h, const float *llr, int64_t n, uint8_t *bits, void *stream) {
     return polar_scs_decode_stats(h, llr, n, bits, nullptr, nullptr, nullptr, nullptr, stream);
+}
+
+int polar_scl_decode(polar_scs_t h, const float *llr, int64_t n, uint8_t *bits, float *pm, uint8_t *status,
+                     void *stream) {
+    if (!h || n < 0) return POLAR_EINVAL;
+    if (h->list_ctas == 0) return POLAR_ENOTSYS;
+    if (n == 0) return POLAR_OK;
+    if (!llr || !bits) return POLAR_EINVAL;
+    if (h->t.N >= 4 && (reinterpret_cast<uintptr_t>(llr) & 15u)) return POLAR_EINVAL;
+    ListParams p = h->list;
+    p.llr = llr; p.n_frames = n; p.out_bits = bits; p.pm = pm; p.status = status;
+    p.queue = h->d_queue;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    cudaError_t e = cudaMemsetAsync(p.queue, 0, sizeof(unsigned long long), st);
+    if (e != cudaSuccess) return cuda_status(e);
+    const int ctas = (int)std::min<int64_t>(h->list_ctas, n);
+    return cuda_status(launch_list(p, h->list_lcap, ctas, h->list_smem, st));
 }
 
 int polar_scs_decode_host(polar_scs_t h, const float *llr_host, int64_t n, uint8_t *bits_host, void *stream) {

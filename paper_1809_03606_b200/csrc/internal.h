@@ -59,6 +59,23 @@ struct DecodeParams {
     int nonsys;                 // 1: read u_hat = x_hat F restricted to A (non-systematic)
 };
 
+// Kernel parameter block of the FSSCL list decoder (list.cu).  One CTA of
+// L warps per frame; the shared-memory offsets (in 32-bit words) are computed
+// by the host (capi.cu, list_layout).
+struct ListParams {
+    const float *llr;
+    int64_t n_frames;
+    uint8_t *out_bits;
+    float *pm;
+    uint8_t *status;
+    const uint32_t *nodes;
+    const uint16_t *info;
+    const uint32_t *crc_bytes;
+    unsigned long long *queue;
+    int N, n, K, c, L, M, nw, nonsys;
+    int o_alpha, o_beta, o_reg, o_clist, o_mi, o_prow, o_cand, o_sel, o_selpm, o_ok, o_misc, words;
+};
+
 struct CodecParams {
     const uint8_t *payload;     // crc attach input
     const uint8_t *block_in;    // encode input
@@ -90,6 +107,8 @@ struct polar_scs_s {
     int chan_in_smem = 0;
     int warps_per_cta = 0, ctas = 0, smem_per_cta = 0;
     polar::DecodeParams base{};     // prefilled params
+    int list_ctas = 0, list_smem = 0, list_lcap = 0;   // FSSCL launch (0 = list decode unsupported)
+    polar::ListParams list{};       // prefilled FSSCL params
     // host-staging for polar_scs_decode_host (lazily allocated)
     cudaStream_t s_h2d = nullptr, s_comp[2] = {nullptr, nullptr}, s_d2h = nullptr;
     float *d_stage_llr[2] = {nullptr, nullptr};
