@@ -53,6 +53,9 @@ def parse():
     ap.add_argument("--chan-smem", action="store_true")
     ap.add_argument("--bit-level", action="store_true",
                     help="bit-level SCS-RM (leaf-only schedule; the paper's SCS-RM comparator, PAPER.md:L797-813)")
+    ap.add_argument("--list", action="store_true",
+                    help="FSSCL list decoder with list size = the config's L (the paper's FSSCL comparator, "
+                         "PAPER.md:L521-587); with --bit-level: plain SCL")
     return ap.parse_args()
 
 
@@ -65,9 +68,30 @@ def dist_env():
 
 def workload_name(cfg, c):
     crc = {0: "no CRC", 0x11021: "CRC-16 0x1021", 0x107: "CRC-8 0x07"}[c["crc_poly"]]
-    mode = "bit-level SCS-RM" if c.get("bit_level") else "FSSCS-RM"
-    return (f"{cfg}: {mode} PC({c['N']},{c['K']}) Bhattacharyya@{c['design_db']}dB, {crc}, D={c['D']}, L={c['L']}, "
+    if c.get("list"):
+        mode = "SCL" if c.get("bit_level") else "FSSCL"
+        dl = f"list size L={c['L']}"
+    else:
+        mode = "bit-level SCS-RM" if c.get("bit_level") else "FSSCS-RM"
+        dl = f"D={c['D']}, L={c['L']}"
+    return (f"{cfg}: {mode} PC({c['N']},{c['K']}) Bhattacharyya@{c['design_db']}dB, {crc}, {dl}, "
             f"{c['frames']} frames x Eb/N0 {c['ebno']} dB, BPSK-AWGN float32 LLRs, seed {c['seed']}")
+
+
+def metric_name(c):
+    if c.get("list"):
+        return (f"info-bit Mbps (decoded frames/s) for PC({c['N']},{c['K']}) "
+                f"{'SCL' if c.get('bit_level') else 'FSSCL'} L={c['L']} on 1 B200 vs roofline")
+    return METRIC
+
+
+def oracle_decoder(c):
+    """the oracle decoder matching the bench mode (stack, or list with --list)"""
+    import oracle as O
+    fr = O.bhattacharyya_mask(c["N"], c["K"], c["design_db"])
+    if c.get("list"):
+        return O.SCLDecoder(fr, c["L"], c["crc_poly"], bit_level=bool(c.get("bit_level")))
+    return O.SCSDecoder(fr, c["D"], c["L"], c["crc_poly"], bit_level=bool(c.get("bit_level")))
 
 
 # ------------------------------------------------------------------ clocks
@@ -130,7 +154,7 @@ def oracle_sample(cfg, c, seconds, rank=0):
     import oracle as O
     threads = os.cpu_count() or 1
     fr = O.bhattacharyya_mask(c["N"], c["K"], c["design_db"])
-    dec = O.SCSDecoder(fr, c["D"], c["L"], c["crc_poly"], bit_level=bool(c.get("bit_level")))
+    dec = oracle_decoder(c)
     cc = O.crc_degree(c["crc_poly"]) if c["crc_poly"] else 0
     # calibrate on a small prefix, then size the sample for ~`seconds` of work
     per_point = max(threads, 64)
@@ -177,7 +201,7 @@ def run_reference(args, cfg, c):
     cb = dict(vals[0])
     cb["value"] = value
     out = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": "Mbps", "n_gpus": world,
+        "impl": "reference", "metric": metric_name(c), "value": value, "unit": "Mbps", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * statistics.median(v["seconds"] for v in vals),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": workload_name(cfg, c), "note": "CPU oracle (oracle/oracle.c) on host cores"},
@@ -225,8 +249,15 @@ def run_ours(args, cfg, c):
 
     stream = torch.cuda.current_stream()
 
+    is_list = bool(c.get("list"))
+    if is_list and dec.info["list_ctas"] == 0:
+        raise SystemExit(f"list size L={c['L']} does not fit the FSSCL kernel for N={N}")
+
     def step():
-        dec.decode(llr, out=out, stream=stream)
+        if is_list:
+            dec.decode_list(llr, out=out, stats=False, stream=stream)
+        else:
+            dec.decode(llr, out=out, stream=stream)
 
     def barrier():
         if dist is not None:
@@ -259,15 +290,17 @@ def run_ours(args, cfg, c):
     value = world * frames * K / (ms_per_step / 1e3) / 1e6
 
     # quality (outside the timed region): FER per Eb/N0 point and search stats
-    stats = dec.decode_stats(llr)
+    stats = dec.decode_list(llr) if is_list else dec.decode_stats(llr)
     torch.cuda.synchronize()
     fer = []
     for p in range(npts):
         errs = int((stats["bits"][p * nf:(p + 1) * nf] != blocks).any(1).sum().item())
         tot = shard.reduce_counters({"frames": nf, "frame_errors": errs}, device="cuda")
         fer.append(tot["frame_errors"] / tot["frames"])
-    pops_mean = [float(stats["pops"][p * nf:(p + 1) * nf].float().mean().item()) for p in range(npts)]
-    sw_mean = [float(stats["switches"][p * nf:(p + 1) * nf].float().mean().item()) for p in range(npts)]
+    pops_mean = sw_mean = None
+    if not is_list:
+        pops_mean = [float(stats["pops"][p * nf:(p + 1) * nf].float().mean().item()) for p in range(npts)]
+        sw_mean = [float(stats["switches"][p * nf:(p + 1) * nf].float().mean().item()) for p in range(npts)]
     assert torch.equal(stats["bits"], out), "decode and decode_stats disagree"
 
     # e2e through the public host-buffer API (H2D + decode + D2H in the timed region)
@@ -276,12 +309,12 @@ def run_ours(args, cfg, c):
         host_llr = torch.empty((frames, N), dtype=torch.float32, pin_memory=True)
         host_llr.copy_(llr)
         host_out = torch.empty((frames, K), dtype=torch.uint8, pin_memory=True)
-        dec.decode_host(host_llr, host_out)          # warm-up (allocates staging once)
+        dec.decode_host(host_llr, host_out, list_decoder=is_list)   # warm-up (allocates staging once)
         reps = max(1, min(3, args.steps))
         barrier()
         t0 = time.perf_counter()
         for _ in range(reps):
-            dec.decode_host(host_llr, host_out)
+            dec.decode_host(host_llr, host_out, list_decoder=is_list)
         barrier()
         e2e_s = (time.perf_counter() - t0) / reps
         e2e_s = shard.max_over_ranks(e2e_s, device="cuda")
@@ -304,7 +337,7 @@ def run_ours(args, cfg, c):
     achieved_gbs = alg_bytes / kern_s / 1e9
     traffic = None
     tfile = os.path.join(ROOT, "profiles", f"decode_traffic_{cfg}.json")
-    if os.path.exists(tfile) and not c.get("bit_level"):
+    if os.path.exists(tfile) and not c.get("bit_level") and not is_list:
         with open(tfile) as fh:
             traffic = json.load(fh)["bytes_per_frame"] * frames     # ncu dram bytes, scaled to this launch
     roofline_hbm = {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm_peak, "unit": "GB/s",
@@ -333,23 +366,25 @@ def run_ours(args, cfg, c):
     clocks = clk.summary()
     info = dec.info
     res = {
-        "metric": METRIC, "value": value, "unit": "Mbps", "n_gpus": world, "steps": args.steps,
+        "metric": metric_name(c), "value": value, "unit": "Mbps", "n_gpus": world, "steps": args.steps,
         "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded device generator: Philox payload, "
         "systematic polar encoding, BPSK-AWGN LLRs)",
         "config": {"workload": workload_name(cfg, c), "frames_per_step_per_gpu": frames,
                    "l2": f"inputs {frames * N * 4 / 1e9:.2f} GB per step > 126 MB L2 (no flush needed)",
-                   "launch": {"ctas": info["ctas"], "warps_per_cta": info["warps_per_cta"],
-                              "smem_per_cta": info["smem_per_cta"], "snap_in_smem": info["snap_in_smem"],
-                              "chan_in_smem": info["chan_in_smem"]}},
+                   "launch": ({"ctas": info["list_ctas"], "warps_per_cta": c["L"],
+                               "smem_per_cta": info["list_smem_per_cta"]} if is_list else
+                              {"ctas": info["ctas"], "warps_per_cta": info["warps_per_cta"],
+                               "smem_per_cta": info["smem_per_cta"], "snap_in_smem": info["snap_in_smem"],
+                               "chan_in_smem": info["chan_in_smem"]})},
         "frames_per_s": world * frames / (ms_per_step / 1e3),
         "frames_per_s_per_gpu": fps_rank,
         "roofline": roofline,
         "e2e": e2e, "gpu_launches": args.steps, "clocks": clocks,
         "kernel_ms_median": statistics.median(launch_ms),
         "fer": dict(zip([str(e) for e in c["ebno"]], fer)),
-        "pops_mean": dict(zip([str(e) for e in c["ebno"]], pops_mean)),
-        "switches_mean": dict(zip([str(e) for e in c["ebno"]], sw_mean)),
+        "pops_mean": dict(zip([str(e) for e in c["ebno"]], pops_mean)) if pops_mean else None,
+        "switches_mean": dict(zip([str(e) for e in c["ebno"]], sw_mean)) if sw_mean else None,
         "gen_s": gen_s,
     }
     if rank == 0:
@@ -364,10 +399,11 @@ def run_ours(args, cfg, c):
 def oracle_ops_per_frame(c, npts, n_sample=64):
     """Algorithmic lane-ops per frame (mean over a sample at every Eb/N0 point):
     f/g evaluations (clean pass + spines) + node elements + BETA XOR bits +
-    stack key compares (D per pop and per candidate insert)."""
+    stack key compares (D per pop and per candidate insert); for the list
+    decoder the last term is the prune's sort cost (T log2 T per node)."""
     import oracle as O
     fr = O.bhattacharyya_mask(c["N"], c["K"], c["design_db"])
-    dec = O.SCSDecoder(fr, c["D"], c["L"], c["crc_poly"], bit_level=bool(c.get("bit_level")))
+    dec = oracle_decoder(c)
     cc = O.crc_degree(c["crc_poly"]) if c["crc_poly"] else 0
     pay = ig.payload_bits(c["seed"], 0, n_sample, c["K"] - cc)
     nz = ig.unit_normals(c["seed"], 0, n_sample, c["N"])
@@ -377,7 +413,7 @@ def oracle_ops_per_frame(c, npts, n_sample=64):
         r = dec.decode(O.awgn_llr(cw, nz, eb, c["K"] / c["N"]), counters=True, threads=os.cpu_count() or 1)
         ct = r["counters"]
         tot += (ct["f_ops"] + ct["g_ops"] + ct["node_elems"] + ct["beta_xor_bits"]
-                + c["D"] * (ct["pops"] + ct["cand_created"]))
+                + (ct["sel_compares"] if c.get("list") else c["D"] * (ct["pops"] + ct["cand_created"])))
     return tot / (n_sample * npts)
 
 
@@ -389,6 +425,8 @@ def main():
         c["frames"] = args.frames
     if args.bit_level:
         c["bit_level"] = True
+    if args.list:
+        c["list"] = True
     if args.impl == "reference":
         run_reference(args, cfg, c)
     else:

@@ -171,6 +171,9 @@ int polar_scl_decode(polar_scs_t h, const float *llr, int64_t n_frames, uint8_t 
  */
 int polar_scs_decode_host(polar_scs_t h, const float *llr_host, int64_t n_frames,
                           uint8_t *out_bits_host, void *stream);
+/* The same host-buffer pipeline around the FSSCL list decoder (polar_scl_decode). */
+int polar_scl_decode_host(polar_scs_t h, const float *llr_host, int64_t n_frames,
+                          uint8_t *out_bits_host, void *stream);
 
 /*
  * CRC attach: block = payload || crc(payload), CRC computed MSB first with zero

@@ -56,6 +56,7 @@ _SIGS = {
     "polar_scs_decode_stats": ([_vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp], C.c_int),
     "polar_scs_decode_host": ([_vp, _vp, _i64, _vp, _vp], C.c_int),
     "polar_scl_decode": ([_vp, _vp, _i64, _vp, _vp, _vp, _vp], C.c_int),
+    "polar_scl_decode_host": ([_vp, _vp, _i64, _vp, _vp], C.c_int),
     "polar_crc_attach_batch": ([_vp, _vp, _i64, _vp, _vp], C.c_int),
     "polar_encode_batch": ([_vp, _vp, _i64, _vp, _vp], C.c_int),
     "polar_modulate_batch": ([_vp, _vp, _vp, _i64, _dbl, _vp, _vp], C.c_int),
@@ -177,20 +178,24 @@ class PolarSCS:
                                       st.data_ptr(), _stream_ptr(stream)), "polar_scs_decode_stats")
         return {"bits": bits, "pm": pm, "pops": pops, "switches": sw, "status": st}
 
-    def decode_list(self, llr, stream=None):
-        """FSSCL list decoding with list size L (polar_scl_decode)."""
+    def decode_list(self, llr, out=None, stats=True, stream=None):
+        """FSSCL list decoding with list size L (polar_scl_decode).
+        Returns {"bits", "pm", "status"} (stats=False: only the bits are written)."""
         import torch
         n = llr.shape[0]
         dev = llr.device
-        bits = torch.empty((n, self.K), dtype=torch.uint8, device=dev)
-        pm = torch.empty(n, dtype=torch.float32, device=dev)
-        st = torch.empty(n, dtype=torch.uint8, device=dev)
-        _check(polar_scl_decode(self._h, _dev(llr, torch.float32, (n, self.N), "llr"), n, bits.data_ptr(),
-                                pm.data_ptr(), st.data_ptr(), _stream_ptr(stream)), "polar_scl_decode")
-        return {"bits": bits, "pm": pm, "status": st}
+        bits = out if out is not None else torch.empty((n, self.K), dtype=torch.uint8, device=dev)
+        pm = torch.empty(n, dtype=torch.float32, device=dev) if stats else None
+        st = torch.empty(n, dtype=torch.uint8, device=dev) if stats else None
+        _check(polar_scl_decode(self._h, _dev(llr, torch.float32, (n, self.N), "llr"), n,
+                                _dev(bits, torch.uint8, (n, self.K), "out"),
+                                pm.data_ptr() if stats else None, st.data_ptr() if stats else None,
+                                _stream_ptr(stream)), "polar_scl_decode")
+        return {"bits": bits, "pm": pm, "status": st} if stats else {"bits": bits}
 
-    def decode_host(self, llr_host, out_host=None, stream=None):
-        """End-to-end from host memory (numpy array or CPU tensor, ideally pinned)."""
+    def decode_host(self, llr_host, out_host=None, stream=None, list_decoder=False):
+        """End-to-end from host memory (numpy array or CPU tensor, ideally pinned);
+        list_decoder=True runs the FSSCL list decoder (polar_scl_decode_host)."""
         import torch
         if isinstance(llr_host, np.ndarray):
             llr_host = torch.from_numpy(np.ascontiguousarray(llr_host, dtype=np.float32))
@@ -199,8 +204,8 @@ class PolarSCS:
         n = llr_host.shape[0]
         if out_host is None:
             out_host = torch.empty((n, self.K), dtype=torch.uint8, pin_memory=llr_host.is_pinned())
-        _check(polar_scs_decode_host(self._h, llr_host.data_ptr(), n, out_host.data_ptr(),
-                                     _stream_ptr(stream)), "polar_scs_decode_host")
+        fn = polar_scl_decode_host if list_decoder else polar_scs_decode_host
+        _check(fn(self._h, llr_host.data_ptr(), n, out_host.data_ptr(), _stream_ptr(stream)), fn.__name__)
         return out_host
 
     # ---------------------------------------------------------------- workload side

@@ -85,6 +85,17 @@ int decode_impl(polar_scs_t h, const float *llr, int64_t n, uint8_t *bits, float
                                      h->smem_per_cta, st));
 }
 
+int list_impl(polar_scs_t h, const float *llr, int64_t n, uint8_t *bits, float *pm, uint8_t *status, cudaStream_t st,
+              int slot = 0) {
+    ListParams p = h->list;
+    p.llr = llr; p.n_frames = n; p.out_bits = bits; p.pm = pm; p.status = status;
+    p.queue = h->d_queue + slot;
+    cudaError_t e = cudaMemsetAsync(p.queue, 0, sizeof(unsigned long long), st);
+    if (e != cudaSuccess) return cuda_status(e);
+    const int ctas = (int)std::min<int64_t>(h->list_ctas, n);
+    return cuda_status(launch_list(p, h->list_lcap, ctas, h->list_smem, st));
+}
+
 // FSSCL shared-memory layout (list.cu): offsets in 32-bit words, each area
 // 16-byte aligned.  Returns the total words.
 int list_layout(ListParams &p) {
@@ -273,18 +284,13 @@ int polar_scl_decode(polar_scs_t h, const float *llr, int64_t n, uint8_t *bits, 
     if (n == 0) return POLAR_OK;
     if (!llr || !bits) return POLAR_EINVAL;
     if (h->t.N >= 4 && (reinterpret_cast<uintptr_t>(llr) & 15u)) return POLAR_EINVAL;
-    ListParams p = h->list;
-    p.llr = llr; p.n_frames = n; p.out_bits = bits; p.pm = pm; p.status = status;
-    p.queue = h->d_queue;
-    cudaStream_t st = static_cast<cudaStream_t>(stream);
-    cudaError_t e = cudaMemsetAsync(p.queue, 0, sizeof(unsigned long long), st);
-    if (e != cudaSuccess) return cuda_status(e);
-    const int ctas = (int)std::min<int64_t>(h->list_ctas, n);
-    return cuda_status(launch_list(p, h->list_lcap, ctas, h->list_smem, st));
+    return list_impl(h, llr, n, bits, pm, status, static_cast<cudaStream_t>(stream));
 }
 
-int polar_scs_decode_host(polar_scs_t h, const float *llr_host, int64_t n, uint8_t *bits_host, void *stream) {
+static int decode_host_impl(polar_scs_t h, bool list, const float *llr_host, int64_t n, uint8_t *bits_host,
+                            void *stream) {
     if (!h || n < 0) return POLAR_EINVAL;
+    if (list && h->list_ctas == 0) return POLAR_ENOTSYS;
     if (n == 0) return POLAR_OK;
     if (!llr_host || !bits_host) return POLAR_EINVAL;
     const int N = h->t.N, K = h->t.K;
@@ -324,8 +330,9 @@ int polar_scs_decode_host(polar_scs_t h, const float *llr_host, int64_t n, uint8
         cudaEventRecord(h->ev_h2d[b], h->s_h2d);
         cudaStreamWaitEvent(h->s_comp[b], h->ev_h2d[b], 0);
         cudaStreamWaitEvent(h->s_comp[b], h->ev_d2h[b], 0);   // bits buffer b has been copied out
-        rc = decode_impl(h, h->d_stage_llr[b], cnt, h->d_stage_bits[b], nullptr, nullptr, nullptr, nullptr,
-                         h->s_comp[b], b);
+        rc = list ? list_impl(h, h->d_stage_llr[b], cnt, h->d_stage_bits[b], nullptr, nullptr, h->s_comp[b], b)
+                  : decode_impl(h, h->d_stage_llr[b], cnt, h->d_stage_bits[b], nullptr, nullptr, nullptr, nullptr,
+                                h->s_comp[b], b);
         cudaEventRecord(h->ev_dec[b], h->s_comp[b]);
         cudaStreamWaitEvent(h->s_d2h, h->ev_dec[b], 0);
         e = cudaMemcpyAsync(bits_host + off * K, h->d_stage_bits[b], (size_t)cnt * K, cudaMemcpyDeviceToHost, h->s_d2h);
@@ -341,6 +348,14 @@ int polar_scs_decode_host(polar_scs_t h, const float *llr_host, int64_t n, uint8
     if (rc == POLAR_OK && e != cudaSuccess) rc = cuda_status(e);
     cudaEventDestroy(start);
     return rc;
+}
+
+int polar_scs_decode_host(polar_scs_t h, const float *llr_host, int64_t n, uint8_t *bits_host, void *stream) {
+    return decode_host_impl(h, false, llr_host, n, bits_host, stream);
+}
+
+int polar_scl_decode_host(polar_scs_t h, const float *llr_host, int64_t n, uint8_t *bits_host, void *stream) {
+    return decode_host_impl(h, true, llr_host, n, bits_host, stream);
 }
 
 int polar_crc_attach_batch(polar_scs_t h, const uint8_t *payload, int64_t n, uint8_t *block, void *stream) {
