@@ -98,7 +98,10 @@ int polar_construct_from_sequence(int32_t N, int32_t K, const int32_t *seq, int3
  * persistent decode launch and its workspace.  Host only + cudaMalloc/copies.
  *   N: power of two in [2, 4096]; K = number of information bits INCLUDING
  *   the crc bits (reading R14), 1 <= K <= N; frozen_mask: host [N], 1 =
- *   frozen, must have exactly N-K ones; D in [1, 128]; L >= 1 (values above
+ *   frozen, must have exactly N-K ones; D in [1, 8192] (D <= 128: the stack
+ *   lives in registers; D > 128, up to the paper's D = NL = 8192 (PAPER.md:
+ *   L599, L966): a per-warp stack in global memory, L2-resident in practice,
+ *   with its snapshot arena of D x N/8 bytes per resident warp); L >= 1 (values above
  *   65535 are clamped: they never prune); crc_poly: 0 = none, else the full
  *   generator including the x^c term (0x11021 = CRC-16 0x1021, 0x107 = CRC-8
  *   0x07), degree c in [1, 31] and c < K; flags: POLAR_FLAG_*.

@@ -114,6 +114,13 @@ CONFIGS = {
                ebno=[1.5, 2.5], seed=3),
     "C5": dict(N=4096, K=3072, design_db=3.5, crc_poly=0x107, D=128, L=32, frames=1_000_000,
                ebno=[3.0, 4.0], seed=4),
+    # The paper's own simulation setup:
+    # PC(1024,512) with CRC-24C 0xB2B117 (K counts its 24 bits), L = 8 and the
+    # maximum stack D = NL = 8192, Eb/N0 0..3 dB as in Fig. 8 (L974-1122).  The
+    # paper's 3GPP information set is not in this container; Bhattacharyya at
+    # 2 dB stands in (polar_construct_from_sequence accepts the real sequence).
+    "P": dict(N=1024, K=512, design_db=2.0, crc_poly=0x1B2B117, D=8192, L=8, frames=50_000,
+              ebno=[0.0, 0.5, 1.0, 1.5, 2.0, 2.5, 3.0], seed=5),
 }
 
 # Every Eb/N0 point of a config uses the same payload and noise draws (common

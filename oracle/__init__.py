@@ -46,7 +46,7 @@ class Counters(C.Structure):
     _fields_ = [(n, C.c_uint64) for n in (
         "pops", "switches", "f_ops", "g_ops", "spine_elems", "beta_xor_bits", "node_elems",
         "node_visits", "cand_created", "cand_inserted", "cand_replaced", "cand_dropped",
-        "pruned", "crc_checks", "sel_compares")]
+        "pruned", "crc_checks", "sel_compares", "stack_peak")]
 
     def as_dict(self):
         return {n: int(getattr(self, n)) for n, _ in self._fields_}
@@ -317,7 +317,7 @@ class SCSDecoder:
             tot = {}
             for ct in cts:
                 for k, v in ct.as_dict().items():
-                    tot[k] = tot.get(k, 0) + v
+                    tot[k] = max(tot.get(k, 0), v) if k == "stack_peak" else tot.get(k, 0) + v
             out["counters"] = tot
         return out
 
@@ -375,6 +375,6 @@ class SCLDecoder:
             tot = {}
             for ct in cts:
                 for k, v in ct.as_dict().items():
-                    tot[k] = tot.get(k, 0) + v
+                    tot[k] = max(tot.get(k, 0), v) if k == "stack_peak" else tot.get(k, 0) + v
             out["counters"] = tot
         return out

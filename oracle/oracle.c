@@ -608,6 +608,7 @@ static int decode_one(const orc_scs_t *h, const float *chan, uint8_t *block, uin
             memcpy(dst->beta, beta_work, (size_t)N);
             apply_candidate(kind, Lam, seg_base, m, c[t].mask, dst->beta + phi * Lam);
         }
+        if (ct && (uint64_t)nS > ct->stack_peak) ct->stack_peak = (uint64_t)nS;
     }
 }
 

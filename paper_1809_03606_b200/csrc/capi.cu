@@ -36,13 +36,13 @@ cudaError_t upload(T **dst, const std::vector<T> &src) {
     return e;
 }
 
-int slots_for(int D) { return D <= 32 ? 1 : (D <= 64 ? 2 : 4); }
+int slots_for(int D) { return D <= 32 ? 1 : (D <= 64 ? 2 : (D <= 128 ? 4 : 0)); }   // 0: global stack
 int round4(int w) { return (w + 3) & ~3; }
 
 void free_handle(polar_scs_t h) {
     if (!h) return;
     cudaFree(h->t.nodes); cudaFree(h->t.info); cudaFree(h->t.crc_tab); cudaFree(h->t.crc_bytes); cudaFree(h->t.info_words);
-    cudaFree(h->d_queue); cudaFree(h->d_snap);
+    cudaFree(h->d_queue); cudaFree(h->d_snap); cudaFree(h->d_stack); cudaFree(h->d_hdr);
     for (int b = 0; b < 2; b++) {
         cudaFree(h->d_stage_llr[b]); cudaFree(h->d_stage_bits[b]);
         if (h->ev_h2d[b]) cudaEventDestroy(h->ev_h2d[b]);
@@ -79,6 +79,8 @@ int decode_impl(polar_scs_t h, const float *llr, int64_t n, uint8_t *bits, float
     p.pm = pm; p.pops = pops; p.switches = sw; p.status = status;
     p.queue = h->d_queue + slot;
     if (h->d_snap) p.snap_global = h->d_snap + (h->snap_bytes / 4) * (size_t)slot;
+    if (h->d_stack) p.stack_global = h->d_stack + h->stack_words * (size_t)slot;
+    if (h->d_hdr) p.hdr_global = h->d_hdr + h->hdr_count * (size_t)slot;
     cudaError_t e = cudaMemsetAsync(p.queue, 0, sizeof(unsigned long long), st);
     if (e != cudaSuccess) return cuda_status(e);
     return cuda_status(launch_decode(p, slots_for(h->D), h->snap_in_smem != 0, h->chan_in_smem != 0, h->ctas,
@@ -179,6 +181,8 @@ int polar_scs_create_ex(polar_scs_t *out, int32_t N, int32_t K, const uint8_t *f
     p.N = N; p.n = t.n; p.K = K; p.c = t.c; p.D = D; p.L = h->L; p.M = t.M;
     p.nw = nw; p.snap_stride = sstride; p.sched_words = sched_words; p.cnt_words = cnt_words;
     p.nonsys = (flags & POLAR_FLAG_NONSYSTEMATIC) ? 1 : 0;
+    p.hdr_words = slots ? 2 * D : 0;
+    p.used_words = slots ? 4 : round4((D + 31) / 32);
 
     // Layout choice: per warp, alpha stages >= 6 (N floats incl. scratch), flat
     // beta, best-effort beta and counters always live in shared memory; the
@@ -194,8 +198,9 @@ int polar_scs_create_ex(polar_scs_t *out, int32_t N, int32_t K, const uint8_t *f
         for (int si = 0; si < 2; si++) {
             const bool snap_smem = (si == 0);
             if (snap_smem && (flags & POLAR_FLAG_SNAP_GLOBAL)) continue;
+            if (snap_smem && slots == 0) continue;          // D > 128: the arena is global
             if (!snap_smem && (flags & POLAR_FLAG_SNAP_SMEM)) continue;
-            const int ww = round4((chan_smem ? N : 0) + N + 2 * nw + cnt_words + 2 * D + 4 + nw +
+            const int ww = round4((chan_smem ? N : 0) + N + 2 * nw + cnt_words + p.hdr_words + p.used_words + nw +
                                   (snap_smem ? D * sstride : 0));
             const int smem = 4 * (sched_words + kDecodeWarps * ww);
             if (smem > optin) continue;
@@ -222,6 +227,16 @@ int polar_scs_create_ex(polar_scs_t *out, int32_t N, int32_t K, const uint8_t *f
         e = cudaMalloc(&h->d_snap, 2 * h->snap_bytes);
         if (e != cudaSuccess) { free_handle(h); return cuda_status(e); }
         p.snap_global = h->d_snap;
+    }
+    if (slots == 0) {
+        const size_t warps = (size_t)h->ctas * kDecodeWarps;
+        h->stack_words = warps * 3 * (size_t)D;
+        h->hdr_count = warps * (size_t)D;
+        e = cudaMalloc(&h->d_stack, 2 * h->stack_words * sizeof(uint32_t));
+        if (e == cudaSuccess) e = cudaMalloc(&h->d_hdr, 2 * h->hdr_count * sizeof(uint2));
+        if (e != cudaSuccess) { free_handle(h); return cuda_status(e); }
+        p.stack_global = h->d_stack;
+        p.hdr_global = h->d_hdr;
     }
     // ---- FSSCL launch (polar_scl_decode): one CTA of L warps per frame
     if (h->L <= 32) {

@@ -82,13 +82,25 @@ __device__ __forceinline__ void alpha_stage(const float *chan, float *alpha, con
 }
 
 // Stack entry packing: jsm = j (13 bits: decision-node ordinal = schedule
-// progress) | snapshot slot (8 bits, 0xFF none) << 13 |
-// flip mask relative to the snapshot (4 bits) << 21.
+// progress) | snapshot slot << 13 | flip mask relative to the
+// snapshot (4 bits).  Register stacks (D <= 128): 8-bit slot (0xFF none), mask
+// at bit 21.  Global stacks (D > 128): 14-bit slot (0x3FFF none), mask at 27.
+template <bool BIG>
+struct Pk {
+    static constexpr uint32_t NONE = BIG ? 0x3FFFu : 0xFFu;
+    static constexpr int MSH = BIG ? 27 : 21;
+    __device__ static __forceinline__ uint32_t j(uint32_t x) { return x & 0x1FFFu; }
+    __device__ static __forceinline__ uint32_t snap(uint32_t x) { return (x >> 13) & NONE; }
+    __device__ static __forceinline__ uint32_t mask(uint32_t x) { return (x >> MSH) & 0xFu; }
+    __device__ static __forceinline__ uint32_t make(uint32_t jj, uint32_t sn, uint32_t m) {
+        return jj | (sn << 13) | (m << MSH);
+    }
+};
 __device__ __forceinline__ uint32_t jsm_j(uint32_t x) { return x & 0x1FFFu; }
-__device__ __forceinline__ uint32_t jsm_snap(uint32_t x) { return (x >> 13) & 0xFFu; }
-__device__ __forceinline__ uint32_t jsm_mask(uint32_t x) { return (x >> 21) & 0xFu; }
+__device__ __forceinline__ uint32_t jsm_snap(uint32_t x) { return Pk<false>::snap(x); }
+__device__ __forceinline__ uint32_t jsm_mask(uint32_t x) { return Pk<false>::mask(x); }
 __device__ __forceinline__ uint32_t jsm_make(uint32_t j, uint32_t snap, uint32_t mask) {
-    return j | (snap << 13) | (mask << 21);
+    return Pk<false>::make(j, snap, mask);
 }
 constexpr uint32_t SNAP_NONE = 0xFFu;
 
@@ -165,9 +177,64 @@ __device__ __forceinline__ int alloc_snapshot_lazy(uint32_t *used, const uint32_
     return slot;
 }
 
+// Global stack (D > 128): the same conservative bitmap over D slots, in
+// shared memory (UW = ceil(D/32) words), searched from a hint word (every word
+// below it is full); the exact recount scans the live entries of the global
+// stack (all but entry `skip`) and marks `extra`.
+__device__ __forceinline__ int alloc_snapshot_big(uint32_t *used, int &uhint, const uint32_t *sjsm, int nS, int D,
+                                                  int skip, uint32_t extra, int lane) {
+    const int UW = (D + 31) >> 5;
+    int slot = -1;
+    #pragma unroll 1
+    for (int pass = 0; pass < 2 && slot < 0; pass++) {
+        if (pass == 1) {
+            #pragma unroll 1
+            for (int w = lane; w < UW; w += 32) used[w] = 0u;
+            __syncwarp();
+            #pragma unroll 1
+            for (int i = lane; i < nS; i += 32) {
+                const uint32_t sn = Pk<true>::snap(sjsm[i]);
+                if (i != skip && sn != Pk<true>::NONE) atomicOr(used + (sn >> 5), 1u << (sn & 31));
+            }
+            __syncwarp();
+            if (lane == 0 && extra != Pk<true>::NONE) used[extra >> 5] |= 1u << (extra & 31);
+            __syncwarp();
+            uhint = 0;
+        }
+        #pragma unroll 1
+        for (int w0 = uhint; w0 < UW; w0 += 32) {
+            const int wi = w0 + lane;
+            uint32_t fm = 0;
+            if (wi < UW) {
+                fm = ~used[wi];
+                const int lim = D - wi * 32;
+                if (lim < 32) fm &= (1u << lim) - 1u;
+            }
+            const uint32_t b = __ballot_sync(FULL, fm != 0u);
+            if (b) {
+                const int fl = __ffs(b) - 1;
+                const uint32_t fv = __shfl_sync(FULL, fm, fl);
+                slot = 32 * (w0 + fl) + __ffs(fv) - 1;
+                uhint = w0 + fl;
+                break;
+            }
+        }
+    }
+    __syncwarp();
+    if (lane == 0) used[slot >> 5] |= 1u << (slot & 31);
+    __syncwarp();
+    return slot;
+}
+
+// SLOTS = 1, 2, 4: register stack of 32 SLOTS entries (D <= 128).  SLOTS = 0:
+// global stack (D up to 8192, the paper's D = NL): dense unsorted arrays per
+// warp in global memory (L2-resident in practice), scanned by the 32 lanes.
 template <int SLOTS, bool SNAP_SMEM, bool CHAN_SMEM, int NL = 0>
 __global__ void __launch_bounds__(kDecodeWarps * 32, SLOTS == 4 ? 3 : (SLOTS == 2 ? 5 : kDecodeMinBlocks))
 fsscs_decode_kernel(const DecodeParams P) {
+    constexpr bool BIG = (SLOTS == 0);
+    constexpr int SL = BIG ? 1 : SLOTS;       // register arrays (unused when BIG)
+    using PK = Pk<BIG>;
     extern __shared__ __align__(16) uint32_t smem[];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
@@ -191,12 +258,18 @@ fsscs_decode_kernel(const DecodeParams P) {
     uint32_t *beta = reinterpret_cast<uint32_t *>(alpha + N);
     uint32_t *best = beta + nw;
     uint16_t *cnt = reinterpret_cast<uint16_t *>(best + nw);
-    uint32_t *shdr = best + nw + P.cnt_words;                      // fork headers m1..m4, 2 words/slot
-    uint32_t *snap_used = shdr + 2 * D;                            // 4 words: snapshot-slot bitmap
-    uint32_t *uhat = snap_used + 4;                                // nw words: u_hat (non-systematic)
+    uint32_t *shdr = best + nw + P.cnt_words;                      // fork headers m1..m4, 2 words/slot (!BIG)
+    uint32_t *snap_used = shdr + P.hdr_words;                      // snapshot-slot bitmap (used_words)
+    uint32_t *uhat = snap_used + P.used_words;                     // nw words: u_hat (non-systematic)
     // snapshot slot k of this warp: shared memory, or global slot index snap0 + k
-    uint32_t *snap_s = shdr + 2 * D + 4 + nw;
-    const uint32_t snap0 = (uint32_t)(blockIdx.x * kDecodeWarps + warp) * (uint32_t)D;
+    uint32_t *snap_s = uhat + nw;
+    const uint32_t gwarp = (uint32_t)(blockIdx.x * kDecodeWarps + warp);
+    const uint32_t snap0 = gwarp * (uint32_t)D;
+    // global stack (BIG): PM bits, serials, jsm words; fork headers per slot
+    uint32_t *spm = BIG ? P.stack_global + (size_t)gwarp * 3 * (size_t)D : nullptr;
+    uint32_t *sser = spm + D, *sjsm = spm + 2 * (size_t)D;
+    uint2 *ghdr = BIG ? P.hdr_global + (size_t)gwarp * (size_t)D : nullptr;
+    auto hdr_at = [&](int k) -> uint2 * { return BIG ? ghdr + k : reinterpret_cast<uint2 *>(shdr) + k; };
     const int sstride = (NL > 0) ? nw : P.snap_stride;
     auto snap_slot = [&](int k) -> uint32_t * {
         if (SNAP_SMEM) return snap_s + k * sstride;
@@ -239,12 +312,20 @@ fsscs_decode_kernel(const DecodeParams P) {
         __syncwarp();
 
         // ---- stack: root path (PM 0, serial 0, j 0) ------------------------
-        uint32_t s_pm[SLOTS], s_ser[SLOTS], s_jsm[SLOTS];
+        uint32_t s_pm[SL], s_ser[SL], s_jsm[SL];
 #pragma unroll
-        for (int s = 0; s < SLOTS; s++) { s_pm[s] = EMPTY; s_ser[s] = EMPTY; s_jsm[s] = jsm_make(0, SNAP_NONE, 0); }
+        for (int s = 0; s < SL; s++) { s_pm[s] = EMPTY; s_ser[s] = EMPTY; s_jsm[s] = PK::make(0, PK::NONE, 0); }
         if (lane == 0) { s_pm[0] = 0u; s_ser[0] = 0u; }
         int nS = 1;
-        if (lane < 4) snap_used[lane] = 0u;      // conservative snapshot-slot bitmap (alloc_snapshot_lazy)
+        int uhint = 0;
+        if (BIG) {
+            if (lane == 0) { spm[0] = 0u; sser[0] = 0u; sjsm[0] = PK::make(0, PK::NONE, 0); }
+            #pragma unroll 1
+            for (int w = lane; w < P.used_words; w += 32) snap_used[w] = 0u;
+        } else if (lane < 4) {
+            snap_used[lane] = 0u;      // conservative snapshot-slot bitmap (alloc_snapshot_lazy)
+        }
+        __syncwarp();
         uint32_t work = 0, next_serial = 1, pops = 0, switches = 0;
         int work_pl = 0;
         // alpha memory content: stages s >= lev_mem hold the node (s, pos_mem >> s)
@@ -269,16 +350,35 @@ fsscs_decode_kernel(const DecodeParams P) {
             // ---- select: min (PM, serial) (reading R7)
             uint32_t lpm = EMPTY, lser = EMPTY, ljsm = 0;
             int ls = 0;
+            if (BIG) {
+                #pragma unroll 1
+                for (int i = lane; i < nS; i += 32) {
+                    const uint32_t a = __ldcg(spm + i), b = __ldcg(sser + i);
+                    if (a < lpm || (a == lpm && b < lser)) { lpm = a; lser = b; ls = i; }
+                }
+            } else {
 #pragma unroll
-            for (int s = 0; s < SLOTS; s++)
-                if (s_pm[s] < lpm || (s_pm[s] == lpm && s_ser[s] < lser)) { lpm = s_pm[s]; lser = s_ser[s]; ljsm = s_jsm[s]; ls = s; }
+                for (int s = 0; s < SL; s++)
+                    if (s_pm[s] < lpm || (s_pm[s] == lpm && s_ser[s] < lser)) { lpm = s_pm[s]; lser = s_ser[s]; ljsm = s_jsm[s]; ls = s; }
+            }
             uint32_t mpm, mser;
             warp_min_key(lpm, lser, mpm, mser);
             const int owner = __ffs(__ballot_sync(FULL, lpm == mpm && lser == mser)) - 1;
-            const uint32_t p_jsm = __shfl_sync(FULL, ljsm, owner);
-            if (lane == owner) {
+            uint32_t p_jsm;
+            if (BIG) {
+                // remove entry `pi`: the last entry moves into its place
+                const int pi = __shfl_sync(FULL, ls, owner);
+                p_jsm = __ldcg(sjsm + pi);
+                if (lane == 0 && pi != nS - 1) {
+                    spm[pi] = __ldcg(spm + nS - 1); sser[pi] = __ldcg(sser + nS - 1); sjsm[pi] = __ldcg(sjsm + nS - 1);
+                }
+                __syncwarp();
+            } else {
+                p_jsm = __shfl_sync(FULL, ljsm, owner);
+                if (lane == owner) {
 #pragma unroll
-                for (int s = 0; s < SLOTS; s++) if (s == ls) { s_pm[s] = EMPTY; s_ser[s] = EMPTY; }
+                    for (int s = 0; s < SL; s++) if (s == ls) { s_pm[s] = EMPTY; s_ser[s] = EMPTY; }
+                }
             }
             nS--;
             pops++;
@@ -292,10 +392,29 @@ fsscs_decode_kernel(const DecodeParams P) {
             if (lane == 0) cnt[j] = (uint16_t)c_j;
             if (c_j == P.L) {
                 int cntv = 0;
+                if (BIG) {
+                    // in-place compaction of the entries with depth > j
+                    #pragma unroll 1
+                    for (int i0 = 0; i0 < nS; i0 += 32) {
+                        const int i = i0 + lane;
+                        uint32_t a = 0, b = 0, x = 0;
+                        if (i < nS) { a = __ldcg(spm + i); b = __ldcg(sser + i); x = __ldcg(sjsm + i); }
+                        const bool keep = (i < nS) && (int)PK::j(x) > j;
+                        const uint32_t kb = __ballot_sync(FULL, keep);
+                        __syncwarp();
+                        if (keep) {
+                            const int o = cntv + __popc(kb & ((1u << lane) - 1u));
+                            spm[o] = a; sser[o] = b; sjsm[o] = x;
+                        }
+                        cntv += __popc(kb);
+                    }
+                    __syncwarp();
+                } else {
 #pragma unroll
-                for (int s = 0; s < SLOTS; s++) {
-                    if (s_ser[s] != EMPTY && (int)jsm_j(s_jsm[s]) <= j) { s_pm[s] = EMPTY; s_ser[s] = EMPTY; }
-                    cntv += __popc(__ballot_sync(FULL, s_ser[s] != EMPTY));
+                    for (int s = 0; s < SL; s++) {
+                        if (s_ser[s] != EMPTY && (int)jsm_j(s_jsm[s]) <= j) { s_pm[s] = EMPTY; s_ser[s] = EMPTY; }
+                        cntv += __popc(__ballot_sync(FULL, s_ser[s] != EMPTY));
+                    }
                 }
                 nS = cntv;
             }
@@ -313,33 +432,54 @@ fsscs_decode_kernel(const DecodeParams P) {
             if (p_ser != work) {
                 switches++;
                 // the path being left keeps its beta in a snapshot if it is still live
+                if (BIG) {
+                    int wi = -1;
+                    #pragma unroll 1
+                    for (int i0 = 0; i0 < nS && wi < 0; i0 += 32) {
+                        const int i = i0 + lane;
+                        const uint32_t hb = __ballot_sync(FULL, i < nS && __ldcg(sser + i) == work);
+                        if (hb) wi = i0 + __ffs(hb) - 1;
+                    }
+                    if (wi >= 0) {
+                        const uint32_t wj = __ldcg(sjsm + wi);
+                        if (PK::snap(wj) == PK::NONE) {
+                            const int slot = alloc_snapshot_big(snap_used, uhint, sjsm, nS, D, -1, PK::snap(p_jsm), lane);
+                            uint32_t *dst = snap_slot(slot);
+                            const int nwords = (work_pl + 31) >> 5;
+                            #pragma unroll 1
+                            for (int w = lane; w < nwords; w += 32) dst[w] = beta[w];
+                            if (lane == 0) sjsm[wi] = PK::make(PK::j(wj), (uint32_t)slot, 0);
+                            __syncwarp();
+                        }
+                    }
+                }
                 int wsl = -1;
 #pragma unroll
-                for (int s = 0; s < SLOTS; s++) if (s_ser[s] == work) wsl = s;
+                for (int s = 0; s < SL; s++) if (!BIG && s_ser[s] == work) wsl = s;
                 const uint32_t wb_ = __ballot_sync(FULL, wsl >= 0);
-                if (wb_) {
+                if (!BIG && wb_) {
                     const int wl = __ffs(wb_) - 1;
                     uint32_t wj = 0;
 #pragma unroll
-                    for (int s = 0; s < SLOTS; s++) if (s == wsl) wj = s_jsm[s];
+                    for (int s = 0; s < SL; s++) if (s == wsl) wj = s_jsm[s];
                     wj = __shfl_sync(FULL, wj, wl);
                     const int wslot = __shfl_sync(FULL, wsl, wl);
                     if (jsm_snap(wj) == SNAP_NONE) {
-                        const int slot = alloc_snapshot_lazy<SLOTS>(snap_used, s_ser, s_jsm, D, -1, 0, jsm_snap(p_jsm), lane);
+                        const int slot = alloc_snapshot_lazy<SL>(snap_used, s_ser, s_jsm, D, -1, 0, jsm_snap(p_jsm), lane);
                         uint32_t *dst = snap_slot(slot);
                         const int nwords = (work_pl + 31) >> 5;
                         #pragma unroll 1
                         for (int w = lane; w < nwords; w += 32) dst[w] = beta[w];
                         if (lane == wl) {
 #pragma unroll
-                            for (int s = 0; s < SLOTS; s++)
+                            for (int s = 0; s < SL; s++)
                                 if (s == wslot) s_jsm[s] = jsm_make(jsm_j(wj), (uint32_t)slot, 0);
                         }
                     }
                 }
                 // restore p's beta (fork snapshot), locating the first bit d where it
                 // differs from the beta the alpha memory was computed from
-                const uint32_t ps = jsm_snap(p_jsm), rel = jsm_mask(p_jsm);
+                const uint32_t ps = PK::snap(p_jsm), rel = PK::mask(p_jsm);
                 const uint32_t *src = snap_slot((int)ps);
                 const int nwords = (pl + 31) >> 5;
                 int d = 0x7FFFFFFF;
@@ -372,7 +512,7 @@ fsscs_decode_kernel(const DecodeParams P) {
                             beta[seg >> 5] ^= ((1u << Lam) - 1u) << (seg & 31);
                         }
                     } else if (lane == 0) {
-                        const uint2 hh = reinterpret_cast<const uint2 *>(shdr)[ps];
+                        const uint2 hh = *hdr_at((int)ps);
                         const uint32_t h0 = hh.x, h1 = hh.y;
                         const uint32_t m[4] = {h0 & 0xFFFFu, h0 >> 16, h1 & 0xFFFFu, h1 >> 16};
 #pragma unroll
@@ -704,23 +844,33 @@ fsscs_decode_kernel(const DecodeParams P) {
             int fslot = -1;
             const int nfit = min(nc, D - nS);
             auto write_fork_snapshot = [&](int victim_lane, int victim_slot) {
-                fslot = alloc_snapshot_lazy<SLOTS>(snap_used, s_ser, s_jsm, D, victim_lane, victim_slot, SNAP_NONE, lane);
+                if (BIG) fslot = alloc_snapshot_big(snap_used, uhint, sjsm, nS, D, victim_slot, PK::NONE, lane);
+                else fslot = alloc_snapshot_lazy<SL>(snap_used, s_ser, s_jsm, D, victim_lane, victim_slot, SNAP_NONE, lane);
                 uint32_t *dst = snap_slot(fslot);
                 const int nwords = (npl + 31) >> 5;
                 #pragma unroll 1
                 for (int w = lane; w < nwords; w += 32) dst[w] = beta[w];
-                if (lane == 0) {
-                    reinterpret_cast<uint2 *>(shdr)[fslot] = make_uint2(mi[0] | (mi[1] << 16), mi[2] | (mi[3] << 16));
-                }
+                if (lane == 0) *hdr_at(fslot) = make_uint2(mi[0] | (mi[1] << 16), mi[2] | (mi[3] << 16));
             };
-            if (nfit > 1) write_fork_snapshot(-1, 0);
+            if (nfit > 1) write_fork_snapshot(-1, -1);
             int c1_lane = 0, c1_slot = 0;
-            {
+            if (BIG) {
+                const uint32_t jbase = PK::make(jn, (nfit == 1) ? PK::NONE : (uint32_t)fslot, 0);
+                if (lane < nfit) {
+                    const uint32_t mk = (clist >> (4 * lane)) & 15u;
+                    spm[nS + lane] = __float_as_uint(p_pm + my_d);
+                    sser[nS + lane] = ser0 + (uint32_t)lane;
+                    sjsm[nS + lane] = jbase | ((mk ^ (uint32_t)m0) << PK::MSH);
+                }
+                c1_slot = nS;
+                __syncwarp();
+                nS += nfit;
+            } else {
                 int base = 0;
                 bool c1_found = false;
                 const uint32_t jbase = jsm_make(jn, (nfit == 1) ? SNAP_NONE : (uint32_t)fslot, 0);
 #pragma unroll
-                for (int s = 0; s < SLOTS; s++) {
+                for (int s = 0; s < SL; s++) {
                     const bool fr = (s_ser[s] == EMPTY);
                     const uint32_t fb = __ballot_sync(FULL, fr);
                     const int k = base + __popc(fb & ((1u << lane) - 1u));    // rank among free entries
@@ -748,28 +898,45 @@ fsscs_decode_kernel(const DecodeParams P) {
                 const float dt = __shfl_sync(FULL, my_d, r);
                 const uint32_t cpm = __float_as_uint(p_pm + dt);
                 uint32_t xpm = 0, xser = 0;
-                int xs = 0;
+                int xs = -1;
+                if (BIG) {
+                    #pragma unroll 1
+                    for (int i = lane; i < nS; i += 32) {
+                        const uint32_t a = __ldcg(spm + i), b = __ldcg(sser + i);
+                        if (xs < 0 || a > xpm || (a == xpm && b > xser)) { xpm = a; xser = b; xs = i; }
+                    }
+                } else {
 #pragma unroll
-                for (int s = 0; s < SLOTS; s++)
-                    if (s_ser[s] != EMPTY && (s_pm[s] > xpm || (s_pm[s] == xpm && s_ser[s] >= xser))) { xpm = s_pm[s]; xser = s_ser[s]; xs = s; }
+                    for (int s = 0; s < SL; s++)
+                        if (s_ser[s] != EMPTY && (xs < 0 || s_pm[s] > xpm || (s_pm[s] == xpm && s_ser[s] > xser))) { xpm = s_pm[s]; xser = s_ser[s]; xs = s; }
+                }
                 const uint32_t Mpm = __reduce_max_sync(FULL, xpm);
                 if (cpm >= Mpm) break;                      // dropped, and so are the rest
-                const uint32_t Mser = __reduce_max_sync(FULL, xpm == Mpm ? xser : 0u);
-                const int tl = __ffs(__ballot_sync(FULL, xpm == Mpm && xser == Mser)) - 1;
+                const uint32_t Mser = __reduce_max_sync(FULL, (xs >= 0 && xpm == Mpm) ? xser : 0u);
+                const int tl = __ffs(__ballot_sync(FULL, xs >= 0 && xpm == Mpm && xser == Mser)) - 1;
                 const int ts = __shfl_sync(FULL, xs, tl);
                 if (fslot < 0) write_fork_snapshot(tl, ts);
-                if (lane == tl) {
+                if (BIG) {
+                    if (lane == 0) {
+                        spm[ts] = cpm; sser[ts] = ser0 + (uint32_t)r;
+                        sjsm[ts] = PK::make(jn, (uint32_t)fslot, (uint32_t)(mt ^ m0));
+                    }
+                    __syncwarp();
+                } else if (lane == tl) {
 #pragma unroll
-                    for (int s = 0; s < SLOTS; s++)
+                    for (int s = 0; s < SL; s++)
                         if (s == ts) {
                             s_pm[s] = cpm; s_ser[s] = ser0 + (uint32_t)r;
                             s_jsm[s] = jsm_make(jn, (uint32_t)fslot, (uint32_t)(mt ^ m0));
                         }
                 }
             }
-            if (fslot >= 0 && lane == c1_lane) {
+            if (BIG) {
+                if (fslot >= 0 && lane == 0) sjsm[c1_slot] = PK::make(jn, (uint32_t)fslot, 0);
+                __syncwarp();
+            } else if (fslot >= 0 && lane == c1_lane) {
 #pragma unroll
-                for (int s = 0; s < SLOTS; s++) if (s == c1_slot) s_jsm[s] = jsm_make(jn, (uint32_t)fslot, 0);
+                for (int s = 0; s < SL; s++) if (s == c1_slot) s_jsm[s] = jsm_make(jn, (uint32_t)fslot, 0);
             }
         }
 
@@ -814,6 +981,7 @@ static cudaError_t launch_t(const DecodeParams &p, int ctas, int smem, cudaStrea
 
 template <bool SM, bool CS>
 static cudaError_t launch_s(const DecodeParams &p, int slots, int ctas, int smem, cudaStream_t st) {
+    if (slots == 0) return launch_t<0, SM, CS>(p, ctas, smem, st);
     if (slots == 1) return launch_t<1, SM, CS>(p, ctas, smem, st);
     if (slots == 2) return launch_t<2, SM, CS>(p, ctas, smem, st);
     return launch_t<4, SM, CS>(p, ctas, smem, st);
@@ -850,6 +1018,7 @@ static cudaError_t occ_t(int smem, int *blocks) {
 }
 template <bool B, bool C>
 static cudaError_t occ_s(int slots, int smem, int *blocks) {
+    if (slots == 0) return occ_t<0, B, C>(smem, blocks);
     if (slots == 1) return occ_t<1, B, C>(smem, blocks);
     if (slots == 2) return occ_t<2, B, C>(smem, blocks);
     return occ_t<4, B, C>(smem, blocks);

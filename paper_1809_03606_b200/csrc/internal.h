@@ -19,7 +19,7 @@ __host__ __device__ inline uint32_t op_lam(uint32_t op) { return (op >> 3) & 31u
 __host__ __device__ inline uint32_t op_phi(uint32_t op) { return op >> 8; }
 
 constexpr int kMaxN = 4096;
-constexpr int kMaxD = 128;
+constexpr int kMaxD = 8192;     // D > 128: global-memory stack (the paper's D = NL)
 constexpr int kDecodeWarps = 4;      // warps (frames in flight) per decode CTA
 constexpr int kDecodeMinBlocks = 8;  // launch bound: 32 resident warps/SM => <= 64 registers
 constexpr int kCodecWarps = 4;       // warps per CTA of the generator/encoder kernels
@@ -50,12 +50,16 @@ struct DecodeParams {
     const uint32_t *crc_bytes;  // [nw][4][256] syndrome contribution of each beta byte (CRC codes)
     unsigned long long *queue;
     uint32_t *snap_global;      // arena when snapshots live in global memory
+    uint32_t *stack_global;     // D > 128: per warp [3][D] (PM bits, serial, jsm)
+    uint2 *hdr_global;          // D > 128: per warp [D] fork headers m1..m4
     int N, n, K, c, D, L, M;
     int nw;                     // beta words = max(1, N/32)
     int snap_stride;            // words per snapshot slot = nw (headers m1..m4 in shared memory)
     int sched_words;            // node-table words staged in shared memory (0 = read global)
     int warp_words;             // shared-memory words per warp
     int cnt_words;              // words of the per-length counters (u16 each)
+    int hdr_words;              // shared-memory fork headers: 2 D (register stacks) or 0
+    int used_words;             // snapshot-slot bitmap words: 4, or ceil(D/32) rounded (D > 128)
     int nonsys;                 // 1: read u_hat = x_hat F restricted to A (non-systematic)
 };
 
@@ -102,6 +106,9 @@ struct polar_scs_s {
     polar::CodeTables t;            // device pointers
     unsigned long long *d_queue = nullptr;  // [2] frame-queue counters (slot 0: decode API; 0/1: host pipeline)
     uint32_t *d_snap = nullptr;     // global snapshot arena, 2 slots (or null)
+    uint32_t *d_stack = nullptr;    // global stacks (D > 128), 2 slots
+    uint2 *d_hdr = nullptr;         // global fork headers (D > 128), 2 slots
+    size_t stack_words = 0, hdr_count = 0;   // per slot
     size_t snap_bytes = 0;          // bytes per slot
     int snap_in_smem = 0;
     int chan_in_smem = 0;

@@ -78,7 +78,7 @@ def test_create_rejects_bad_arguments():
         (8192, 64, ok, 8, 4, 0),         # N above the cap
         (128, 65, ok, 8, 4, 0),          # mask weight != N - K
         (128, 64, ok, 0, 4, 0),          # D < 1
-        (128, 64, ok, 129, 4, 0),        # D > 128
+        (128, 64, ok, 8193, 4, 0),       # D > 8192
         (128, 64, ok, 8, 0, 0),          # L < 1
         (128, 64, None, 8, 4, 0),        # NULL mask
         (128, 64, ok, 8, 4, 1),          # degenerate polynomial
