@@ -67,7 +67,8 @@ def dist_env():
 
 
 def workload_name(cfg, c):
-    crc = {0: "no CRC", 0x11021: "CRC-16 0x1021", 0x107: "CRC-8 0x07"}[c["crc_poly"]]
+    crc = {0: "no CRC", 0x11021: "CRC-16 0x1021", 0x107: "CRC-8 0x07",
+           0x1B2B117: "CRC-24C 0xB2B117"}.get(c["crc_poly"], f"CRC poly {c['crc_poly']:#x}")
     if c.get("list"):
         mode = "SCL" if c.get("bit_level") else "FSSCL"
         dl = f"list size L={c['L']}"

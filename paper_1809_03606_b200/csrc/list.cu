@@ -382,21 +382,13 @@ __global__ void __launch_bounds__(LCAP * 32) fsscl_decode_kernel(const ListParam
             __syncthreads();
 
             // ---- prune to the L best keys (reading R22): rank by counting
-            // (each key's count is split over `sub` consecutive lanes of one warp)
             const int total = nL * nc;
-            int sub = 1;
-            while (sub < 32 && total * sub * 2 <= (int)blockDim.x) sub *= 2;
-            {
-                const int ci = tid / sub, part = tid & (sub - 1);
-                unsigned long long key = 0;
+            if (tid < total) {
+                const unsigned long long key = cand_s[tid];
                 int rank = 0;
-                if (ci < total) {
-                    key = cand_s[ci];
-                    #pragma unroll 4
-                    for (int u = part; u < total; u += sub) rank += (cand_s[u] < key) ? 1 : 0;
-                }
-                for (int o = sub >> 1; o >= 1; o >>= 1) rank += __shfl_xor_sync(FULL, rank, o);
-                if (ci < total && part == 0 && rank < L) {
+                #pragma unroll 4
+                for (int u = 0; u < total; u++) rank += (cand_s[u] < key) ? 1 : 0;
+                if (rank < L) {
                     sel_s[rank] = (uint32_t)key;
                     selpm_s[rank] = __uint_as_float((uint32_t)(key >> 32));
                 }
