@@ -42,7 +42,7 @@ int round4(int w) { return (w + 3) & ~3; }
 void free_handle(polar_scs_t h) {
     if (!h) return;
     cudaFree(h->t.nodes); cudaFree(h->t.info); cudaFree(h->t.crc_tab); cudaFree(h->t.crc_bytes); cudaFree(h->t.info_words);
-    cudaFree(h->d_queue); cudaFree(h->d_snap); cudaFree(h->d_stack); cudaFree(h->d_hdr);
+    cudaFree(h->d_queue); cudaFree(h->d_snap); cudaFree(h->d_keys); cudaFree(h->d_jsm); cudaFree(h->d_hdr);
     for (int b = 0; b < 2; b++) {
         cudaFree(h->d_stage_llr[b]); cudaFree(h->d_stage_bits[b]);
         if (h->ev_h2d[b]) cudaEventDestroy(h->ev_h2d[b]);
@@ -79,7 +79,7 @@ int decode_impl(polar_scs_t h, const float *llr, int64_t n, uint8_t *bits, float
     p.pm = pm; p.pops = pops; p.switches = sw; p.status = status;
     p.queue = h->d_queue + slot;
     if (h->d_snap) p.snap_global = h->d_snap + (h->snap_bytes / 4) * (size_t)slot;
-    if (h->d_stack) p.stack_global = h->d_stack + h->stack_words * (size_t)slot;
+    if (h->d_keys) { p.stack_keys = h->d_keys + h->stack_count * (size_t)slot; p.stack_jsm = h->d_jsm + h->stack_count * (size_t)slot; }
     if (h->d_hdr) p.hdr_global = h->d_hdr + h->hdr_count * (size_t)slot;
     cudaError_t e = cudaMemsetAsync(p.queue, 0, sizeof(unsigned long long), st);
     if (e != cudaSuccess) return cuda_status(e);
@@ -230,12 +230,14 @@ int polar_scs_create_ex(polar_scs_t *out, int32_t N, int32_t K, const uint8_t *f
     }
     if (slots == 0) {
         const size_t warps = (size_t)h->ctas * kDecodeWarps;
-        h->stack_words = warps * 3 * (size_t)D;
+        h->stack_count = warps * (size_t)D;
         h->hdr_count = warps * (size_t)D;
-        e = cudaMalloc(&h->d_stack, 2 * h->stack_words * sizeof(uint32_t));
+        e = cudaMalloc(&h->d_keys, 2 * h->stack_count * sizeof(unsigned long long));
+        if (e == cudaSuccess) e = cudaMalloc(&h->d_jsm, 2 * h->stack_count * sizeof(uint32_t));
         if (e == cudaSuccess) e = cudaMalloc(&h->d_hdr, 2 * h->hdr_count * sizeof(uint2));
         if (e != cudaSuccess) { free_handle(h); return cuda_status(e); }
-        p.stack_global = h->d_stack;
+        p.stack_keys = h->d_keys;
+        p.stack_jsm = h->d_jsm;
         p.hdr_global = h->d_hdr;
     }
     // ---- FSSCL launch (polar_scl_decode): one CTA of L warps per frame

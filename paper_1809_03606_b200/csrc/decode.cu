@@ -265,9 +265,10 @@ fsscs_decode_kernel(const DecodeParams P) {
     uint32_t *snap_s = uhat + nw;
     const uint32_t gwarp = (uint32_t)(blockIdx.x * kDecodeWarps + warp);
     const uint32_t snap0 = gwarp * (uint32_t)D;
-    // global stack (BIG): PM bits, serials, jsm words; fork headers per slot
-    uint32_t *spm = BIG ? P.stack_global + (size_t)gwarp * 3 * (size_t)D : nullptr;
-    uint32_t *sser = spm + D, *sjsm = spm + 2 * (size_t)D;
+    // global stack (BIG): keys (PM bits << 32 | serial: u64 order = (PM, serial)
+    // order, reading R7) and jsm words; fork headers per slot
+    unsigned long long *skey = BIG ? P.stack_keys + (size_t)gwarp * (size_t)D : nullptr;
+    uint32_t *sjsm = BIG ? P.stack_jsm + (size_t)gwarp * (size_t)D : nullptr;
     uint2 *ghdr = BIG ? P.hdr_global + (size_t)gwarp * (size_t)D : nullptr;
     auto hdr_at = [&](int k) -> uint2 * { return BIG ? ghdr + k : reinterpret_cast<uint2 *>(shdr) + k; };
     const int sstride = (NL > 0) ? nw : P.snap_stride;
@@ -318,8 +319,9 @@ fsscs_decode_kernel(const DecodeParams P) {
         if (lane == 0) { s_pm[0] = 0u; s_ser[0] = 0u; }
         int nS = 1;
         int uhint = 0;
+        int widx = 0;                     // BIG: index of the working path's entry (-1: not live)
         if (BIG) {
-            if (lane == 0) { spm[0] = 0u; sser[0] = 0u; sjsm[0] = PK::make(0, PK::NONE, 0); }
+            if (lane == 0) { skey[0] = 0ull; sjsm[0] = PK::make(0, PK::NONE, 0); }
             #pragma unroll 1
             for (int w = lane; w < P.used_words; w += 32) snap_used[w] = 0u;
         } else if (lane < 4) {
@@ -351,11 +353,22 @@ fsscs_decode_kernel(const DecodeParams P) {
             uint32_t lpm = EMPTY, lser = EMPTY, ljsm = 0;
             int ls = 0;
             if (BIG) {
+                // 4 independent loads in flight per lane per round
+                unsigned long long lk = ~0ull;
                 #pragma unroll 1
-                for (int i = lane; i < nS; i += 32) {
-                    const uint32_t a = __ldcg(spm + i), b = __ldcg(sser + i);
-                    if (a < lpm || (a == lpm && b < lser)) { lpm = a; lser = b; ls = i; }
+                for (int i0 = 0; i0 < nS; i0 += 128) {
+                    unsigned long long k4[4];
+#pragma unroll
+                    for (int q = 0; q < 4; q++) {
+                        const int i = i0 + 32 * q + lane;
+                        k4[q] = (i < nS) ? __ldcg(skey + i) : ~0ull;
+                    }
+#pragma unroll
+                    for (int q = 0; q < 4; q++)
+                        if (k4[q] < lk) { lk = k4[q]; ls = i0 + 32 * q + lane; }
                 }
+                lpm = (uint32_t)(lk >> 32);
+                lser = (uint32_t)lk;
             } else {
 #pragma unroll
                 for (int s = 0; s < SL; s++)
@@ -369,10 +382,10 @@ fsscs_decode_kernel(const DecodeParams P) {
                 // remove entry `pi`: the last entry moves into its place
                 const int pi = __shfl_sync(FULL, ls, owner);
                 p_jsm = __ldcg(sjsm + pi);
-                if (lane == 0 && pi != nS - 1) {
-                    spm[pi] = __ldcg(spm + nS - 1); sser[pi] = __ldcg(sser + nS - 1); sjsm[pi] = __ldcg(sjsm + nS - 1);
-                }
+                if (lane == 0 && pi != nS - 1) { skey[pi] = __ldcg(skey + nS - 1); sjsm[pi] = __ldcg(sjsm + nS - 1); }
                 __syncwarp();
+                if (widx == pi) widx = -1;
+                else if (widx == nS - 1) widx = pi;
             } else {
                 p_jsm = __shfl_sync(FULL, ljsm, owner);
                 if (lane == owner) {
@@ -394,20 +407,23 @@ fsscs_decode_kernel(const DecodeParams P) {
                 int cntv = 0;
                 if (BIG) {
                     // in-place compaction of the entries with depth > j
+                    int nwidx = -1;
                     #pragma unroll 1
                     for (int i0 = 0; i0 < nS; i0 += 32) {
                         const int i = i0 + lane;
-                        uint32_t a = 0, b = 0, x = 0;
-                        if (i < nS) { a = __ldcg(spm + i); b = __ldcg(sser + i); x = __ldcg(sjsm + i); }
+                        unsigned long long a = 0;
+                        uint32_t x = 0;
+                        if (i < nS) { a = __ldcg(skey + i); x = __ldcg(sjsm + i); }
                         const bool keep = (i < nS) && (int)PK::j(x) > j;
                         const uint32_t kb = __ballot_sync(FULL, keep);
+                        const int o = cntv + __popc(kb & ((1u << lane) - 1u));
+                        const uint32_t wbb = __ballot_sync(FULL, keep && i == widx);
+                        if (wbb) nwidx = cntv + __popc(kb & ((1u << (__ffs(wbb) - 1)) - 1u));
                         __syncwarp();
-                        if (keep) {
-                            const int o = cntv + __popc(kb & ((1u << lane) - 1u));
-                            spm[o] = a; sser[o] = b; sjsm[o] = x;
-                        }
+                        if (keep) { skey[o] = a; sjsm[o] = x; }
                         cntv += __popc(kb);
                     }
+                    widx = nwidx;
                     __syncwarp();
                 } else {
 #pragma unroll
@@ -433,13 +449,7 @@ fsscs_decode_kernel(const DecodeParams P) {
                 switches++;
                 // the path being left keeps its beta in a snapshot if it is still live
                 if (BIG) {
-                    int wi = -1;
-                    #pragma unroll 1
-                    for (int i0 = 0; i0 < nS && wi < 0; i0 += 32) {
-                        const int i = i0 + lane;
-                        const uint32_t hb = __ballot_sync(FULL, i < nS && __ldcg(sser + i) == work);
-                        if (hb) wi = i0 + __ffs(hb) - 1;
-                    }
+                    const int wi = widx;
                     if (wi >= 0) {
                         const uint32_t wj = __ldcg(sjsm + wi);
                         if (PK::snap(wj) == PK::NONE) {
@@ -525,6 +535,7 @@ fsscs_decode_kernel(const DecodeParams P) {
                     __syncwarp();
                 }
                 work = p_ser;
+                widx = -1;                      // the new working path is not on the stack
             }
             work_pl = pl;
 
@@ -858,11 +869,11 @@ fsscs_decode_kernel(const DecodeParams P) {
                 const uint32_t jbase = PK::make(jn, (nfit == 1) ? PK::NONE : (uint32_t)fslot, 0);
                 if (lane < nfit) {
                     const uint32_t mk = (clist >> (4 * lane)) & 15u;
-                    spm[nS + lane] = __float_as_uint(p_pm + my_d);
-                    sser[nS + lane] = ser0 + (uint32_t)lane;
+                    skey[nS + lane] = ((unsigned long long)__float_as_uint(p_pm + my_d) << 32) | (ser0 + (uint32_t)lane);
                     sjsm[nS + lane] = jbase | ((mk ^ (uint32_t)m0) << PK::MSH);
                 }
                 c1_slot = nS;
+                widx = nS;
                 __syncwarp();
                 nS += nfit;
             } else {
@@ -900,11 +911,14 @@ fsscs_decode_kernel(const DecodeParams P) {
                 uint32_t xpm = 0, xser = 0;
                 int xs = -1;
                 if (BIG) {
+                    unsigned long long xk = 0;
                     #pragma unroll 1
                     for (int i = lane; i < nS; i += 32) {
-                        const uint32_t a = __ldcg(spm + i), b = __ldcg(sser + i);
-                        if (xs < 0 || a > xpm || (a == xpm && b > xser)) { xpm = a; xser = b; xs = i; }
+                        const unsigned long long k = __ldcg(skey + i);
+                        if (xs < 0 || k > xk) { xk = k; xs = i; }
                     }
+                    xpm = (uint32_t)(xk >> 32);
+                    xser = (uint32_t)xk;
                 } else {
 #pragma unroll
                     for (int s = 0; s < SL; s++)
@@ -918,7 +932,7 @@ fsscs_decode_kernel(const DecodeParams P) {
                 if (fslot < 0) write_fork_snapshot(tl, ts);
                 if (BIG) {
                     if (lane == 0) {
-                        spm[ts] = cpm; sser[ts] = ser0 + (uint32_t)r;
+                        skey[ts] = ((unsigned long long)cpm << 32) | (ser0 + (uint32_t)r);
                         sjsm[ts] = PK::make(jn, (uint32_t)fslot, (uint32_t)(mt ^ m0));
                     }
                     __syncwarp();

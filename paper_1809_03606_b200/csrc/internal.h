@@ -50,7 +50,8 @@ struct DecodeParams {
     const uint32_t *crc_bytes;  // [nw][4][256] syndrome contribution of each beta byte (CRC codes)
     unsigned long long *queue;
     uint32_t *snap_global;      // arena when snapshots live in global memory
-    uint32_t *stack_global;     // D > 128: per warp [3][D] (PM bits, serial, jsm)
+    unsigned long long *stack_keys;   // D > 128: per warp [D] (PM bits << 32 | serial)
+    uint32_t *stack_jsm;        // D > 128: per warp [D] (depth | snapshot | flips)
     uint2 *hdr_global;          // D > 128: per warp [D] fork headers m1..m4
     int N, n, K, c, D, L, M;
     int nw;                     // beta words = max(1, N/32)
@@ -106,9 +107,10 @@ struct polar_scs_s {
     polar::CodeTables t;            // device pointers
     unsigned long long *d_queue = nullptr;  // [2] frame-queue counters (slot 0: decode API; 0/1: host pipeline)
     uint32_t *d_snap = nullptr;     // global snapshot arena, 2 slots (or null)
-    uint32_t *d_stack = nullptr;    // global stacks (D > 128), 2 slots
+    unsigned long long *d_keys = nullptr;   // global stacks (D > 128), 2 slots
+    uint32_t *d_jsm = nullptr;
     uint2 *d_hdr = nullptr;         // global fork headers (D > 128), 2 slots
-    size_t stack_words = 0, hdr_count = 0;   // per slot
+    size_t stack_count = 0, hdr_count = 0;   // entries per slot
     size_t snap_bytes = 0;          // bytes per slot
     int snap_in_smem = 0;
     int chan_in_smem = 0;
