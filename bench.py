@@ -400,7 +400,8 @@ def run_ours(args, cfg, c):
 def oracle_ops_per_frame(c, npts, n_sample=64):
     """Algorithmic lane-ops per frame (mean over a sample at every Eb/N0 point):
     f/g evaluations (clean pass + spines) + node elements + BETA XOR bits +
-    stack key compares (D per pop and per candidate insert); for the list
+    stack key compares (the live entries examined by each linear search for
+    the best entry, and for the worst one, L599); for the list
     decoder the last term is the prune's sort cost (T log2 T per node)."""
     import oracle as O
     fr = O.bhattacharyya_mask(c["N"], c["K"], c["design_db"])
@@ -414,7 +415,7 @@ def oracle_ops_per_frame(c, npts, n_sample=64):
         r = dec.decode(O.awgn_llr(cw, nz, eb, c["K"] / c["N"]), counters=True, threads=os.cpu_count() or 1)
         ct = r["counters"]
         tot += (ct["f_ops"] + ct["g_ops"] + ct["node_elems"] + ct["beta_xor_bits"]
-                + (ct["sel_compares"] if c.get("list") else c["D"] * (ct["pops"] + ct["cand_created"])))
+                + (ct["sel_compares"] if c.get("list") else ct["key_compares"]))
     return tot / (n_sample * npts)
 
 

@@ -494,6 +494,7 @@ static int decode_one(const orc_scs_t *h, const float *chan, uint8_t *block, uin
         /* select: linear search for the winning (PM, serial) */
         int w = 0;
         for (int e = 1; e < nS; e++) if (key_less(&S[e], &S[w])) w = e;
+        if (ct) ct->key_compares += (uint64_t)nS;
         entry_t p = S[w];
         S[w] = S[nS - 1];           /* remove it; its beta buffer moves to the tail */
         S[nS - 1] = p;
@@ -600,6 +601,7 @@ static int decode_one(const orc_scs_t *h, const float *chan, uint8_t *block, uin
                 /* full stack: replace the least reliable iff strictly better */
                 int worst = 0;
                 for (int e = 1; e < nS; e++) if (key_less(&S[worst], &S[e])) worst = e;
+                if (ct) ct->key_compares += (uint64_t)nS;
                 if (cpm < S[worst].pm) { dst = &S[worst]; if (ct) ct->cand_replaced++; }
                 else if (ct) ct->cand_dropped++;
             }

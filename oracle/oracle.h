@@ -89,7 +89,9 @@ typedef struct {
     uint64_t pruned;                /* entries removed by the per-length rule */
     uint64_t crc_checks;
     uint64_t sel_compares;
-    uint64_t stack_peak;            /* stack decoder: max live entries seen (a max, not a sum) */          /* list decoder: prune cost, sum over nodes of T ceil(log2 T), T = candidates */
+    uint64_t stack_peak;            /* stack decoder: max live entries seen (a max, not a sum) */
+    uint64_t key_compares;          /* stack decoder: entries examined by the linear searches
+                                       (selection, L793, and worst-entry search, L599) */          /* list decoder: prune cost, sum over nodes of T ceil(log2 T), T = candidates */
 } orc_counters_t;
 
 orc_scs_t *orc_scs_create(int N, const uint8_t *frozen, int D, int L, uint32_t crc_poly, int bit_level);
