@@ -177,15 +177,12 @@ __device__ __forceinline__ int alloc_snapshot_lazy(uint32_t *used, const uint32_
     return slot;
 }
 
-// Hybrid stack (D > 128): the same conservative bitmap over D slots, in
+// Global stack (D > 128): the same conservative bitmap over D slots, in
 // shared memory (UW = ceil(D/32) words), searched from a hint word (every word
-// below it is full); the exact recount marks the snapshots of the live hot
-// (register) entries, except (skip_lane, skip_slot), and of the cold (global)
-// entries, plus `extra`.
-template <int SL>
-__device__ __forceinline__ int alloc_snapshot_hyb(uint32_t *used, int &uhint, const uint32_t (&s_ser)[SL],
-                                                  const uint32_t (&s_jsm)[SL], int skip_lane, int skip_slot,
-                                                  const uint32_t *cjsm, int nC, int D, uint32_t extra, int lane) {
+// below it is full); the exact recount scans the live entries of the global
+// stack (all but entry `skip`) and marks `extra`.
+__device__ __forceinline__ int alloc_snapshot_big(uint32_t *used, int &uhint, const uint32_t *sjsm, int nS, int D,
+                                                  int skip, uint32_t extra, int lane) {
     const int UW = (D + 31) >> 5;
     int slot = -1;
     #pragma unroll 1
@@ -194,16 +191,10 @@ __device__ __forceinline__ int alloc_snapshot_hyb(uint32_t *used, int &uhint, co
             #pragma unroll 1
             for (int w = lane; w < UW; w += 32) used[w] = 0u;
             __syncwarp();
-#pragma unroll
-            for (int s = 0; s < SL; s++) {
-                const uint32_t sn = Pk<true>::snap(s_jsm[s]);
-                if (s_ser[s] != 0xFFFFFFFFu && !(lane == skip_lane && s == skip_slot) && sn != Pk<true>::NONE)
-                    atomicOr(used + (sn >> 5), 1u << (sn & 31));
-            }
             #pragma unroll 1
-            for (int i = lane; i < nC; i += 32) {
-                const uint32_t sn = Pk<true>::snap(__ldcg(cjsm + i));
-                if (sn != Pk<true>::NONE) atomicOr(used + (sn >> 5), 1u << (sn & 31));
+            for (int i = lane; i < nS; i += 32) {
+                const uint32_t sn = Pk<true>::snap(sjsm[i]);
+                if (i != skip && sn != Pk<true>::NONE) atomicOr(used + (sn >> 5), 1u << (sn & 31));
             }
             __syncwarp();
             if (lane == 0 && extra != Pk<true>::NONE) used[extra >> 5] |= 1u << (extra & 31);
@@ -236,18 +227,13 @@ __device__ __forceinline__ int alloc_snapshot_hyb(uint32_t *used, int &uhint, co
 }
 
 // SLOTS = 1, 2, 4: register stack of 32 SLOTS entries (D <= 128).  SLOTS = 0:
-// hybrid stack for D up to 8192 (the paper's D = NL): a hot set of 128 entries
-// in registers (as SLOTS = 4) and a cold overflow of dense unsorted arrays in
-// global memory (L2-resident in practice), with the invariant that every cold
-// key (PM, serial) is larger than every hot key.  Selection therefore only
-// looks at the hot set; the cold set is touched by appends, evictions of the
-// hot maximum, the per-length prune and refills of an empty hot set.
+// global stack (D up to 8192, the paper's D = NL): dense unsorted arrays per
+// warp in global memory (L2-resident in practice), scanned by the 32 lanes.
 template <int SLOTS, bool SNAP_SMEM, bool CHAN_SMEM, int NL = 0>
-__global__ void __launch_bounds__(kDecodeWarps * 32, (SLOTS == 4 || SLOTS == 0) ? 3 : (SLOTS == 2 ? 5 : kDecodeMinBlocks))
+__global__ void __launch_bounds__(kDecodeWarps * 32, SLOTS == 4 ? 3 : (SLOTS == 2 ? 5 : kDecodeMinBlocks))
 fsscs_decode_kernel(const DecodeParams P) {
     constexpr bool BIG = (SLOTS == 0);
-    constexpr int SL = BIG ? 4 : SLOTS;       // register entries per lane (BIG: the hot set)
-    constexpr int HOT = 32 * SL;
+    constexpr int SL = BIG ? 1 : SLOTS;       // register arrays (unused when BIG)
     using PK = Pk<BIG>;
     extern __shared__ __align__(16) uint32_t smem[];
     const int lane = threadIdx.x & 31;
@@ -331,11 +317,11 @@ fsscs_decode_kernel(const DecodeParams P) {
 #pragma unroll
         for (int s = 0; s < SL; s++) { s_pm[s] = EMPTY; s_ser[s] = EMPTY; s_jsm[s] = PK::make(0, PK::NONE, 0); }
         if (lane == 0) { s_pm[0] = 0u; s_ser[0] = 0u; }
-        int nS = 1;                       // live entries (BIG: hot + cold)
+        int nS = 1;
         int uhint = 0;
-        int nC = 0;                       // BIG: cold entries
-        unsigned long long cmin = ~0ull;  // BIG: smallest cold key (~0: none)
+        int widx = 0;                     // BIG: index of the working path's entry (-1: not live)
         if (BIG) {
+            if (lane == 0) { skey[0] = 0ull; sjsm[0] = PK::make(0, PK::NONE, 0); }
             #pragma unroll 1
             for (int w = lane; w < P.used_words; w += 32) snap_used[w] = 0u;
         } else if (lane < 4) {
@@ -364,62 +350,54 @@ fsscs_decode_kernel(const DecodeParams P) {
                 break;
             }
             // ---- select: min (PM, serial) (reading R7)
-            if (BIG && nS == nC) {
-                // refill the empty hot set from the cold set: T = the smallest of the
-                // lanes' 4th-smallest cold keys; the keys <= T are a prefix of the cold
-                // order, at most 4 per lane (each lane takes its own, i = lane mod 32)
-                unsigned long long t0 = ~0ull, t1 = ~0ull, t2 = ~0ull, t3 = ~0ull;
-                #pragma unroll 1
-                for (int i = lane; i < nC; i += 32) top4_insert(__ldcg(skey + i), t0, t1, t2, t3);
-                uint32_t th, tl_;
-                warp_min_key((uint32_t)(t3 >> 32), (uint32_t)t3, th, tl_);
-                const unsigned long long T = ((unsigned long long)th << 32) | tl_;
-                int kept = 0, hs = 0;
-                unsigned long long nmin = ~0ull;
-                #pragma unroll 1
-                for (int i0 = 0; i0 < nC; i0 += 32) {
-                    const int i = i0 + lane;
-                    unsigned long long k = ~0ull;
-                    uint32_t x = 0;
-                    if (i < nC) { k = __ldcg(skey + i); x = __ldcg(sjsm + i); }
-                    const bool mv = (i < nC) && k <= T;
-                    const bool keep = (i < nC) && !mv;
-                    const uint32_t kb = __ballot_sync(FULL, keep);
-                    const int o = kept + __popc(kb & ((1u << lane) - 1u));
-                    __syncwarp();
-                    if (keep) { skey[o] = k; sjsm[o] = x; if (k < nmin) nmin = k; }
-                    if (mv) {
-#pragma unroll
-                        for (int s = 0; s < SL; s++)
-                            if (s == hs) { s_pm[s] = (uint32_t)(k >> 32); s_ser[s] = (uint32_t)k; s_jsm[s] = x; }
-                        hs++;
-                    }
-                    kept += __popc(kb);
-                }
-                __syncwarp();
-                nC = kept;
-                uint32_t mh, ml;
-                warp_min_key((uint32_t)(nmin >> 32), (uint32_t)nmin, mh, ml);
-                cmin = ((unsigned long long)mh << 32) | ml;
-            }
             uint32_t lpm = EMPTY, lser = EMPTY, ljsm = 0;
             int ls = 0;
+            if (BIG) {
+                // 4 independent loads in flight per lane per round
+                unsigned long long lk = ~0ull;
+                #pragma unroll 1
+                for (int i0 = 0; i0 < nS; i0 += 128) {
+                    unsigned long long k4[4];
 #pragma unroll
-            for (int s = 0; s < SL; s++)
-                if (s_pm[s] < lpm || (s_pm[s] == lpm && s_ser[s] < lser)) { lpm = s_pm[s]; lser = s_ser[s]; ljsm = s_jsm[s]; ls = s; }
+                    for (int q = 0; q < 4; q++) {
+                        const int i = i0 + 32 * q + lane;
+                        k4[q] = (i < nS) ? __ldcg(skey + i) : ~0ull;
+                    }
+#pragma unroll
+                    for (int q = 0; q < 4; q++)
+                        if (k4[q] < lk) { lk = k4[q]; ls = i0 + 32 * q + lane; }
+                }
+                lpm = (uint32_t)(lk >> 32);
+                lser = (uint32_t)lk;
+            } else {
+#pragma unroll
+                for (int s = 0; s < SL; s++)
+                    if (s_pm[s] < lpm || (s_pm[s] == lpm && s_ser[s] < lser)) { lpm = s_pm[s]; lser = s_ser[s]; ljsm = s_jsm[s]; ls = s; }
+            }
             uint32_t mpm, mser;
             warp_min_key(lpm, lser, mpm, mser);
             const int owner = __ffs(__ballot_sync(FULL, lpm == mpm && lser == mser)) - 1;
-            const uint32_t p_jsm = __shfl_sync(FULL, ljsm, owner);
-            if (lane == owner) {
+            uint32_t p_jsm;
+            if (BIG) {
+                // remove entry `pi`: the last entry moves into its place
+                const int pi = __shfl_sync(FULL, ls, owner);
+                p_jsm = __ldcg(sjsm + pi);
+                if (lane == 0 && pi != nS - 1) { skey[pi] = __ldcg(skey + nS - 1); sjsm[pi] = __ldcg(sjsm + nS - 1); }
+                __syncwarp();
+                if (widx == pi) widx = -1;
+                else if (widx == nS - 1) widx = pi;
+            } else {
+                p_jsm = __shfl_sync(FULL, ljsm, owner);
+                if (lane == owner) {
 #pragma unroll
-                for (int s = 0; s < SL; s++) if (s == ls) { s_pm[s] = EMPTY; s_ser[s] = EMPTY; }
+                    for (int s = 0; s < SL; s++) if (s == ls) { s_pm[s] = EMPTY; s_ser[s] = EMPTY; }
+                }
             }
             nS--;
             pops++;
             const float p_pm = __uint_as_float(mpm);
             const uint32_t p_ser = mser;
-            const int j = (int)PK::j(p_jsm);
+            const int j = (int)jsm_j(p_jsm);
 
             // ---- per-length counter and prune (readings R9, R10)
             const int c_j = (int)cnt[j] + 1;
@@ -427,35 +405,34 @@ fsscs_decode_kernel(const DecodeParams P) {
             if (lane == 0) cnt[j] = (uint16_t)c_j;
             if (c_j == P.L) {
                 int cntv = 0;
-#pragma unroll
-                for (int s = 0; s < SL; s++) {
-                    if (s_ser[s] != EMPTY && (int)PK::j(s_jsm[s]) <= j) { s_pm[s] = EMPTY; s_ser[s] = EMPTY; }
-                    cntv += __popc(__ballot_sync(FULL, s_ser[s] != EMPTY));
-                }
-                if (BIG && nC > 0) {
-                    // cold set: in-place compaction of the entries with depth > j
-                    int kept = 0;
-                    unsigned long long nmin = ~0ull;
+                if (BIG) {
+                    // in-place compaction of the entries with depth > j
+                    int nwidx = -1;
                     #pragma unroll 1
-                    for (int i0 = 0; i0 < nC; i0 += 32) {
+                    for (int i0 = 0; i0 < nS; i0 += 32) {
                         const int i = i0 + lane;
                         unsigned long long a = 0;
                         uint32_t x = 0;
-                        if (i < nC) { a = __ldcg(skey + i); x = __ldcg(sjsm + i); }
-                        const bool keep = (i < nC) && (int)PK::j(x) > j;
+                        if (i < nS) { a = __ldcg(skey + i); x = __ldcg(sjsm + i); }
+                        const bool keep = (i < nS) && (int)PK::j(x) > j;
                         const uint32_t kb = __ballot_sync(FULL, keep);
-                        const int o = kept + __popc(kb & ((1u << lane) - 1u));
+                        const int o = cntv + __popc(kb & ((1u << lane) - 1u));
+                        const uint32_t wbb = __ballot_sync(FULL, keep && i == widx);
+                        if (wbb) nwidx = cntv + __popc(kb & ((1u << (__ffs(wbb) - 1)) - 1u));
                         __syncwarp();
-                        if (keep) { skey[o] = a; sjsm[o] = x; if (a < nmin) nmin = a; }
-                        kept += __popc(kb);
+                        if (keep) { skey[o] = a; sjsm[o] = x; }
+                        cntv += __popc(kb);
                     }
+                    widx = nwidx;
                     __syncwarp();
-                    nC = kept;
-                    uint32_t mh, ml;
-                    warp_min_key((uint32_t)(nmin >> 32), (uint32_t)nmin, mh, ml);
-                    cmin = ((unsigned long long)mh << 32) | ml;
+                } else {
+#pragma unroll
+                    for (int s = 0; s < SL; s++) {
+                        if (s_ser[s] != EMPTY && (int)jsm_j(s_jsm[s]) <= j) { s_pm[s] = EMPTY; s_ser[s] = EMPTY; }
+                        cntv += __popc(__ballot_sync(FULL, s_ser[s] != EMPTY));
+                    }
                 }
-                nS = cntv + (BIG ? nC : 0);
+                nS = cntv;
             }
 
             // position after the node that created p (its path length)
@@ -471,24 +448,12 @@ fsscs_decode_kernel(const DecodeParams P) {
             if (p_ser != work) {
                 switches++;
                 // the path being left keeps its beta in a snapshot if it is still live
-                int wsl = -1;
-#pragma unroll
-                for (int s = 0; s < SL; s++) if (s_ser[s] == work) wsl = s;
-                const uint32_t wb_ = __ballot_sync(FULL, wsl >= 0);
-                if (BIG && !wb_ && nC > 0) {
-                    // the working path's entry may be cold
-                    int wi = -1;
-                    #pragma unroll 1
-                    for (int i0 = 0; i0 < nC && wi < 0; i0 += 32) {
-                        const int i = i0 + lane;
-                        const uint32_t hb = __ballot_sync(FULL, i < nC && (uint32_t)__ldcg(skey + i) == work);
-                        if (hb) wi = i0 + __ffs(hb) - 1;
-                    }
+                if (BIG) {
+                    const int wi = widx;
                     if (wi >= 0) {
                         const uint32_t wj = __ldcg(sjsm + wi);
                         if (PK::snap(wj) == PK::NONE) {
-                            const int slot = alloc_snapshot_hyb<SL>(snap_used, uhint, s_ser, s_jsm, -1, 0, sjsm, nC, D,
-                                                                    PK::snap(p_jsm), lane);
+                            const int slot = alloc_snapshot_big(snap_used, uhint, sjsm, nS, D, -1, PK::snap(p_jsm), lane);
                             uint32_t *dst = snap_slot(slot);
                             const int nwords = (work_pl + 31) >> 5;
                             #pragma unroll 1
@@ -498,17 +463,19 @@ fsscs_decode_kernel(const DecodeParams P) {
                         }
                     }
                 }
-                if (wb_) {
+                int wsl = -1;
+#pragma unroll
+                for (int s = 0; s < SL; s++) if (!BIG && s_ser[s] == work) wsl = s;
+                const uint32_t wb_ = __ballot_sync(FULL, wsl >= 0);
+                if (!BIG && wb_) {
                     const int wl = __ffs(wb_) - 1;
                     uint32_t wj = 0;
 #pragma unroll
                     for (int s = 0; s < SL; s++) if (s == wsl) wj = s_jsm[s];
                     wj = __shfl_sync(FULL, wj, wl);
                     const int wslot = __shfl_sync(FULL, wsl, wl);
-                    if (PK::snap(wj) == PK::NONE) {
-                        int slot;
-                        if (BIG) slot = alloc_snapshot_hyb<SL>(snap_used, uhint, s_ser, s_jsm, -1, 0, sjsm, nC, D, PK::snap(p_jsm), lane);
-                        else slot = alloc_snapshot_lazy<SL>(snap_used, s_ser, s_jsm, D, -1, 0, PK::snap(p_jsm), lane);
+                    if (jsm_snap(wj) == SNAP_NONE) {
+                        const int slot = alloc_snapshot_lazy<SL>(snap_used, s_ser, s_jsm, D, -1, 0, jsm_snap(p_jsm), lane);
                         uint32_t *dst = snap_slot(slot);
                         const int nwords = (work_pl + 31) >> 5;
                         #pragma unroll 1
@@ -516,7 +483,7 @@ fsscs_decode_kernel(const DecodeParams P) {
                         if (lane == wl) {
 #pragma unroll
                             for (int s = 0; s < SL; s++)
-                                if (s == wslot) s_jsm[s] = PK::make(PK::j(wj), (uint32_t)slot, 0);
+                                if (s == wslot) s_jsm[s] = jsm_make(jsm_j(wj), (uint32_t)slot, 0);
                         }
                     }
                 }
@@ -568,6 +535,7 @@ fsscs_decode_kernel(const DecodeParams P) {
                     __syncwarp();
                 }
                 work = p_ser;
+                widx = -1;                      // the new working path is not on the stack
             }
             work_pl = pl;
 
@@ -887,72 +855,31 @@ fsscs_decode_kernel(const DecodeParams P) {
             int fslot = -1;
             const int nfit = min(nc, D - nS);
             auto write_fork_snapshot = [&](int victim_lane, int victim_slot) {
-                if (BIG) fslot = alloc_snapshot_hyb<SL>(snap_used, uhint, s_ser, s_jsm, victim_lane, victim_slot, sjsm, nC, D,
-                                                        PK::NONE, lane);
-                else fslot = alloc_snapshot_lazy<SL>(snap_used, s_ser, s_jsm, D, victim_lane, victim_slot, PK::NONE, lane);
+                if (BIG) fslot = alloc_snapshot_big(snap_used, uhint, sjsm, nS, D, victim_slot, PK::NONE, lane);
+                else fslot = alloc_snapshot_lazy<SL>(snap_used, s_ser, s_jsm, D, victim_lane, victim_slot, SNAP_NONE, lane);
                 uint32_t *dst = snap_slot(fslot);
                 const int nwords = (npl + 31) >> 5;
                 #pragma unroll 1
                 for (int w = lane; w < nwords; w += 32) dst[w] = beta[w];
                 if (lane == 0) *hdr_at(fslot) = make_uint2(mi[0] | (mi[1] << 16), mi[2] | (mi[3] << 16));
             };
-            // hybrid stack: one entry into the hot set (evicting the hot maximum to
-            // the cold set when full) or, if it is larger than a cold key, the cold set
-            auto hyb_insert = [&](unsigned long long key, uint32_t x) {
-                if (nC > 0 && key > cmin) {
-                    if (lane == 0) { skey[nC] = key; sjsm[nC] = x; }
-                    __syncwarp();
-                    nC++;
-                } else {
-                    if (nS - nC == HOT) {
-                        uint32_t xpm = 0, xser = 0, xj = 0;
-                        int xs = -1;
-#pragma unroll
-                        for (int s = 0; s < SL; s++)
-                            if (s_ser[s] != EMPTY && (xs < 0 || s_pm[s] > xpm || (s_pm[s] == xpm && s_ser[s] > xser))) {
-                                xpm = s_pm[s]; xser = s_ser[s]; xj = s_jsm[s]; xs = s;
-                            }
-                        const uint32_t Mpm = __reduce_max_sync(FULL, xpm);
-                        const uint32_t Mser = __reduce_max_sync(FULL, (xs >= 0 && xpm == Mpm) ? xser : 0u);
-                        const int tl = __ffs(__ballot_sync(FULL, xs >= 0 && xpm == Mpm && xser == Mser)) - 1;
-                        if (lane == tl) {
-                            skey[nC] = ((unsigned long long)Mpm << 32) | Mser;
-                            sjsm[nC] = xj;
-#pragma unroll
-                            for (int s = 0; s < SL; s++) if (s == xs) { s_pm[s] = EMPTY; s_ser[s] = EMPTY; }
-                        }
-                        __syncwarp();
-                        nC++;
-                        cmin = ((unsigned long long)Mpm << 32) | Mser;
-                    }
-                    bool done = false;
-#pragma unroll
-                    for (int s = 0; s < SL; s++) {
-                        const uint32_t fb = __ballot_sync(FULL, s_ser[s] == EMPTY);
-                        if (!done && fb) {
-                            done = true;
-                            if (lane == __ffs(fb) - 1) { s_pm[s] = (uint32_t)(key >> 32); s_ser[s] = (uint32_t)key; s_jsm[s] = x; }
-                        }
-                    }
-                }
-                nS++;
-            };
-            // BIG: the fork snapshot is written whenever the node has siblings, so
-            // c1's entry never needs a late fix-up (it may move between the sets)
-            if (BIG ? (nc > 1) : (nfit > 1)) write_fork_snapshot(-1, -1);
+            if (nfit > 1) write_fork_snapshot(-1, -1);
             int c1_lane = 0, c1_slot = 0;
-            const uint32_t jbase = PK::make(jn, (fslot < 0) ? PK::NONE : (uint32_t)fslot, 0);
-            if (BIG && !(nC == 0 && nS + nfit <= HOT)) {
-                #pragma unroll 1
-                for (int k = 0; k < nfit; k++) {
-                    const float dk = __shfl_sync(FULL, my_d, k);
-                    const uint32_t mk = (clist >> (4 * k)) & 15u;
-                    hyb_insert(((unsigned long long)__float_as_uint(p_pm + dk) << 32) | (ser0 + (uint32_t)k),
-                               jbase | ((mk ^ (uint32_t)m0) << PK::MSH));
+            if (BIG) {
+                const uint32_t jbase = PK::make(jn, (nfit == 1) ? PK::NONE : (uint32_t)fslot, 0);
+                if (lane < nfit) {
+                    const uint32_t mk = (clist >> (4 * lane)) & 15u;
+                    skey[nS + lane] = ((unsigned long long)__float_as_uint(p_pm + my_d) << 32) | (ser0 + (uint32_t)lane);
+                    sjsm[nS + lane] = jbase | ((mk ^ (uint32_t)m0) << PK::MSH);
                 }
+                c1_slot = nS;
+                widx = nS;
+                __syncwarp();
+                nS += nfit;
             } else {
                 int base = 0;
                 bool c1_found = false;
+                const uint32_t jbase = jsm_make(jn, (nfit == 1) ? SNAP_NONE : (uint32_t)fslot, 0);
 #pragma unroll
                 for (int s = 0; s < SL; s++) {
                     const bool fr = (s_ser[s] == EMPTY);
@@ -963,7 +890,7 @@ fsscs_decode_kernel(const DecodeParams P) {
                         const uint32_t mk = (clist >> (4 * k)) & 15u;
                         s_pm[s] = __float_as_uint(p_pm + dk);
                         s_ser[s] = ser0 + (uint32_t)k;
-                        s_jsm[s] = jbase | ((mk ^ (uint32_t)m0) << PK::MSH);
+                        s_jsm[s] = jbase | ((mk ^ (uint32_t)m0) << 21);
                     }
                     const uint32_t b0 = __ballot_sync(FULL, fr && k == 0);
                     if (!c1_found && b0) { c1_found = true; c1_lane = __ffs(b0) - 1; c1_slot = s; }
@@ -983,11 +910,10 @@ fsscs_decode_kernel(const DecodeParams P) {
                 const uint32_t cpm = __float_as_uint(p_pm + dt);
                 uint32_t xpm = 0, xser = 0;
                 int xs = -1;
-                if (BIG && nC > 0) {
-                    // the worst entry is cold
+                if (BIG) {
                     unsigned long long xk = 0;
                     #pragma unroll 1
-                    for (int i = lane; i < nC; i += 32) {
+                    for (int i = lane; i < nS; i += 32) {
                         const unsigned long long k = __ldcg(skey + i);
                         if (xs < 0 || k > xk) { xk = k; xs = i; }
                     }
@@ -1003,35 +929,28 @@ fsscs_decode_kernel(const DecodeParams P) {
                 const uint32_t Mser = __reduce_max_sync(FULL, (xs >= 0 && xpm == Mpm) ? xser : 0u);
                 const int tl = __ffs(__ballot_sync(FULL, xs >= 0 && xpm == Mpm && xser == Mser)) - 1;
                 const int ts = __shfl_sync(FULL, xs, tl);
-                if (BIG) {
-                    // remove the worst entry, then insert by the hybrid rule
-                    if (nC > 0) {
-                        if (lane == 0 && ts != nC - 1) { skey[ts] = __ldcg(skey + nC - 1); sjsm[ts] = __ldcg(sjsm + nC - 1); }
-                        __syncwarp();
-                        nC--;
-                        if (nC == 0) cmin = ~0ull;
-                    } else if (lane == tl) {
-#pragma unroll
-                        for (int s = 0; s < SL; s++) if (s == ts) { s_pm[s] = EMPTY; s_ser[s] = EMPTY; }
-                    }
-                    nS--;
-                    hyb_insert(((unsigned long long)cpm << 32) | (ser0 + (uint32_t)r),
-                               PK::make(jn, (uint32_t)fslot, (uint32_t)(mt ^ m0)));
-                    continue;
-                }
                 if (fslot < 0) write_fork_snapshot(tl, ts);
-                if (lane == tl) {
+                if (BIG) {
+                    if (lane == 0) {
+                        skey[ts] = ((unsigned long long)cpm << 32) | (ser0 + (uint32_t)r);
+                        sjsm[ts] = PK::make(jn, (uint32_t)fslot, (uint32_t)(mt ^ m0));
+                    }
+                    __syncwarp();
+                } else if (lane == tl) {
 #pragma unroll
                     for (int s = 0; s < SL; s++)
                         if (s == ts) {
                             s_pm[s] = cpm; s_ser[s] = ser0 + (uint32_t)r;
-                            s_jsm[s] = PK::make(jn, (uint32_t)fslot, (uint32_t)(mt ^ m0));
+                            s_jsm[s] = jsm_make(jn, (uint32_t)fslot, (uint32_t)(mt ^ m0));
                         }
                 }
             }
-            if (!BIG && fslot >= 0 && lane == c1_lane) {
+            if (BIG) {
+                if (fslot >= 0 && lane == 0) sjsm[c1_slot] = PK::make(jn, (uint32_t)fslot, 0);
+                __syncwarp();
+            } else if (fslot >= 0 && lane == c1_lane) {
 #pragma unroll
-                for (int s = 0; s < SL; s++) if (s == c1_slot) s_jsm[s] = PK::make(jn, (uint32_t)fslot, 0);
+                for (int s = 0; s < SL; s++) if (s == c1_slot) s_jsm[s] = jsm_make(jn, (uint32_t)fslot, 0);
             }
         }
 
