@@ -253,7 +253,10 @@ fsscs_decode_kernel(const DecodeParams P) {
     }
     auto node_rec = [&](int jj) -> uint32_t { return nodes_smem ? smem[jj] : __ldg(P.nodes + jj); };
     uint32_t *wb = smem + P.sched_words + warp * P.warp_words;
-    float *chan_s = reinterpret_cast<float *>(wb);                 // channel row (CHAN_SMEM)
+    // BIG: the first KW stack keys live in shared memory (the rest in global)
+    constexpr int KW = 128;
+    unsigned long long *wkey = reinterpret_cast<unsigned long long *>(wb);
+    float *chan_s = reinterpret_cast<float *>(wb + P.win_words);   // channel row (CHAN_SMEM)
     float *alpha = CHAN_SMEM ? chan_s + N : chan_s;                // stages >= 6 (+ scratch)
     uint32_t *beta = reinterpret_cast<uint32_t *>(alpha + N);
     uint32_t *best = beta + nw;
@@ -270,6 +273,11 @@ fsscs_decode_kernel(const DecodeParams P) {
     unsigned long long *skey = BIG ? P.stack_keys + (size_t)gwarp * (size_t)D : nullptr;
     uint32_t *sjsm = BIG ? P.stack_jsm + (size_t)gwarp * (size_t)D : nullptr;
     uint2 *ghdr = BIG ? P.hdr_global + (size_t)gwarp * (size_t)D : nullptr;
+    auto kget = [&](int i) -> unsigned long long { return i < KW ? wkey[i] : __ldcg(skey + i); };
+    auto kset = [&](int i, unsigned long long k) {
+        if (i < KW) wkey[i] = k;
+        else skey[i] = k;
+    };
     auto hdr_at = [&](int k) -> uint2 * { return BIG ? ghdr + k : reinterpret_cast<uint2 *>(shdr) + k; };
     const int sstride = (NL > 0) ? nw : P.snap_stride;
     auto snap_slot = [&](int k) -> uint32_t * {
@@ -320,8 +328,9 @@ fsscs_decode_kernel(const DecodeParams P) {
         int nS = 1;
         int uhint = 0;
         int widx = 0;                     // BIG: index of the working path's entry (-1: not live)
+        int nA = 1, hole = -1;            // BIG: array extent; the popped entry's index until refilled
         if (BIG) {
-            if (lane == 0) { skey[0] = 0ull; sjsm[0] = PK::make(0, PK::NONE, 0); }
+            if (lane == 0) { kset(0, 0ull); sjsm[0] = PK::make(0, PK::NONE, 0); }
             #pragma unroll 1
             for (int w = lane; w < P.used_words; w += 32) snap_used[w] = 0u;
         } else if (lane < 4) {
@@ -356,12 +365,12 @@ fsscs_decode_kernel(const DecodeParams P) {
                 // 4 independent loads in flight per lane per round
                 unsigned long long lk = ~0ull;
                 #pragma unroll 1
-                for (int i0 = 0; i0 < nS; i0 += 128) {
+                for (int i0 = 0; i0 < nA; i0 += 128) {
                     unsigned long long k4[4];
 #pragma unroll
                     for (int q = 0; q < 4; q++) {
                         const int i = i0 + 32 * q + lane;
-                        k4[q] = (i < nS) ? __ldcg(skey + i) : ~0ull;
+                        k4[q] = (i < nA) ? kget(i) : ~0ull;
                     }
 #pragma unroll
                     for (int q = 0; q < 4; q++)
@@ -379,13 +388,11 @@ fsscs_decode_kernel(const DecodeParams P) {
             const int owner = __ffs(__ballot_sync(FULL, lpm == mpm && lser == mser)) - 1;
             uint32_t p_jsm;
             if (BIG) {
-                // remove entry `pi`: the last entry moves into its place
+                // remove entry `pi`: it becomes a hole that c1 of this pop refills
                 const int pi = __shfl_sync(FULL, ls, owner);
                 p_jsm = __ldcg(sjsm + pi);
-                if (lane == 0 && pi != nS - 1) { skey[pi] = __ldcg(skey + nS - 1); sjsm[pi] = __ldcg(sjsm + nS - 1); }
-                __syncwarp();
+                hole = pi;
                 if (widx == pi) widx = -1;
-                else if (widx == nS - 1) widx = pi;
             } else {
                 p_jsm = __shfl_sync(FULL, ljsm, owner);
                 if (lane == owner) {
@@ -409,21 +416,23 @@ fsscs_decode_kernel(const DecodeParams P) {
                     // in-place compaction of the entries with depth > j
                     int nwidx = -1;
                     #pragma unroll 1
-                    for (int i0 = 0; i0 < nS; i0 += 32) {
+                    for (int i0 = 0; i0 < nA; i0 += 32) {
                         const int i = i0 + lane;
                         unsigned long long a = 0;
                         uint32_t x = 0;
-                        if (i < nS) { a = __ldcg(skey + i); x = __ldcg(sjsm + i); }
-                        const bool keep = (i < nS) && (int)PK::j(x) > j;
+                        if (i < nA) { a = kget(i); x = __ldcg(sjsm + i); }
+                        const bool keep = (i < nA) && i != hole && (int)PK::j(x) > j;
                         const uint32_t kb = __ballot_sync(FULL, keep);
                         const int o = cntv + __popc(kb & ((1u << lane) - 1u));
                         const uint32_t wbb = __ballot_sync(FULL, keep && i == widx);
                         if (wbb) nwidx = cntv + __popc(kb & ((1u << (__ffs(wbb) - 1)) - 1u));
                         __syncwarp();
-                        if (keep) { skey[o] = a; sjsm[o] = x; }
+                        if (keep) { kset(o, a); sjsm[o] = x; }
                         cntv += __popc(kb);
                     }
                     widx = nwidx;
+                    nA = cntv;
+                    hole = -1;
                     __syncwarp();
                 } else {
 #pragma unroll
@@ -453,7 +462,7 @@ fsscs_decode_kernel(const DecodeParams P) {
                     if (wi >= 0) {
                         const uint32_t wj = __ldcg(sjsm + wi);
                         if (PK::snap(wj) == PK::NONE) {
-                            const int slot = alloc_snapshot_big(snap_used, uhint, sjsm, nS, D, -1, PK::snap(p_jsm), lane);
+                            const int slot = alloc_snapshot_big(snap_used, uhint, sjsm, nA, D, hole, PK::snap(p_jsm), lane);
                             uint32_t *dst = snap_slot(slot);
                             const int nwords = (work_pl + 31) >> 5;
                             #pragma unroll 1
@@ -595,6 +604,19 @@ fsscs_decode_kernel(const DecodeParams P) {
                     __syncwarp();
                     have_best = true;
                     best_pm = p_pm;
+                }
+                if (BIG && hole >= 0) {
+                    // no candidate refills the hole: the last entry moves into it
+                    if (hole != nA - 1) {
+                        const unsigned long long k = kget(nA - 1);
+                        const uint32_t x = __ldcg(sjsm + nA - 1);
+                        __syncwarp();
+                        if (lane == 0) { kset(hole, k); sjsm[hole] = x; }
+                        if (widx == nA - 1) widx = hole;
+                    }
+                    __syncwarp();
+                    nA--;
+                    hole = -1;
                 }
                 continue;
             }
@@ -855,7 +877,7 @@ fsscs_decode_kernel(const DecodeParams P) {
             int fslot = -1;
             const int nfit = min(nc, D - nS);
             auto write_fork_snapshot = [&](int victim_lane, int victim_slot) {
-                if (BIG) fslot = alloc_snapshot_big(snap_used, uhint, sjsm, nS, D, victim_slot, PK::NONE, lane);
+                if (BIG) fslot = alloc_snapshot_big(snap_used, uhint, sjsm, nA, D, hole >= 0 ? hole : victim_slot, PK::NONE, lane);
                 else fslot = alloc_snapshot_lazy<SL>(snap_used, s_ser, s_jsm, D, victim_lane, victim_slot, SNAP_NONE, lane);
                 uint32_t *dst = snap_slot(fslot);
                 const int nwords = (npl + 31) >> 5;
@@ -867,14 +889,19 @@ fsscs_decode_kernel(const DecodeParams P) {
             int c1_lane = 0, c1_slot = 0;
             if (BIG) {
                 const uint32_t jbase = PK::make(jn, (nfit == 1) ? PK::NONE : (uint32_t)fslot, 0);
+                // c1 refills the hole left by p (if any), the siblings are appended
+                const int pos0 = (hole >= 0) ? hole : nA;
+                const int posk = (lane == 0) ? pos0 : (hole >= 0 ? nA + lane - 1 : nA + lane);
                 if (lane < nfit) {
                     const uint32_t mk = (clist >> (4 * lane)) & 15u;
-                    skey[nS + lane] = ((unsigned long long)__float_as_uint(p_pm + my_d) << 32) | (ser0 + (uint32_t)lane);
-                    sjsm[nS + lane] = jbase | ((mk ^ (uint32_t)m0) << PK::MSH);
+                    kset(posk, ((unsigned long long)__float_as_uint(p_pm + my_d) << 32) | (ser0 + (uint32_t)lane));
+                    sjsm[posk] = jbase | ((mk ^ (uint32_t)m0) << PK::MSH);
                 }
-                c1_slot = nS;
-                widx = nS;
+                c1_slot = pos0;
+                widx = pos0;
                 __syncwarp();
+                nA += nfit - (hole >= 0 ? 1 : 0);
+                hole = -1;
                 nS += nfit;
             } else {
                 int base = 0;
@@ -913,8 +940,8 @@ fsscs_decode_kernel(const DecodeParams P) {
                 if (BIG) {
                     unsigned long long xk = 0;
                     #pragma unroll 1
-                    for (int i = lane; i < nS; i += 32) {
-                        const unsigned long long k = __ldcg(skey + i);
+                    for (int i = lane; i < nA; i += 32) {
+                        const unsigned long long k = kget(i);
                         if (xs < 0 || k > xk) { xk = k; xs = i; }
                     }
                     xpm = (uint32_t)(xk >> 32);
@@ -932,7 +959,7 @@ fsscs_decode_kernel(const DecodeParams P) {
                 if (fslot < 0) write_fork_snapshot(tl, ts);
                 if (BIG) {
                     if (lane == 0) {
-                        skey[ts] = ((unsigned long long)cpm << 32) | (ser0 + (uint32_t)r);
+                        kset(ts, ((unsigned long long)cpm << 32) | (ser0 + (uint32_t)r));
                         sjsm[ts] = PK::make(jn, (uint32_t)fslot, (uint32_t)(mt ^ m0));
                     }
                     __syncwarp();
