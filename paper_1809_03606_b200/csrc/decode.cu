@@ -361,16 +361,26 @@ fsscs_decode_kernel(const DecodeParams P) {
             // ---- select: min (PM, serial) (reading R7)
             uint32_t lpm = EMPTY, lser = EMPTY, ljsm = 0;
             int ls = 0;
+            uint32_t ljsm_big = 0;
             if (BIG) {
-                // 4 independent loads in flight per lane per round
+                // window keys from shared memory, the rest from global memory with 4
+                // independent loads in flight per lane per round
                 unsigned long long lk = ~0ull;
+                int lq = 0;
+#pragma unroll
+                for (int q = 0; q < 4; q++) {
+                    const int i = 32 * q + lane;
+                    const unsigned long long k = (i < nA) ? wkey[i] : ~0ull;
+                    if (k < lk) { lk = k; lq = q; }
+                }
+                ls = 32 * lq + lane;
                 #pragma unroll 1
-                for (int i0 = 0; i0 < nA; i0 += 128) {
+                for (int i0 = KW; i0 < nA; i0 += 128) {
                     unsigned long long k4[4];
 #pragma unroll
                     for (int q = 0; q < 4; q++) {
                         const int i = i0 + 32 * q + lane;
-                        k4[q] = (i < nA) ? kget(i) : ~0ull;
+                        k4[q] = (i < nA) ? __ldcg(skey + i) : ~0ull;
                     }
 #pragma unroll
                     for (int q = 0; q < 4; q++)
@@ -378,6 +388,9 @@ fsscs_decode_kernel(const DecodeParams P) {
                 }
                 lpm = (uint32_t)(lk >> 32);
                 lser = (uint32_t)lk;
+                // speculative: every lane fetches the jsm word of its own best entry
+                // while the warp reduction runs
+                ljsm_big = (lk != ~0ull) ? __ldcg(sjsm + ls) : 0u;
             } else {
 #pragma unroll
                 for (int s = 0; s < SL; s++)
@@ -390,7 +403,7 @@ fsscs_decode_kernel(const DecodeParams P) {
             if (BIG) {
                 // remove entry `pi`: it becomes a hole that c1 of this pop refills
                 const int pi = __shfl_sync(FULL, ls, owner);
-                p_jsm = __ldcg(sjsm + pi);
+                p_jsm = __shfl_sync(FULL, ljsm_big, owner);
                 hole = pi;
                 if (widx == pi) widx = -1;
             } else {
@@ -1035,6 +1048,7 @@ int specialised_nl(int n, int slots, bool snap_smem, bool chan_smem) {
     if (n == 10 && slots == 1 && !snap_smem && !chan_smem) return 10;
     if (n == 11 && slots == 2 && !snap_smem && !chan_smem) return 11;
     if (n == 12 && slots == 4 && !snap_smem && !chan_smem) return 12;
+    if (n == 10 && slots == 0 && !snap_smem && !chan_smem) return 100;   // the paper's workload, D > 128
     return 0;
 }
 
@@ -1045,6 +1059,7 @@ cudaError_t launch_decode(const DecodeParams &p, int slots, bool snap_smem, bool
     case 10: return launch_t<1, false, false, 10>(p, ctas, smem, st);
     case 11: return launch_t<2, false, false, 11>(p, ctas, smem, st);
     case 12: return launch_t<4, false, false, 12>(p, ctas, smem, st);
+    case 100: return launch_t<0, false, false, 10>(p, ctas, smem, st);
     default: break;
     }
     if (snap_smem) return chan_smem ? launch_s<true, true>(p, slots, ctas, smem, st) : launch_s<true, false>(p, slots, ctas, smem, st);
@@ -1071,6 +1086,7 @@ cudaError_t decode_occupancy(int n, int slots, bool snap_smem, bool chan_smem, i
     case 10: return occ_t<1, false, false, 10>(smem, blocks_per_sm);
     case 11: return occ_t<2, false, false, 11>(smem, blocks_per_sm);
     case 12: return occ_t<4, false, false, 12>(smem, blocks_per_sm);
+    case 100: return occ_t<0, false, false, 10>(smem, blocks_per_sm);
     default: break;
     }
     if (snap_smem) return chan_smem ? occ_s<true, true>(slots, smem, blocks_per_sm) : occ_s<true, false>(slots, smem, blocks_per_sm);
