@@ -184,6 +184,7 @@ int polar_scs_create_ex(polar_scs_t *out, int32_t N, int32_t K, const uint8_t *f
     p.hdr_words = slots ? 2 * D : 0;
     p.used_words = slots ? 4 : round4((D + 31) / 32);
     p.win_words = slots ? 0 : 256;
+    p.uhat_words = p.nonsys ? nw : 0;
 
     // Layout choice: per warp, alpha stages >= 6 (N floats incl. scratch), flat
     // beta, best-effort beta and counters always live in shared memory; the
@@ -201,7 +202,8 @@ int polar_scs_create_ex(polar_scs_t *out, int32_t N, int32_t K, const uint8_t *f
             if (snap_smem && (flags & POLAR_FLAG_SNAP_GLOBAL)) continue;
             if (snap_smem && slots == 0) continue;          // D > 128: the arena is global
             if (!snap_smem && (flags & POLAR_FLAG_SNAP_SMEM)) continue;
-            const int ww = round4(p.win_words + (chan_smem ? N : 0) + N + 2 * nw + cnt_words + p.hdr_words + p.used_words + nw +
+            const int ww = round4(p.win_words + (chan_smem ? N : 0) + N + 2 * nw + cnt_words + p.hdr_words + p.used_words +
+                                  p.uhat_words +
                                   (snap_smem ? D * sstride : 0));
             const int smem = 4 * (sched_words + kDecodeWarps * ww);
             if (smem > optin) continue;

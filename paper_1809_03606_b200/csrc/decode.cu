@@ -265,7 +265,7 @@ fsscs_decode_kernel(const DecodeParams P) {
     uint32_t *snap_used = shdr + P.hdr_words;                      // snapshot-slot bitmap (used_words)
     uint32_t *uhat = snap_used + P.used_words;                     // nw words: u_hat (non-systematic)
     // snapshot slot k of this warp: shared memory, or global slot index snap0 + k
-    uint32_t *snap_s = uhat + nw;
+    uint32_t *snap_s = uhat + P.uhat_words;                        // (uhat_words = nw only when non-systematic)
     const uint32_t gwarp = (uint32_t)(blockIdx.x * kDecodeWarps + warp);
     const uint32_t snap0 = gwarp * (uint32_t)D;
     // global stack (BIG): keys (PM bits << 32 | serial: u64 order = (PM, serial)

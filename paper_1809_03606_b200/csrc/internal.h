@@ -61,6 +61,7 @@ struct DecodeParams {
     int cnt_words;              // words of the per-length counters (u16 each)
     int hdr_words;              // shared-memory fork headers: 2 D (register stacks) or 0
     int used_words;             // snapshot-slot bitmap words: 4, or ceil(D/32) rounded (D > 128)
+    int uhat_words;             // nw when non-systematic (u_hat scratch), else 0
     int win_words;              // D > 128: shared-memory window of the first 128 stack keys (256 words)
     int nonsys;                 // 1: read u_hat = x_hat F restricted to A (non-systematic)
 };
