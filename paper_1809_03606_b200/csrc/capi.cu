@@ -16,7 +16,7 @@ cudaError_t launch_decode(const DecodeParams &p, int slots, bool snap_smem, bool
                           cudaStream_t st);
 cudaError_t decode_occupancy(int n, int slots, bool snap_smem, bool chan_smem, int smem, int *blocks_per_sm);
 cudaError_t launch_list(const ListParams &p, int lcap, int ctas, int smem, cudaStream_t st);
-cudaError_t list_occupancy(int lcap, int L, int smem, int *blocks_per_sm);
+cudaError_t list_occupancy(int lcap, int n, int L, int smem, int *blocks_per_sm);
 cudaError_t launch_crc_attach(const CodecParams &p, cudaStream_t st);
 cudaError_t launch_encode(const CodecParams &p, cudaStream_t st);
 cudaError_t launch_modulate(const CodecParams &p, cudaStream_t st);
@@ -252,7 +252,7 @@ int polar_scs_create_ex(polar_scs_t *out, int32_t N, int32_t K, const uint8_t *f
         const int smem = 4 * list_layout(lp);
         const int lcap = h->L <= 8 ? 8 : (h->L <= 16 ? 16 : 32);
         int occ = 0;
-        if (smem <= optin && list_occupancy(lcap, h->L, smem, &occ) == cudaSuccess && occ >= 1) {
+        if (smem <= optin && list_occupancy(lcap, t.n, h->L, smem, &occ) == cudaSuccess && occ >= 1) {
             h->list_ctas = occ * sms;
             h->list_smem = smem;
             h->list_lcap = lcap;

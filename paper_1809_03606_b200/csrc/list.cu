@@ -73,13 +73,15 @@ __device__ __forceinline__ void list_alpha_stage(const float *src, bool src_glob
 
 }  // namespace
 
-template <int LCAP>
+// NL > 0: compile-time code length 2^NL (the BASELINE codes), else any N.
+template <int LCAP, int NL = 0>
 __global__ void __launch_bounds__(LCAP * 32) fsscl_decode_kernel(const ListParams P) {
     extern __shared__ __align__(16) uint32_t smem[];
     const int lane = threadIdx.x & 31;
     const int w = threadIdx.x >> 5;
     const int tid = threadIdx.x;
-    const int n = P.n, N = 1 << n, nw = P.nw, L = P.L, M = P.M, K = P.K;
+    const int n = (NL > 0) ? NL : P.n, N = 1 << n, nw = (NL > 0) ? (NL >= 5 ? (1 << NL) / 32 : 1) : P.nw;
+    const int L = P.L, M = P.M, K = P.K;
 
     uint32_t *nodes_s = smem;                                         // [M]
     float *abuf = reinterpret_cast<float *>(smem + P.o_alpha);         // stage s: L buffers of 2^s at L(2^s - 64)
@@ -381,7 +383,8 @@ __global__ void __launch_bounds__(LCAP * 32) fsscl_decode_kernel(const ListParam
             lev_mem = lam + 1;
             __syncthreads();
 
-            // ---- prune to the L best keys (reading R22): rank by counting
+            // ---- prune to the L best keys (reading R22): rank by
+            // counting (every thread reads the same key at a time: smem broadcast)
             const int total = nL * nc;
             if (tid < total) {
                 const unsigned long long key = cand_s[tid];
@@ -489,9 +492,9 @@ __global__ void __launch_bounds__(LCAP * 32) fsscl_decode_kernel(const ListParam
     }
 }
 
-template <int LCAP>
+template <int LCAP, int NL = 0>
 static cudaError_t launch_list_t(const ListParams &p, int ctas, int smem, cudaStream_t st) {
-    auto kern = fsscl_decode_kernel<LCAP>;
+    auto kern = fsscl_decode_kernel<LCAP, NL>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     kern<<<ctas, p.L * 32, smem, st>>>(p);
@@ -499,6 +502,9 @@ static cudaError_t launch_list_t(const ListParams &p, int ctas, int smem, cudaSt
 }
 
 cudaError_t launch_list(const ListParams &p, int lcap, int ctas, int smem, cudaStream_t st) {
+    if (lcap == 8 && p.n == 10) return launch_list_t<8, 10>(p, ctas, smem, st);
+    if (lcap == 8 && p.n == 7) return launch_list_t<8, 7>(p, ctas, smem, st);
+    if (lcap == 16 && p.n == 11) return launch_list_t<16, 11>(p, ctas, smem, st);
     switch (lcap) {
     case 8: return launch_list_t<8>(p, ctas, smem, st);
     case 16: return launch_list_t<16>(p, ctas, smem, st);
@@ -506,14 +512,17 @@ cudaError_t launch_list(const ListParams &p, int lcap, int ctas, int smem, cudaS
     }
 }
 
-template <int LCAP>
+template <int LCAP, int NL = 0>
 static cudaError_t list_occ_t(int L, int smem, int *blocks) {
-    cudaError_t e = cudaFuncSetAttribute(fsscl_decode_kernel<LCAP>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaError_t e = cudaFuncSetAttribute(fsscl_decode_kernel<LCAP, NL>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, fsscl_decode_kernel<LCAP>, L * 32, smem);
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, fsscl_decode_kernel<LCAP, NL>, L * 32, smem);
 }
 
-cudaError_t list_occupancy(int lcap, int L, int smem, int *blocks_per_sm) {
+cudaError_t list_occupancy(int lcap, int n, int L, int smem, int *blocks_per_sm) {
+    if (lcap == 8 && n == 10) return list_occ_t<8, 10>(L, smem, blocks_per_sm);
+    if (lcap == 8 && n == 7) return list_occ_t<8, 7>(L, smem, blocks_per_sm);
+    if (lcap == 16 && n == 11) return list_occ_t<16, 11>(L, smem, blocks_per_sm);
     switch (lcap) {
     case 8: return list_occ_t<8>(L, smem, blocks_per_sm);
     case 16: return list_occ_t<16>(L, smem, blocks_per_sm);
