@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--chan-smem", action="store_true")
     ap.add_argument("--bit-level", action="store_true",
                     help="bit-level SCS-RM (leaf-only schedule; the paper's SCS-RM comparator, PAPER.md:L797-813)")
+    ap.add_argument("--list-kernel", default="auto", choices=["auto", "cta", "packed"],
+                    help="FSSCL kernel: CTA of L warps per frame, or one warp per frame with packed paths")
     ap.add_argument("--list", action="store_true",
                     help="FSSCL list decoder with list size = the config's L (the paper's FSSCL comparator, "
                          "PAPER.md:L521-587); with --bit-level: plain SCL")
@@ -231,7 +233,7 @@ def run_ours(args, cfg, c):
     fr = P.bhattacharyya_mask(c["N"], c["K"], c["design_db"])
     dec = P.PolarSCS(fr, c["D"], c["L"], c["crc_poly"], bit_level=bool(c.get("bit_level")),
                      snap_global=args.snap_global, snap_smem=args.snap_smem,
-                     chan_global=args.chan_global, chan_smem=args.chan_smem)
+                     chan_global=args.chan_global, chan_smem=args.chan_smem, list_kernel=args.list_kernel)
     K, N = c["K"], c["N"]
 
     # inputs: device generator, each rank its own frame range; all points share
@@ -373,7 +375,9 @@ def run_ours(args, cfg, c):
         "systematic polar encoding, BPSK-AWGN LLRs)",
         "config": {"workload": workload_name(cfg, c), "frames_per_step_per_gpu": frames,
                    "l2": f"inputs {frames * N * 4 / 1e9:.2f} GB per step > 126 MB L2 (no flush needed)",
-                   "launch": ({"ctas": info["list_ctas"], "warps_per_cta": c["L"],
+                   "launch": ({"ctas": info["list_ctas"],
+                               "kernel": "packed (warp per frame)" if info["list_packed"] else "cta (warp per path)",
+                               "warps_per_cta": info["list_warps_per_cta"] if info["list_packed"] else c["L"],
                                "smem_per_cta": info["list_smem_per_cta"]} if is_list else
                               {"ctas": info["ctas"], "warps_per_cta": info["warps_per_cta"],
                                "smem_per_cta": info["smem_per_cta"], "snap_in_smem": info["snap_in_smem"],

@@ -53,6 +53,10 @@ extern "C" {
 #define POLAR_FLAG_NONSYSTEMATIC 0x40u /* non-systematic code: encoders emit c = u F,
                                           decoders read u_hat = x_hat F restricted to A
                                           (PAPER.md:L503); any mask is allowed */
+#define POLAR_FLAG_LIST_CTA     0x80u /* polar_scl_decode: one CTA of L warps per frame
+                                         (warp = path) instead of the automatic choice */
+#define POLAR_FLAG_LIST_PACKED  0x100u /* polar_scl_decode: one warp per frame with the L
+                                          paths packed across its lanes */
 
 typedef struct polar_scs_s *polar_scs_t;
 
@@ -67,6 +71,8 @@ typedef struct {
     int32_t systematic_ok;    /* 1 if the mask is systematic-encodable            */
     uint32_t flags;
     int32_t list_ctas, list_smem_per_cta;  /* polar_scl_decode launch (0: unsupported) */
+    int32_t list_packed;      /* 1: warp-per-frame packed FSSCL kernel, 0: CTA of L warps */
+    int32_t list_warps_per_cta;
 } polar_scs_info_t;
 
 /*

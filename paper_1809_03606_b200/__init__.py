@@ -31,13 +31,15 @@ POLAR_FLAG_CHAN_GLOBAL = 0x4
 POLAR_FLAG_SNAP_SMEM = 0x8
 POLAR_FLAG_CHAN_SMEM = 0x10
 POLAR_FLAG_NONSYSTEMATIC = 0x40
+POLAR_FLAG_LIST_CTA = 0x80
+POLAR_FLAG_LIST_PACKED = 0x100
 
 
 class PolarInfo(C.Structure):
     _fields_ = [(n, C.c_int32) for n in (
         "N", "n", "K", "crc_bits", "D", "L", "num_ops", "num_nodes", "warps_per_cta", "ctas",
         "smem_per_cta", "snap_in_smem", "chan_in_smem", "systematic_ok")] + [("flags", C.c_uint32)] + [
-        (n, C.c_int32) for n in ("list_ctas", "list_smem_per_cta")]
+        (n, C.c_int32) for n in ("list_ctas", "list_smem_per_cta", "list_packed", "list_warps_per_cta")]
 
     def as_dict(self):
         return {n: int(getattr(self, n)) for n, _ in self._fields_}
@@ -121,13 +123,14 @@ class PolarSCS:
 
     def __init__(self, frozen_mask, D: int, L: int, crc_poly: int = 0, bit_level: bool = False,
                  snap_global: bool = False, chan_global: bool = False, snap_smem: bool = False,
-                 chan_smem: bool = False, nonsystematic: bool = False):
+                 chan_smem: bool = False, nonsystematic: bool = False, list_kernel: str = "auto"):
         fm = np.ascontiguousarray(frozen_mask, dtype=np.uint8)
         self.N = int(fm.size)
         self.K = int(self.N - int(fm.sum()))
         flags = ((POLAR_FLAG_BIT_LEVEL if bit_level else 0) | (POLAR_FLAG_SNAP_GLOBAL if snap_global else 0)
                  | (POLAR_FLAG_CHAN_GLOBAL if chan_global else 0) | (POLAR_FLAG_SNAP_SMEM if snap_smem else 0)
-                 | (POLAR_FLAG_CHAN_SMEM if chan_smem else 0) | (POLAR_FLAG_NONSYSTEMATIC if nonsystematic else 0))
+                 | (POLAR_FLAG_CHAN_SMEM if chan_smem else 0) | (POLAR_FLAG_NONSYSTEMATIC if nonsystematic else 0)
+                 | {"auto": 0, "cta": POLAR_FLAG_LIST_CTA, "packed": POLAR_FLAG_LIST_PACKED}[list_kernel])
         h = _vp()
         _check(polar_scs_create_ex(C.byref(h), self.N, self.K, fm.ctypes.data, int(D), int(L),
                                    int(crc_poly), flags), "polar_scs_create")

@@ -17,6 +17,8 @@ cudaError_t launch_decode(const DecodeParams &p, int slots, bool snap_smem, bool
 cudaError_t decode_occupancy(int n, int slots, bool snap_smem, bool chan_smem, int smem, int *blocks_per_sm);
 cudaError_t launch_list(const ListParams &p, int lcap, int ctas, int smem, cudaStream_t st);
 cudaError_t list_occupancy(int lcap, int n, int L, int smem, int *blocks_per_sm);
+cudaError_t launch_list_packed(const ListParams &p, int ctas, int smem, cudaStream_t st);
+cudaError_t list_packed_occupancy(int n, int pwarps, int smem, int *blocks_per_sm);
 cudaError_t launch_crc_attach(const CodecParams &p, cudaStream_t st);
 cudaError_t launch_encode(const CodecParams &p, cudaStream_t st);
 cudaError_t launch_modulate(const CodecParams &p, cudaStream_t st);
@@ -42,7 +44,7 @@ int round4(int w) { return (w + 3) & ~3; }
 void free_handle(polar_scs_t h) {
     if (!h) return;
     cudaFree(h->t.nodes); cudaFree(h->t.info); cudaFree(h->t.crc_tab); cudaFree(h->t.crc_bytes); cudaFree(h->t.info_words);
-    cudaFree(h->d_queue); cudaFree(h->d_snap); cudaFree(h->d_keys); cudaFree(h->d_jsm); cudaFree(h->d_hdr);
+    cudaFree(h->d_queue); cudaFree(h->d_snap); cudaFree(h->d_keys); cudaFree(h->d_jsm); cudaFree(h->d_hdr); cudaFree(h->d_galpha);
     for (int b = 0; b < 2; b++) {
         cudaFree(h->d_stage_llr[b]); cudaFree(h->d_stage_bits[b]);
         if (h->ev_h2d[b]) cudaEventDestroy(h->ev_h2d[b]);
@@ -92,10 +94,38 @@ int list_impl(polar_scs_t h, const float *llr, int64_t n, uint8_t *bits, float *
     ListParams p = h->list;
     p.llr = llr; p.n_frames = n; p.out_bits = bits; p.pm = pm; p.status = status;
     p.queue = h->d_queue + slot;
+    if (p.galpha) p.galpha += (size_t)h->list_ctas * p.pwarps * p.gstride * (size_t)slot;
     cudaError_t e = cudaMemsetAsync(p.queue, 0, sizeof(unsigned long long), st);
     if (e != cudaSuccess) return cuda_status(e);
+    if (h->list_packed) {
+        const int ctas = (int)std::min<int64_t>(h->list_ctas, (n + p.pwarps - 1) / p.pwarps);
+        return cuda_status(launch_list_packed(p, ctas, h->list_smem, st));
+    }
     const int ctas = (int)std::min<int64_t>(h->list_ctas, n);
     return cuda_status(launch_list(p, h->list_lcap, ctas, h->list_smem, st));
+}
+
+// packed FSSCL layout (list_packed.cu): node table, then one block per warp
+// with the offsets below (words, 16-byte aligned areas).  Returns the words
+// of one CTA.
+int list_packed_layout(ListParams &p) {
+    const int L = p.L, N = p.N;
+    p.o_warp0 = round4(p.M);
+    int o = 0;
+    if (p.M == 1) p.sg = p.n;                 // the root node uses the alpha area as scratch
+    p.o_alpha = o; o += round4(std::max(L * ((1 << p.sg) - 1), p.M == 1 ? N : 0));
+    p.gstride = (size_t)L * (size_t)(N - (1 << p.sg));
+    p.o_beta = o;  o += round4(2 * L * p.nw);
+    p.o_clist = o; o += round4(L);
+    p.o_mi = o;    o += round4(2 * L);
+    p.o_prow = o;  o += round4(4 * L);
+    p.o_cand = o;  o += round4(16 * L);
+    p.o_sel = o;   o += round4(L);
+    p.o_selpm = o; o += round4(2 * L);
+    p.o_ok = o;    o += round4(L);
+    p.o_reg = p.o_misc = 0;
+    p.words = o;
+    return p.o_warp0 + p.pwarps * o;
 }
 
 // FSSCL shared-memory layout (list.cu): offsets in 32-bit words, each area
@@ -140,7 +170,9 @@ int polar_scs_create_ex(polar_scs_t *out, int32_t N, int32_t K, const uint8_t *f
     if (!out) return POLAR_EINVAL;
     *out = nullptr;
     const uint32_t known = POLAR_FLAG_BIT_LEVEL | POLAR_FLAG_SNAP_GLOBAL | POLAR_FLAG_CHAN_GLOBAL |
-                           POLAR_FLAG_SNAP_SMEM | POLAR_FLAG_CHAN_SMEM | POLAR_FLAG_NONSYSTEMATIC;
+                           POLAR_FLAG_SNAP_SMEM | POLAR_FLAG_CHAN_SMEM | POLAR_FLAG_NONSYSTEMATIC |
+                           POLAR_FLAG_LIST_CTA | POLAR_FLAG_LIST_PACKED;
+    if ((flags & POLAR_FLAG_LIST_CTA) && (flags & POLAR_FLAG_LIST_PACKED)) return POLAR_EINVAL;
     if (D < 1 || D > kMaxD || L < 1 || (flags & ~known)) return POLAR_EINVAL;
     if ((flags & POLAR_FLAG_SNAP_GLOBAL) && (flags & POLAR_FLAG_SNAP_SMEM)) return POLAR_EINVAL;
     if ((flags & POLAR_FLAG_CHAN_GLOBAL) && (flags & POLAR_FLAG_CHAN_SMEM)) return POLAR_EINVAL;
@@ -243,21 +275,52 @@ int polar_scs_create_ex(polar_scs_t *out, int32_t N, int32_t K, const uint8_t *f
         p.stack_jsm = h->d_jsm;
         p.hdr_global = h->d_hdr;
     }
-    // ---- FSSCL launch (polar_scl_decode): one CTA of L warps per frame
+    // ---- FSSCL launch (polar_scl_decode): a CTA of L warps per frame, or one
+    // warp per frame with the paths packed across its lanes; automatic choice:
+    // the packed kernel when it keeps at least 4 frames per SM in flight
+    // (DESIGN.md §Kernels), else the CTA kernel
     if (h->L <= 32) {
-        ListParams &lp = h->list;
-        lp.nodes = t.nodes; lp.info = t.info; lp.crc_bytes = t.crc_bytes; lp.queue = h->d_queue;
-        lp.N = N; lp.n = t.n; lp.K = K; lp.c = t.c; lp.L = h->L; lp.M = t.M; lp.nw = nw;
-        lp.nonsys = p.nonsys;
-        const int smem = 4 * list_layout(lp);
+        ListParams base{};
+        base.nodes = t.nodes; base.info = t.info; base.crc_bytes = t.crc_bytes; base.queue = h->d_queue;
+        base.N = N; base.n = t.n; base.K = K; base.c = t.c; base.L = h->L; base.M = t.M; base.nw = nw;
+        base.nonsys = p.nonsys;
+        ListParams lc = base, lpk = base;
+        const int smem_c = 4 * list_layout(lc);
         const int lcap = h->L <= 8 ? 8 : (h->L <= 16 ? 16 : 32);
-        int occ = 0;
-        if (smem <= optin && list_occupancy(lcap, t.n, h->L, smem, &occ) == cudaSuccess && occ >= 1) {
-            h->list_ctas = occ * sms;
-            h->list_smem = smem;
-            h->list_lcap = lcap;
-        }
+        int occ_c = 0, occ_p = 0;
+        if (smem_c > optin || list_occupancy(lcap, t.n, h->L, smem_c, &occ_c) != cudaSuccess) occ_c = 0;
         cudaGetLastError();
+        // packed: 4, 2 or 1 warps per CTA, whichever keeps the most warps resident
+        int smem_p = 0, pw_best = 0;
+        // the top alpha stages move to a global (L2-resident) arena while that
+        // raises the resident warps (frames) per SM: take the fewest global
+        // stages that reach the best occupancy
+        for (int gst = 0; gst <= t.n; gst++) {
+            for (int pw = kListPackedWarps; pw >= 1; pw >>= 1) {
+                ListParams tp = base;
+                tp.pwarps = pw;
+                tp.sg = t.n - gst;
+                const int sm = 4 * list_packed_layout(tp);
+                int oc = 0;
+                if (sm > optin || list_packed_occupancy(t.n, pw, sm, &oc) != cudaSuccess) oc = 0;
+                cudaGetLastError();
+                if (oc * pw > occ_p * pw_best) { occ_p = oc; pw_best = pw; smem_p = sm; lpk = tp; }
+            }
+        }
+        bool packed = occ_p >= 1;                 // measured faster on C1-C4
+        if (flags & POLAR_FLAG_LIST_CTA) packed = false;
+        if (flags & POLAR_FLAG_LIST_PACKED) packed = true;
+        if (packed && occ_p >= 1) {
+            h->list = lpk; h->list_packed = 1; h->list_ctas = occ_p * sms; h->list_smem = smem_p;
+            if (lpk.gstride > 0) {
+                const size_t per = (size_t)h->list_ctas * lpk.pwarps * lpk.gstride;
+                e = cudaMalloc(&h->d_galpha, 2 * per * sizeof(float));
+                if (e != cudaSuccess) { free_handle(h); return cuda_status(e); }
+                h->list.galpha = h->d_galpha;
+            }
+        } else if (!packed && occ_c >= 1) {
+            h->list = lc; h->list_packed = 0; h->list_ctas = occ_c * sms; h->list_smem = smem_c; h->list_lcap = lcap;
+        }
     }
     *out = h;
     return POLAR_OK;
@@ -280,7 +343,8 @@ int polar_scs_get_info(polar_scs_t h, polar_scs_info_t *o) {
     o->num_ops = h->t.nops; o->num_nodes = h->t.M;
     o->warps_per_cta = h->warps_per_cta; o->ctas = h->ctas; o->smem_per_cta = h->smem_per_cta;
     o->snap_in_smem = h->snap_in_smem; o->chan_in_smem = h->chan_in_smem; o->systematic_ok = h->t.systematic_ok ? 1 : 0; o->flags = h->flags;
-    o->list_ctas = h->list_ctas; o->list_smem_per_cta = h->list_smem;
+    o->list_ctas = h->list_ctas; o->list_smem_per_cta = h->list_smem; o->list_packed = h->list_packed;
+    o->list_warps_per_cta = h->list_packed ? h->list.pwarps : h->L;
     return POLAR_OK;
 }
 

@@ -23,6 +23,7 @@ constexpr int kMaxD = 8192;     // D > 128: global-memory stack (the paper's D =
 constexpr int kDecodeWarps = 4;      // warps (frames in flight) per decode CTA
 constexpr int kDecodeMinBlocks = 8;  // launch bound: 32 resident warps/SM => <= 64 registers
 constexpr int kCodecWarps = 4;       // warps per CTA of the generator/encoder kernels
+constexpr int kListPackedWarps = 4;  // max warps (frames in flight) per CTA of the packed FSSCL kernel
 
 // Host-side compiled code description (host.cpp)
 struct CodeTables {
@@ -81,6 +82,11 @@ struct ListParams {
     unsigned long long *queue;
     int N, n, K, c, L, M, nw, nonsys;
     int o_alpha, o_beta, o_reg, o_clist, o_mi, o_prow, o_cand, o_sel, o_selpm, o_ok, o_misc, words;
+    int o_warp0;                // packed kernel: words before the per-warp blocks (node table)
+    int pwarps;                 // packed kernel: warps (frames) per CTA
+    int sg;                     // packed kernel: first alpha stage kept in the global arena (n: none)
+    float *galpha;              // packed kernel: global alpha arena (stages >= sg), gstride floats per warp
+    size_t gstride;
 };
 
 struct CodecParams {
@@ -119,6 +125,8 @@ struct polar_scs_s {
     int warps_per_cta = 0, ctas = 0, smem_per_cta = 0;
     polar::DecodeParams base{};     // prefilled params
     int list_ctas = 0, list_smem = 0, list_lcap = 0;   // FSSCL launch (0 = list decode unsupported)
+    int list_packed = 0;            // 1: the warp-per-frame packed FSSCL kernel (list_packed.cu)
+    float *d_galpha = nullptr;      // packed FSSCL: global arena of the top alpha stages, 2 slots
     polar::ListParams list{};       // prefilled FSSCL params
     // host-staging for polar_scs_decode_host (lazily allocated)
     cudaStream_t s_h2d = nullptr, s_comp[2] = {nullptr, nullptr}, s_d2h = nullptr;

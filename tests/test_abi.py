@@ -86,7 +86,8 @@ def test_create_rejects_bad_arguments():
     for args in bad:
         assert P.polar_scs_create(ctypes.byref(h), *args) == P.POLAR_EINVAL, args
     assert P.polar_scs_create(None, 128, 64, ok, 8, 4, 0) == P.POLAR_EINVAL
-    assert P.polar_scs_create_ex(ctypes.byref(h), 128, 64, ok, 8, 4, 0, 0x80) == P.POLAR_EINVAL
+    assert P.polar_scs_create_ex(ctypes.byref(h), 128, 64, ok, 8, 4, 0, 0x200) == P.POLAR_EINVAL   # unknown flag
+    assert P.polar_scs_create_ex(ctypes.byref(h), 128, 64, ok, 8, 4, 0, 0x180) == P.POLAR_EINVAL   # both list kernels
     small = P.bhattacharyya_mask(16, 4, 2.0)
     assert P.polar_scs_create(ctypes.byref(h), 16, 4, small.ctypes.data, 8, 4, 0x11021) == P.POLAR_EINVAL  # c >= K
     P.polar_scs_destroy(None)                                     # no-op

@@ -33,8 +33,12 @@ def _compare(gpu, ref, ctx=""):
     np.testing.assert_allclose(g["pm"], ref["pm"], rtol=PM_RTOL, atol=0, err_msg=ctx)
 
 
-def _run(fr, L, crc, ebnos, n, seed, bit_level=False, nonsys=False, D=8):
-    dec = P.PolarSCS(fr, D, L, crc, bit_level=bit_level, nonsystematic=nonsys)
+def _run(fr, L, crc, ebnos, n, seed, bit_level=False, nonsys=False, D=8, lk="auto"):
+    dec = P.PolarSCS(fr, D, L, crc, bit_level=bit_level, nonsystematic=nonsys, list_kernel=lk)
+    if dec.info["list_ctas"] == 0:
+        pytest.skip(f"{lk} list kernel does not fit shared memory")
+    if lk != "auto":
+        assert dec.info["list_packed"] == int(lk == "packed")
     K = dec.K
     for ebno in ebnos:
         pay = ig.payload_bits(seed, 0, n, K - dec.c)
@@ -58,11 +62,13 @@ def _run(fr, L, crc, ebnos, n, seed, bit_level=False, nonsys=False, D=8):
     ("C3", 8, (1.0, 2.0), 300),
     ("C4", 16, (1.5, 2.5), 100),
     ("C5", 8, (3.0, 4.0), 40),
+    ("C5", 32, (3.0,), 24),          # the config's L = 32: packed kernel only (alpha stages in L2)
 ])
-def test_list_parity_configs(cfg, L, ebnos, n):
+@pytest.mark.parametrize("lk", ["cta", "packed"])
+def test_list_parity_configs(cfg, L, ebnos, n, lk):
     c = ig.CONFIGS[cfg]
     fr = P.bhattacharyya_mask(c["N"], c["K"], c["design_db"])
-    _run(fr, L, c["crc_poly"], ebnos, n, c["seed"])
+    _run(fr, L, c["crc_poly"], ebnos, n, c["seed"], lk=lk)
 
 
 @pytest.mark.parametrize("N,K,L,crc,bit_level", [
@@ -77,19 +83,21 @@ def test_list_parity_configs(cfg, L, ebnos, n):
     (64, 64, 4, 0, False), (128, 1, 4, 0, False), (256, 255, 4, 0, False),
     (2048, 1024, 4, 0, False), (4096, 2048, 2, 0x11021, False),
 ])
-def test_list_parity_edge(N, K, L, crc, bit_level):
+@pytest.mark.parametrize("lk", ["cta", "packed"])
+def test_list_parity_edge(N, K, L, crc, bit_level, lk):
     fr = P.bhattacharyya_mask(N, K, 2.0)
     if K == 0 or (crc and O.crc_degree(crc) >= K):
         pytest.skip("no information bits")
     n = 257 if N <= 1024 else 40
-    _run(fr, L, crc, (-1.0, 1.0, 3.0), n, N + K + L, bit_level=bit_level)
+    _run(fr, L, crc, (-1.0, 1.0, 3.0), n, N + K + L, bit_level=bit_level, lk=lk)
 
 
 @pytest.mark.parametrize("cfg,random_mask", [("C1", False), ("C3", False), ("C1", True)])
-def test_list_nonsystematic_parity(cfg, random_mask):
+@pytest.mark.parametrize("lk", ["cta", "packed"])
+def test_list_nonsystematic_parity(cfg, random_mask, lk):
     c = ig.CONFIGS[cfg]
     fr = _random_mask(c["N"], c["K"], 6) if random_mask else P.bhattacharyya_mask(c["N"], c["K"], c["design_db"])
-    _run(fr, min(c["L"], 8), c["crc_poly"], (1.5,), 200, 41, nonsys=True)
+    _run(fr, min(c["L"], 8), c["crc_poly"], (1.5,), 200, 41, nonsys=True, lk=lk)
 
 
 def test_list_degenerate_and_limits():
@@ -110,9 +118,10 @@ def test_list_degenerate_and_limits():
     llr = (1.0 - 2.0 * dec.encode(blk).float()) * 4.0
     r = dec.decode_list(llr)
     assert torch.equal(r["bits"], blk) and float(r["pm"].abs().max()) == 0.0
-    # a list that cannot fit: L > 32, or L * N too large for shared memory
-    for L, N, K in ((33, 128, 64), (32, 4096, 3072)):
-        d2 = P.PolarSCS(P.bhattacharyya_mask(N, K, 2.0), 8, L, 0)
+    # a list that cannot fit: L > 32 (any kernel), or the CTA kernel with L * N
+    # too large for shared memory (the packed kernel moves stages to L2)
+    for L, N, K, lk in ((33, 128, 64, "auto"), (32, 4096, 3072, "cta")):
+        d2 = P.PolarSCS(P.bhattacharyya_mask(N, K, 2.0), 8, L, 0, list_kernel=lk)
         assert d2.info["list_ctas"] == 0
         with pytest.raises(P.PolarError) as ei:
             d2.decode_list(torch.zeros((1, N), dtype=torch.float32, device="cuda"))

@@ -1,0 +1,4 @@
+mkdir -p gpurun_out
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1
+timeout 900 python -m pytest tests/test_gpu_list.py tests/test_gpu_random.py -m gpu -x -q > gpurun_out/pytest_list.log 2>&1; echo list=$? > gpurun_out/status15.txt
+for c in C1 C2 C3 C4 C5; do timeout 900 python bench.py --config $c --list --no-cpu > gpurun_out/lst_${c}.log 2>&1; done
