@@ -164,6 +164,11 @@ __global__ void __launch_bounds__(kListPackedWarps * 32) fsscl_packed_kernel(con
                 const int boff = (psi - 1) << s;
                 const bool top = (s + 1 == n), first = (s == s_hi);
                 const int tot = nL << s;
+                // buffers of one stage are contiguous: path k's element i of stage s
+                // is dst[(k << s) + i] = dst[idx]
+                float *dst = stage_buf(s, 0);
+                const float *sb = top ? chan : stage_buf(s + 1, 0);
+                const uint32_t *bpar = betaA + (size_t)par * L * nw;
                 #pragma unroll 1
                 for (int idx = lane; idx < tot; idx += 32) {
                     const int k = idx >> s, i = idx & (Ls - 1);
@@ -172,18 +177,19 @@ __global__ void __launch_bounds__(kListPackedWarps * 32) fsscl_packed_kernel(con
                         lo = __ldg(chan + i);
                         hi = __ldg(chan + Ls + i);
                     } else {
-                        const float *src = stage_buf(s + 1, first ? prow5(prow_s[par * L + k], s + 1) : k);
-                        lo = src[i];
-                        hi = src[Ls + i];
+                        const int kb = first ? prow5(prow_s[par * L + k], s + 1) : k;
+                        const float *src = sb + (kb << (s + 1)) + i;
+                        lo = src[0];
+                        hi = src[Ls];
                     }
                     float v;
                     if (odd) {
                         const int bp = boff + i;
-                        v = g_exact(lo, hi, (beta_of(par, k)[bp >> 5] >> (bp & 31)) & 1u);
+                        v = g_exact(lo, hi, (bpar[k * nw + (bp >> 5)] >> (bp & 31)) & 1u);
                     } else {
                         v = f_minsum(lo, hi);
                     }
-                    stage_buf(s, k)[i] = v;
+                    dst[idx] = v;
                 }
                 __syncwarp();
             }
@@ -218,15 +224,20 @@ __global__ void __launch_bounds__(kListPackedWarps * 32) fsscl_packed_kernel(con
                             vn += __shfl_down_sync(FULL, vn, h);
                             vp += __shfl_down_sync(FULL, vp, h);
                         }
-                        if (leader) {
+                        // the group leader holds the sums
+                        vn = __shfl_sync(FULL, vn, lane & ~(Lam - 1));
+                        vp = __shfl_sync(FULL, vp, lane & ~(Lam - 1));
+                        const bool rep = (kind == OP_REP);
+                        const uint32_t clist = rep ? ((vp < vn) ? 0x01u : 0x10u) : 0u;
+                        if (valid) {
                             const float pm = pm_s[par * L + k];
-                            const bool rep = (kind == OP_REP);
-                            const uint32_t clist = rep ? ((vp < vn) ? 0x01u : 0x10u) : 0u;
                             #pragma unroll 1
-                            for (int t = 0; t < nc; t++) {
+                            for (int t = i; t < nc; t += Lam) {
                                 const float d = ((clist >> (4 * t)) & 15u) ? vp : vn;
                                 cand_s[k * nc + t] = ((unsigned long long)__float_as_uint(pm + d) << 32) | (uint32_t)((k << 3) | t);
                             }
+                        }
+                        if (leader) {
                             clist_s[k] = clist;
                             const uint32_t fill = (rep && (clist & 15u)) ? FULL : 0u;
                             const uint32_t lm = ((Lam == 32) ? FULL : ((1u << Lam) - 1u)) << (seg & 31);
@@ -258,14 +269,16 @@ __global__ void __launch_bounds__(kListPackedWarps * 32) fsscl_packed_kernel(con
                                 if ((uint32_t)i == mx) key = 0xFFFFFFFFu;
                             }
                         }
-                        if (leader) {
+                        const uint32_t clist = cand_order(kind, parity, A);
+                        if (valid) {
                             const float pm = pm_s[par * L + k];
-                            const uint32_t clist = cand_order(kind, parity, A);
                             #pragma unroll 1
-                            for (int t = 0; t < nc; t++) {
+                            for (int t = i; t < nc; t += Lam) {
                                 const float d = flip_dpm((clist >> (4 * t)) & 15u, A);
                                 cand_s[k * nc + t] = ((unsigned long long)__float_as_uint(pm + d) << 32) | (uint32_t)((k << 3) | t);
                             }
+                        }
+                        if (leader) {
                             clist_s[k] = clist;
                             mi_s[k] = make_uint2(m[0] | (m[1] << 16), m[2] | (m[3] << 16));
                             // the HD word with c1's flips in path k's beta
@@ -375,25 +388,32 @@ __global__ void __launch_bounds__(kListPackedWarps * 32) fsscl_packed_kernel(con
             }
             __syncwarp();
 
-            // ---- prune to the L best keys (reading R22)
+            // ---- prune to the L best keys (reading R22).  Each
+            // path's nc keys ascend (dPM, then candidate rank), so the survivors
+            // come out of a tournament over the paths' list heads: lane k holds
+            // path k's head, L rounds of a warp minimum, the winner advances.
             const int total = nL * nc;
             const int npar = par ^ 1;
-            #pragma unroll 1
-            for (int u0 = 0; u0 < total; u0 += 32) {
-                const int u = u0 + lane;
-                const unsigned long long key = (u < total) ? cand_s[u] : ~0ull;
-                int rank = 0;
-                #pragma unroll 4
-                for (int v = 0; v < total; v++) rank += (cand_s[v] < key) ? 1 : 0;
-                if (u < total && rank < L) {
-                    sel_s[rank] = (uint32_t)key;
-                    pm_s[npar * L + rank] = __uint_as_float((uint32_t)(key >> 32));
+            const int nL2 = min(total, L);
+            {
+                int h = 0;
+                unsigned long long head = (lane < nL) ? cand_s[lane * nc] : ~0ull;
+                #pragma unroll 1
+                for (int r = 0; r < nL2; r++) {
+                    uint32_t mh, ml;
+                    warp_min_key((uint32_t)(head >> 32), (uint32_t)head, mh, ml);
+                    const unsigned long long mk = ((unsigned long long)mh << 32) | ml;
+                    if (head == mk) {            // keys are unique: one winner
+                        sel_s[r] = ml;
+                        pm_s[npar * L + r] = __uint_as_float(mh);
+                        h++;
+                        head = (h < nc) ? cand_s[lane * nc + h] : ~0ull;
+                    }
                 }
             }
             __syncwarp();
 
             // ---- rank r takes its parent's beta prefix, flips and pointer row
-            const int nL2 = min(total, L);
             const int npl = (phi + 1) << lam;
             const int nwp = (npl + 31) >> 5;
             #pragma unroll 1
