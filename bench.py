@@ -338,11 +338,16 @@ def run_ours(args, cfg, c):
     kern_s = statistics.median(launch_ms) / 1e3
     alg_bytes = frames * (4 * N + K)
     achieved_gbs = alg_bytes / kern_s / 1e9
-    traffic = None
-    tfile = os.path.join(ROOT, "profiles", f"decode_traffic_{cfg}.json")
-    if os.path.exists(tfile) and not c.get("bit_level") and not is_list:
-        with open(tfile) as fh:
-            traffic = json.load(fh)["bytes_per_frame"] * frames     # ncu dram bytes, scaled to this launch
+    # ncu evidence of the dominant kernel for this workload (committed capture):
+    # DRAM bytes per frame (scaled to this launch) and the issue-slot utilisation
+    traffic, ncu_ev = None, None
+    efile = os.path.join(ROOT, "profiles", "ncu_evidence.json")
+    ekey = cfg + ("_list" if is_list else "")
+    if os.path.exists(efile) and not c.get("bit_level"):
+        with open(efile) as fh:
+            ncu_ev = json.load(fh).get(ekey)
+        if ncu_ev:
+            traffic = ncu_ev["dram_bytes_per_frame"] * frames
     roofline_hbm = {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm_peak, "unit": "GB/s",
                     "frac": achieved_gbs / hbm_peak, "traffic": traffic, "algorithmic_bytes": alg_bytes,
                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6.65 TB/s"}
@@ -359,6 +364,7 @@ def run_ours(args, cfg, c):
             roofline_alu = {"bound": "alu", "achieved": achieved_alu, "peak": alu_peak, "unit": "Tops/s",
                             "frac": achieved_alu / alu_peak, "traffic": traffic,
                             "ops_per_frame": ops_per_frame,
+                            "ncu_issue_active_pct": ncu_ev and ncu_ev["issue_active_pct"],
                             "peak_source": "148 SM x 128 lanes x sm_max_mhz (MEASURED_PEAKS.json)"}
             roofline = roofline_alu if roofline_alu["frac"] > roofline_hbm["frac"] else roofline_hbm
             roofline_other = roofline_hbm if roofline is roofline_alu else roofline_alu
