@@ -380,7 +380,7 @@ static int decode_host_impl(polar_scs_t h, bool list, const float *llr_host, int
     const int N = h->t.N, K = h->t.K;
     cudaError_t e = cudaSuccess;
     if (!h->s_comp[0]) {
-        // chunks of about 256 MiB of LLRs, double-buffered; consecutive chunks
+        // chunks of up to 256 MiB of LLRs, double-buffered; consecutive chunks
         // decode on two streams with separate queue/arena slots, so the next
         // chunk's CTAs fill the SMs while the previous chunk's last frames finish
         h->stage_frames = std::max<int64_t>(1, (int64_t)(256ll << 20) / (4ll * N));
@@ -405,9 +405,12 @@ static int decode_host_impl(polar_scs_t h, bool list, const float *llr_host, int
     cudaStreamWaitEvent(h->s_comp[1], start, 0);
     int rc = POLAR_OK;
     int64_t i = 0;
-    for (int64_t off = 0; off < n && rc == POLAR_OK; off += h->stage_frames, i++) {
+    // chunk sizes ramp up geometrically from ~16 MiB, so the first decode
+    // starts after a short copy, to the staging size
+    int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(h->stage_frames, (int64_t)(16ll << 20) / (4ll * N)));
+    for (int64_t off = 0; off < n && rc == POLAR_OK; off += chunk, chunk = std::min<int64_t>(2 * chunk, h->stage_frames), i++) {
         const int b = (int)(i & 1);
-        const int64_t cnt = std::min<int64_t>(h->stage_frames, n - off);
+        const int64_t cnt = std::min<int64_t>(chunk, n - off);
         cudaStreamWaitEvent(h->s_h2d, h->ev_dec[b], 0);       // buffer b's previous decode has read it
         e = cudaMemcpyAsync(h->d_stage_llr[b], llr_host + off * N, (size_t)cnt * N * 4, cudaMemcpyHostToDevice, h->s_h2d);
         if (e != cudaSuccess) { rc = cuda_status(e); break; }
