@@ -46,7 +46,8 @@ def parse():
     ap.add_argument("--frames", type=int, default=0, help="override frames per Eb/N0 point")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
-    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--cpu-seconds", type=float, default=15.0,
+                    help="oracle sample length (s) of the cpu_baseline; with --impl reference, per timed step")
     ap.add_argument("--snap-global", action="store_true")
     ap.add_argument("--snap-smem", action="store_true")
     ap.add_argument("--chan-global", action="store_true")
@@ -196,6 +197,8 @@ def run_reference(args, cfg, c):
         return
     # each timed "step" is a bounded sample; the whole run stays within minutes
     per_step_s = max(2.0, min(20.0, 150.0 / max(1, args.steps + args.warmup)))
+    if args.cpu_seconds != 15.0:
+        per_step_s = args.cpu_seconds
     for _ in range(args.warmup):
         oracle_sample(cfg, c, per_step_s / 4)
     vals = [oracle_sample(cfg, c, per_step_s) for _ in range(args.steps)]
