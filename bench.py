@@ -358,10 +358,11 @@ def run_ours(args, cfg, c):
     # a sample of the same workload, scaled to the batch; peak = 148 SMs x 128
     # FP32/INT lanes x max SM clock
     roofline = roofline_hbm
+    roofline_smem = None
     cpu = None
     if rank == 0:
         try:
-            ops_per_frame = oracle_ops_per_frame(c, npts)
+            ops_per_frame, smem_bytes_per_frame = oracle_ops_per_frame(c, npts)
             alu_peak = 148 * 128 * sm_max * 1e6 / 1e12       # Tops/s
             achieved_alu = ops_per_frame * frames / kern_s / 1e12
             roofline_alu = {"bound": "alu", "achieved": achieved_alu, "peak": alu_peak, "unit": "Tops/s",
@@ -371,6 +372,13 @@ def run_ours(args, cfg, c):
                             "peak_source": "148 SM x 128 lanes x sm_max_mhz (MEASURED_PEAKS.json)"}
             roofline = roofline_alu if roofline_alu["frac"] > roofline_hbm["frac"] else roofline_hbm
             roofline_other = roofline_hbm if roofline is roofline_alu else roofline_alu
+            # shared-memory roofline: 12 B per f/g (two loads, one
+            # store) + 4 B per node element, against 148 SM x 128 B/clk
+            smem_alg = smem_bytes_per_frame * frames
+            smem_peak = 148 * 128 * sm_max * 1e6 / 1e9                  # GB/s
+            roofline_smem = {"bound": "smem", "achieved": smem_alg / kern_s / 1e9, "peak": smem_peak,
+                             "unit": "GB/s", "frac": smem_alg / kern_s / 1e9 / smem_peak,
+                             "bytes_per_frame": smem_bytes_per_frame}
         except Exception as e:  # noqa: BLE001
             roofline_other = {"error": str(e)}
         if not args.no_cpu:
@@ -403,6 +411,8 @@ def run_ours(args, cfg, c):
     }
     if rank == 0:
         res["roofline_other"] = roofline_other
+        res["roofline_smem"] = roofline_smem
+        res["ncu_evidence"] = ncu_ev
         res["cpu_baseline"] = cpu
         print(json.dumps(res), flush=True)
     if dist is not None:
@@ -423,13 +433,14 @@ def oracle_ops_per_frame(c, npts, n_sample=64):
     pay = ig.payload_bits(c["seed"], 0, n_sample, c["K"] - cc)
     nz = ig.unit_normals(c["seed"], 0, n_sample, c["N"])
     cw = O.encode_systematic(fr, O.crc_attach(pay, c["crc_poly"]))
-    tot = 0
+    tot = smem = 0
     for eb in c["ebno"]:
         r = dec.decode(O.awgn_llr(cw, nz, eb, c["K"] / c["N"]), counters=True, threads=os.cpu_count() or 1)
         ct = r["counters"]
         tot += (ct["f_ops"] + ct["g_ops"] + ct["node_elems"] + ct["beta_xor_bits"]
                 + (ct["sel_compares"] if c.get("list") else ct["key_compares"]))
-    return tot / (n_sample * npts)
+        smem += 12 * (ct["f_ops"] + ct["g_ops"]) + 4 * ct["node_elems"]
+    return tot / (n_sample * npts), smem / (n_sample * npts)
 
 
 def main():
