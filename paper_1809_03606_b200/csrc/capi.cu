@@ -113,7 +113,7 @@ int list_packed_layout(ListParams &p) {
     p.o_warp0 = round4(p.M);
     int o = 0;
     if (p.M == 1) p.sg = p.n;                 // the root node uses the alpha area as scratch
-    p.o_alpha = o; o += round4(std::max(L * ((1 << p.sg) - 1), p.M == 1 ? N : 0));
+    p.o_alpha = o; o += round4(std::max(L * ((1 << p.sg) - 1) + 6, p.M == 1 ? N : 0));   // + stage padding
     p.gstride = (size_t)L * (size_t)(N - (1 << p.sg));
     p.o_beta = o;  o += round4(2 * L * p.nw);
     p.o_clist = o; o += round4(L);

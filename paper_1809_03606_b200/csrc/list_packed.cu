@@ -51,7 +51,7 @@ __device__ __forceinline__ float flip_dpm(uint32_t m, const float (&A)[4]) {
 }  // namespace
 
 template <int NL>
-__global__ void __launch_bounds__(kListPackedWarps * 32) fsscl_packed_kernel(const ListParams P) {
+__global__ void __launch_bounds__(kListPackedWarps * 32, 8) fsscl_packed_kernel(const ListParams P) {
     extern __shared__ __align__(16) uint32_t smem[];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
@@ -76,9 +76,12 @@ __global__ void __launch_bounds__(kListPackedWarps * 32) fsscl_packed_kernel(con
     // stages >= sg live in a per-warp global arena (L2), the rest in shared memory
     const int sg = P.sg;
     float *garena = P.galpha ? P.galpha + (size_t)(blockIdx.x * P.pwarps + warp) * P.gstride : nullptr;
+    // shared stage s starts at L (2^s - 1) plus padding that keeps stages >= 2
+    // 16-byte aligned (stage 0 takes round4(L), stage 1 round4(2L) floats)
+    const int pad1 = ((L + 3) & ~3) - L, pad2 = pad1 + ((2 * L + 3) & ~3) - 2 * L;
     auto stage_buf = [&](int s, int k) -> float * {
         if (s >= sg) return garena + (size_t)L * ((1 << s) - (1 << sg)) + (size_t)k * (1 << s);
-        return abuf + (size_t)L * ((1 << s) - 1) + (size_t)k * (1 << s);
+        return abuf + (size_t)L * ((1 << s) - 1) + (s >= 2 ? pad2 : (s == 1 ? pad1 : 0)) + (size_t)k * (1 << s);
     };
     auto beta_of = [&](int par, int k) -> uint32_t * { return betaA + (size_t)(par * L + k) * nw; };
 
@@ -169,6 +172,37 @@ __global__ void __launch_bounds__(kListPackedWarps * 32) fsscl_packed_kernel(con
                 float *dst = stage_buf(s, 0);
                 const float *sb = top ? chan : stage_buf(s + 1, 0);
                 const uint32_t *bpar = betaA + (size_t)par * L * nw;
+                if (Ls >= 64) {
+                    // four consecutive elements of one path per lane (float4; the
+                    // beta bits of a g sit in one word)
+                    #pragma unroll 1
+                    for (int idx = lane * 4; idx < tot; idx += 128) {
+                        const int k = idx >> s, i = idx & (Ls - 1);
+                        float4 lo, hi;
+                        if (top) {
+                            lo = __ldg(reinterpret_cast<const float4 *>(chan + i));
+                            hi = __ldg(reinterpret_cast<const float4 *>(chan + Ls + i));
+                        } else {
+                            const int kb = first ? prow5(prow_s[par * L + k], s + 1) : k;
+                            const float *src = sb + (kb << (s + 1)) + i;
+                            lo = *reinterpret_cast<const float4 *>(src);
+                            hi = *reinterpret_cast<const float4 *>(src + Ls);
+                        }
+                        float4 v;
+                        if (odd) {
+                            const int bp = boff + i;
+                            const uint32_t b = bpar[k * nw + (bp >> 5)] >> (bp & 31);
+                            v.x = g_exact(lo.x, hi.x, b & 1u); v.y = g_exact(lo.y, hi.y, (b >> 1) & 1u);
+                            v.z = g_exact(lo.z, hi.z, (b >> 2) & 1u); v.w = g_exact(lo.w, hi.w, (b >> 3) & 1u);
+                        } else {
+                            v.x = f_minsum(lo.x, hi.x); v.y = f_minsum(lo.y, hi.y);
+                            v.z = f_minsum(lo.z, hi.z); v.w = f_minsum(lo.w, hi.w);
+                        }
+                        *reinterpret_cast<float4 *>(dst + idx) = v;
+                    }
+                    __syncwarp();
+                    continue;
+                }
                 #pragma unroll 1
                 for (int idx = lane; idx < tot; idx += 32) {
                     const int k = idx >> s, i = idx & (Ls - 1);
