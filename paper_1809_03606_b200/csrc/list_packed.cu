@@ -172,7 +172,7 @@ __global__ void __launch_bounds__(kListPackedWarps * 32, 8) fsscl_packed_kernel(
                 float *dst = stage_buf(s, 0);
                 const float *sb = top ? chan : stage_buf(s + 1, 0);
                 const uint32_t *bpar = betaA + (size_t)par * L * nw;
-                if (Ls >= 64) {
+                if (Ls >= 4) {
                     // four consecutive elements of one path per lane (float4; the
                     // beta bits of a g sit in one word)
                     #pragma unroll 1
