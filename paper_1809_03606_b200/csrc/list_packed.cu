@@ -244,12 +244,13 @@ __global__ void __launch_bounds__(kListPackedWarps * 32, 8) fsscl_packed_kernel(
                 // lane groups of Lambda lanes, one path per group
                 const int G = 32 >> lam;
                 const int i = lane & (Lam - 1);
+                const float *nb = (lam == n) ? chan : stage_buf(lam, 0);   // path k at nb[(k << lam) + i]
                 #pragma unroll 1
                 for (int k0 = 0; k0 < nL; k0 += G) {
                     const int k = k0 + (lane >> lam);
                     const bool valid = k < nL;
                     float xr = 0.f;
-                    if (valid) xr = (lam == n) ? __ldg(chan + i) : stage_buf(lam, k)[i];
+                    if (valid) xr = (lam == n) ? __ldg(chan + i) : nb[(k << lam) + i];
                     const bool leader = valid && i == 0;
                     if (sum_kind) {
                         float vn = negpart(xr), vp = pospart(xr);
@@ -290,14 +291,14 @@ __global__ void __launch_bounds__(kListPackedWarps * 32, 8) fsscl_packed_kernel(
 #pragma unroll
                         for (int q = 0; q < 4; q++) {
                             if (q < need) {
-                                // segmented argmin of (|alpha| bits, index) in the group
-                                uint32_t mk = key, mx = (uint32_t)i;
+                                // segmented argmin of (|alpha| bits, index) in the group:
+                                // the group minimum by shuffles, the lowest lane holding it
+                                // by one ballot (lowest index wins ties, reading R4)
+                                uint32_t mk = key;
                                 #pragma unroll 1
-                                for (int off = 1; off < Lam; off <<= 1) {
-                                    const uint32_t ok2 = __shfl_xor_sync(FULL, mk, off);
-                                    const uint32_t ox = __shfl_xor_sync(FULL, mx, off);
-                                    if (ok2 < mk || (ok2 == mk && ox < mx)) { mk = ok2; mx = ox; }
-                                }
+                                for (int off = 1; off < Lam; off <<= 1) mk = min(mk, __shfl_xor_sync(FULL, mk, off));
+                                const uint32_t eqb = (__ballot_sync(FULL, key == mk) >> (lane & ~(Lam - 1) & 31)) & lm;
+                                const uint32_t mx = (uint32_t)(__ffs(eqb) - 1);
                                 m[q] = mx;
                                 A[q] = __uint_as_float(mk);
                                 if ((uint32_t)i == mx) key = 0xFFFFFFFFu;
@@ -450,9 +451,12 @@ __global__ void __launch_bounds__(kListPackedWarps * 32, 8) fsscl_packed_kernel(
             // ---- rank r takes its parent's beta prefix, flips and pointer row
             const int npl = (phi + 1) << lam;
             const int nwp = (npl + 31) >> 5;
+            const uint32_t magic = (uint32_t)((0x100000000ull + (uint64_t)nwp - 1) / (uint64_t)nwp);
             #pragma unroll 1
             for (int idx = lane; idx < nL2 * nwp; idx += 32) {
-                const int r = idx / nwp, q = idx - r * nwp;
+                // idx / nwp by a reciprocal multiply (exact for idx <= 4096, nwp <= 128;
+                // nwp = 1 has no 32-bit reciprocal)
+                const int r = (nwp == 1) ? idx : (int)__umulhi((uint32_t)idx, magic), q = idx - r * nwp;
                 beta_of(npar, r)[q] = beta_of(par, (int)(sel_s[r] >> 3))[q];
             }
             __syncwarp();
