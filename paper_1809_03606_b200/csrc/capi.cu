@@ -44,7 +44,7 @@ int round4(int w) { return (w + 3) & ~3; }
 void free_handle(polar_scs_t h) {
     if (!h) return;
     cudaFree(h->t.nodes); cudaFree(h->t.info); cudaFree(h->t.crc_tab); cudaFree(h->t.crc_bytes); cudaFree(h->t.info_words);
-    cudaFree(h->d_queue); cudaFree(h->d_snap); cudaFree(h->d_keys); cudaFree(h->d_jsm); cudaFree(h->d_hdr); cudaFree(h->d_galpha);
+    cudaFree(h->d_queue); cudaFree(h->d_snap); cudaFree(h->d_keys); cudaFree(h->d_jsm); cudaFree(h->d_hdr); cudaFree(h->d_galpha); cudaFree(h->d_salpha);
     for (int b = 0; b < 2; b++) {
         cudaFree(h->d_stage_llr[b]); cudaFree(h->d_stage_bits[b]);
         if (h->ev_h2d[b]) cudaEventDestroy(h->ev_h2d[b]);
@@ -81,6 +81,7 @@ int decode_impl(polar_scs_t h, const float *llr, int64_t n, uint8_t *bits, float
     p.pm = pm; p.pops = pops; p.switches = sw; p.status = status;
     p.queue = h->d_queue + slot;
     if (h->d_snap) p.snap_global = h->d_snap + (h->snap_bytes / 4) * (size_t)slot;
+    if (h->d_salpha) p.galpha = h->d_salpha + h->salpha_floats * (size_t)slot;
     if (h->d_keys) { p.stack_keys = h->d_keys + h->stack_count * (size_t)slot; p.stack_jsm = h->d_jsm + h->stack_count * (size_t)slot; }
     if (h->d_hdr) p.hdr_global = h->d_hdr + h->hdr_count * (size_t)slot;
     cudaError_t e = cudaMemsetAsync(p.queue, 0, sizeof(unsigned long long), st);
@@ -223,8 +224,15 @@ int polar_scs_create_ex(polar_scs_t *out, int32_t N, int32_t K, const uint8_t *f
     // channel row and the snapshot arena go to shared memory or L1/L2.  Among
     // the allowed placements take the one with the most resident warps per SM;
     // ties prefer shared memory.
-    int best_occ = -1, best_smem = 0, best_ww = 0;
+    int best_occ = -1, best_smem = 0, best_ww = 0, best_gst = 0;
     bool best_snap = false, best_chan = false;
+    // alpha stages >= n - gst may move to a global (L2) arena; the fewest such
+    // stages that reach the best occupancy win (the root-node code keeps its
+    // shared scratch)
+    // (only the specialised N = 4096 kernel is built with the arena: measured
+    // +12% on C5 from 3 to 4 CTAs/SM; a run-time arena cost C2 5%)
+    const int gst_max = (t.M == 1 || t.n != 12 || slots != 4) ? 0 : 2;
+    for (int gst = 0; gst <= gst_max; gst++)
     for (int ci = 0; ci < 2; ci++) {
         const bool chan_smem = (ci == 0);
         if (chan_smem && (flags & POLAR_FLAG_CHAN_GLOBAL)) continue;
@@ -234,7 +242,9 @@ int polar_scs_create_ex(polar_scs_t *out, int32_t N, int32_t K, const uint8_t *f
             if (snap_smem && (flags & POLAR_FLAG_SNAP_GLOBAL)) continue;
             if (snap_smem && slots == 0) continue;          // D > 128: the arena is global
             if (!snap_smem && (flags & POLAR_FLAG_SNAP_SMEM)) continue;
-            const int ww = round4(p.win_words + (chan_smem ? N : 0) + N + 2 * nw + cnt_words + p.hdr_words + p.used_words +
+            if (gst > 0 && (snap_smem || chan_smem)) continue;  // only the GA kernel has the arena
+            const int aw = gst ? (1 << (t.n - gst)) : N;
+            const int ww = round4(p.win_words + (chan_smem ? N : 0) + aw + 2 * nw + cnt_words + p.hdr_words + p.used_words +
                                   p.uhat_words +
                                   (snap_smem ? D * sstride : 0));
             const int smem = 4 * (sched_words + kDecodeWarps * ww);
@@ -243,6 +253,7 @@ int polar_scs_create_ex(polar_scs_t *out, int32_t N, int32_t K, const uint8_t *f
             if (decode_occupancy(t.n, slots, snap_smem, chan_smem, smem, &occ) != cudaSuccess || occ < 1) continue;
             if (occ > best_occ) {
                 best_occ = occ; best_smem = smem; best_ww = ww; best_snap = snap_smem; best_chan = chan_smem;
+                best_gst = gst;
             }
         }
     }
@@ -251,6 +262,8 @@ int polar_scs_create_ex(polar_scs_t *out, int32_t N, int32_t K, const uint8_t *f
     const int occ = best_occ;
     const bool use_smem = best_snap;
     p.warp_words = best_ww;
+    p.sg = t.n - best_gst;
+    p.alpha_words = best_gst ? (1 << p.sg) : N;
     h->smem_per_cta = best_smem;
     h->chan_in_smem = best_chan ? 1 : 0;
     cudaGetLastError();
@@ -262,6 +275,12 @@ int polar_scs_create_ex(polar_scs_t *out, int32_t N, int32_t K, const uint8_t *f
         e = cudaMalloc(&h->d_snap, 2 * h->snap_bytes);
         if (e != cudaSuccess) { free_handle(h); return cuda_status(e); }
         p.snap_global = h->d_snap;
+    }
+    if (best_gst > 0) {
+        h->salpha_floats = (size_t)h->ctas * kDecodeWarps * (size_t)N;
+        e = cudaMalloc(&h->d_salpha, 2 * h->salpha_floats * sizeof(float));
+        if (e != cudaSuccess) { free_handle(h); return cuda_status(e); }
+        p.galpha = h->d_salpha;
     }
     if (slots == 0) {
         const size_t warps = (size_t)h->ctas * kDecodeWarps;

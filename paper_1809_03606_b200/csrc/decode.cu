@@ -40,13 +40,12 @@ __device__ __forceinline__ float ld1(const float *p, bool top) {
     return *p;
 }
 
+// src: stage s+1 (or the channel row when s+1 == n); dst: stage s
 template <bool CHAN_SMEM>
-__device__ __forceinline__ void alpha_stage(const float *chan, float *alpha, const uint32_t *beta,
+__device__ __forceinline__ void alpha_stage(const float *src, float *dst, const uint32_t *beta,
                                             int n, int s, int psi, int lane) {
     const int Ls = 1 << s;
     const bool top = (s + 1 == n);
-    const float *src = top ? chan : alpha + (2 << s);
-    float *dst = alpha + Ls;
     const bool odd = (psi & 1) != 0;
     const int boff = (psi - 1) << s;                 // left sibling's segment of the flat beta
     if (Ls == 64) {
@@ -229,7 +228,7 @@ __device__ __forceinline__ int alloc_snapshot_big(uint32_t *used, int &uhint, co
 // SLOTS = 1, 2, 4: register stack of 32 SLOTS entries (D <= 128).  SLOTS = 0:
 // global stack (D up to 8192, the paper's D = NL): dense unsorted arrays per
 // warp in global memory (L2-resident in practice), scanned by the 32 lanes.
-template <int SLOTS, bool SNAP_SMEM, bool CHAN_SMEM, int NL = 0>
+template <int SLOTS, bool SNAP_SMEM, bool CHAN_SMEM, int NL = 0, bool GA = false>
 __global__ void __launch_bounds__(kDecodeWarps * 32, SLOTS == 4 ? 3 : (SLOTS == 2 ? 5 : kDecodeMinBlocks))
 fsscs_decode_kernel(const DecodeParams P) {
     constexpr bool BIG = (SLOTS == 0);
@@ -258,7 +257,15 @@ fsscs_decode_kernel(const DecodeParams P) {
     unsigned long long *wkey = reinterpret_cast<unsigned long long *>(wb);
     float *chan_s = reinterpret_cast<float *>(wb + P.win_words);   // channel row (CHAN_SMEM)
     float *alpha = CHAN_SMEM ? chan_s + N : chan_s;                // stages >= 6 (+ scratch)
-    uint32_t *beta = reinterpret_cast<uint32_t *>(alpha + N);
+    uint32_t *beta = reinterpret_cast<uint32_t *>(alpha + P.alpha_words);
+    // stage t lives at [2^t, 2^{t+1}) of the shared alpha memory, or of this
+    // warp's global (L2) arena for t >= sg (sg = n: everything in shared memory)
+    const int sg = P.sg;
+    float *galpha = P.galpha ? P.galpha + (size_t)(blockIdx.x * kDecodeWarps + warp) * (size_t)N : alpha;
+    auto SP = [&](int t) -> float * {
+        if constexpr (GA) return (t >= sg ? galpha : alpha) + (1 << t);
+        return alpha + (1 << t);
+    };
     uint32_t *best = beta + nw;
     uint16_t *cnt = reinterpret_cast<uint16_t *>(best + nw);
     uint32_t *shdr = best + nw + P.cnt_words;                      // fork headers m1..m4, 2 words/slot (!BIG)
@@ -649,7 +656,7 @@ fsscs_decode_kernel(const DecodeParams P) {
 #define POLAR_SSTAGE(T)                                                                       \
     if constexpr ((T) < NL && (T) >= 6) {                                                     \
         if ((T) < lam) break;                                                                 \
-        alpha_stage<CHAN_SMEM>(chan, alpha, beta, n, (T), pl >> (T), lane);                   \
+        alpha_stage<CHAN_SMEM>((T) + 1 == n ? chan : SP((T) + 1), SP(T), beta, n, (T), pl >> (T), lane); \
     }
                     switch (s_hi) {
                     case 12: POLAR_SSTAGE(12)
@@ -664,7 +671,8 @@ fsscs_decode_kernel(const DecodeParams P) {
 #undef POLAR_SSTAGE
                 } else {
                     #pragma unroll 1
-                    for (int s = s_hi; s >= max(lam, 6); s--) alpha_stage<CHAN_SMEM>(chan, alpha, beta, n, s, pl >> s, lane);
+                    for (int s = s_hi; s >= max(lam, 6); s--)
+                        alpha_stage<CHAN_SMEM>(s + 1 == n ? chan : SP(s + 1), SP(s), beta, n, s, pl >> s, lane);
                 }
                 // register stages (Lambda <= 32): lo = element i, hi = element i + Lambda
                 // by shuffle; enter the cascade at the first stage to compute, leave
@@ -677,8 +685,8 @@ fsscs_decode_kernel(const DecodeParams P) {
             lo = ld1<CHAN_SMEM>(chan + (lane & (Lt - 1)), true);                            \
             hi = ld1<CHAN_SMEM>(chan + Lt + (lane & (Lt - 1)), true);                       \
         } else if ((T) == 5) {                                                             \
-            lo = alpha[64 + lane];                                                         \
-            hi = alpha[96 + lane];                                                         \
+            lo = SP(6)[lane];                                                              \
+            hi = SP(6)[32 + lane];                                                         \
         } else {                                                                           \
             lo = r[((T) + 1) % 6];                                                         \
             hi = __shfl_down_sync(FULL, r[((T) + 1) % 6], Lt);                              \
@@ -713,7 +721,7 @@ fsscs_decode_kernel(const DecodeParams P) {
             // ---- decision node ----------
             const int Lam = 1 << lam;
             const int seg = phi << lam;
-            float *a = alpha + Lam;           // node alpha in shared memory (Lambda > 32)
+            float *a = SP(lam);               // node alpha (Lambda > 32)
             if (Lam <= 32) {
                 if (lam == n) xr = ld1<CHAN_SMEM>(chan + (lane & (Lam - 1)), true);
                 if (lane >= Lam) xr = 0.f;
@@ -1024,9 +1032,9 @@ fsscs_decode_kernel(const DecodeParams P) {
     }
 }
 
-template <int SLOTS, bool SM, bool CS, int NL = 0>
+template <int SLOTS, bool SM, bool CS, int NL = 0, bool GA = false>
 static cudaError_t launch_t(const DecodeParams &p, int ctas, int smem, cudaStream_t st) {
-    auto kern = fsscs_decode_kernel<SLOTS, SM, CS, NL>;
+    auto kern = fsscs_decode_kernel<SLOTS, SM, CS, NL, GA>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     kern<<<ctas, kDecodeWarps * 32, smem, st>>>(p);
@@ -1042,7 +1050,8 @@ static cudaError_t launch_s(const DecodeParams &p, int slots, int ctas, int smem
 }
 
 // code-length-specialised instantiations: the BASELINE configs in the
-// placements create() picks for them
+// placements create() picks for them (n = 12 with the top alpha stage(s) in a
+// global arena when that raises the occupancy: GA)
 int specialised_nl(int n, int slots, bool snap_smem, bool chan_smem) {
     if (n == 7 && slots == 1 && snap_smem && chan_smem) return 7;
     if (n == 10 && slots == 1 && !snap_smem && !chan_smem) return 10;
@@ -1058,7 +1067,7 @@ cudaError_t launch_decode(const DecodeParams &p, int slots, bool snap_smem, bool
     case 7: return launch_t<1, true, true, 7>(p, ctas, smem, st);
     case 10: return launch_t<1, false, false, 10>(p, ctas, smem, st);
     case 11: return launch_t<2, false, false, 11>(p, ctas, smem, st);
-    case 12: return launch_t<4, false, false, 12>(p, ctas, smem, st);
+    case 12: return launch_t<4, false, false, 12, true>(p, ctas, smem, st);
     case 100: return launch_t<0, false, false, 10>(p, ctas, smem, st);
     default: break;
     }
@@ -1066,11 +1075,11 @@ cudaError_t launch_decode(const DecodeParams &p, int slots, bool snap_smem, bool
     return chan_smem ? launch_s<false, true>(p, slots, ctas, smem, st) : launch_s<false, false>(p, slots, ctas, smem, st);
 }
 
-template <int S, bool B, bool C, int NL = 0>
+template <int S, bool B, bool C, int NL = 0, bool GA = false>
 static cudaError_t occ_t(int smem, int *blocks) {
-    cudaError_t e = cudaFuncSetAttribute(fsscs_decode_kernel<S, B, C, NL>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaError_t e = cudaFuncSetAttribute(fsscs_decode_kernel<S, B, C, NL, GA>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, fsscs_decode_kernel<S, B, C, NL>, kDecodeWarps * 32, smem);
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, fsscs_decode_kernel<S, B, C, NL, GA>, kDecodeWarps * 32, smem);
 }
 template <bool B, bool C>
 static cudaError_t occ_s(int slots, int smem, int *blocks) {
@@ -1085,7 +1094,7 @@ cudaError_t decode_occupancy(int n, int slots, bool snap_smem, bool chan_smem, i
     case 7: return occ_t<1, true, true, 7>(smem, blocks_per_sm);
     case 10: return occ_t<1, false, false, 10>(smem, blocks_per_sm);
     case 11: return occ_t<2, false, false, 11>(smem, blocks_per_sm);
-    case 12: return occ_t<4, false, false, 12>(smem, blocks_per_sm);
+    case 12: return occ_t<4, false, false, 12, true>(smem, blocks_per_sm);
     case 100: return occ_t<0, false, false, 10>(smem, blocks_per_sm);
     default: break;
     }

@@ -64,6 +64,9 @@ struct DecodeParams {
     int used_words;             // snapshot-slot bitmap words: 4, or ceil(D/32) rounded (D > 128)
     int uhat_words;             // nw when non-systematic (u_hat scratch), else 0
     int win_words;              // D > 128: shared-memory window of the first 128 stack keys (256 words)
+    int alpha_words;            // shared alpha memory (floats): N, or 2^sg when stages >= sg are global
+    int sg;                     // first alpha stage kept in the global arena (n: none)
+    float *galpha;              // global alpha arena, N floats per resident warp (or null)
     int nonsys;                 // 1: read u_hat = x_hat F restricted to A (non-systematic)
 };
 
@@ -118,6 +121,8 @@ struct polar_scs_s {
     unsigned long long *d_keys = nullptr;   // global stacks (D > 128), 2 slots
     uint32_t *d_jsm = nullptr;
     uint2 *d_hdr = nullptr;         // global fork headers (D > 128), 2 slots
+    float *d_salpha = nullptr;      // global alpha arena of the top stages (stack decoder), 2 slots
+    size_t salpha_floats = 0;       // per slot
     size_t stack_count = 0, hdr_count = 0;   // entries per slot
     size_t snap_bytes = 0;          // bytes per slot
     int snap_in_smem = 0;
