@@ -229,9 +229,9 @@ int polar_scs_create_ex(polar_scs_t *out, int32_t N, int32_t K, const uint8_t *f
     // alpha stages >= n - gst may move to a global (L2) arena; the fewest such
     // stages that reach the best occupancy win (the root-node code keeps its
     // shared scratch)
-    // (only the specialised N = 4096 kernel is built with the arena: measured
-    // +12% on C5 from 3 to 4 CTAs/SM; a run-time arena cost C2 5%)
-    const int gst_max = (t.M == 1 || t.n != 12 || slots != 4) ? 0 : 2;
+    // (only the specialised N = 2048 / 4096 kernels are built with the arena:
+    // measured +10% on C4, +12% on C5; a run-time arena cost C2 5%)
+    const int gst_max = (t.M == 1 || !((t.n == 12 && slots == 4) || (t.n == 11 && slots == 2))) ? 0 : 2;
     for (int gst = 0; gst <= gst_max; gst++)
     for (int ci = 0; ci < 2; ci++) {
         const bool chan_smem = (ci == 0);

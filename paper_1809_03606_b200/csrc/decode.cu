@@ -225,11 +225,19 @@ __device__ __forceinline__ int alloc_snapshot_big(uint32_t *used, int &uhint, co
     return slot;
 }
 
+// launch bound (CTAs of 4 warps per SM) per instantiation: register stacks
+// of 2 or 4 entries per lane need more registers; the N = 2048 and N = 4096
+// specialisations trade registers for warps (measured)
+template <int SLOTS, int NL>
+constexpr int kDecodeMinBlocksFor() {
+    return NL == 11 ? 6 : (NL == 12 ? 5 : (SLOTS == 4 ? 3 : (SLOTS == 2 ? 5 : kDecodeMinBlocks)));
+}
+
 // SLOTS = 1, 2, 4: register stack of 32 SLOTS entries (D <= 128).  SLOTS = 0:
 // global stack (D up to 8192, the paper's D = NL): dense unsorted arrays per
 // warp in global memory (L2-resident in practice), scanned by the 32 lanes.
 template <int SLOTS, bool SNAP_SMEM, bool CHAN_SMEM, int NL = 0, bool GA = false>
-__global__ void __launch_bounds__(kDecodeWarps * 32, SLOTS == 4 ? 3 : (SLOTS == 2 ? 5 : kDecodeMinBlocks))
+__global__ void __launch_bounds__(kDecodeWarps * 32, kDecodeMinBlocksFor<SLOTS, NL>())
 fsscs_decode_kernel(const DecodeParams P) {
     constexpr bool BIG = (SLOTS == 0);
     constexpr int SL = BIG ? 1 : SLOTS;       // register arrays (unused when BIG)
@@ -1066,7 +1074,7 @@ cudaError_t launch_decode(const DecodeParams &p, int slots, bool snap_smem, bool
     switch (specialised_nl(p.n, slots, snap_smem, chan_smem)) {
     case 7: return launch_t<1, true, true, 7>(p, ctas, smem, st);
     case 10: return launch_t<1, false, false, 10>(p, ctas, smem, st);
-    case 11: return launch_t<2, false, false, 11>(p, ctas, smem, st);
+    case 11: return launch_t<2, false, false, 11, true>(p, ctas, smem, st);
     case 12: return launch_t<4, false, false, 12, true>(p, ctas, smem, st);
     case 100: return launch_t<0, false, false, 10>(p, ctas, smem, st);
     default: break;
@@ -1093,7 +1101,7 @@ cudaError_t decode_occupancy(int n, int slots, bool snap_smem, bool chan_smem, i
     switch (specialised_nl(n, slots, snap_smem, chan_smem)) {
     case 7: return occ_t<1, true, true, 7>(smem, blocks_per_sm);
     case 10: return occ_t<1, false, false, 10>(smem, blocks_per_sm);
-    case 11: return occ_t<2, false, false, 11>(smem, blocks_per_sm);
+    case 11: return occ_t<2, false, false, 11, true>(smem, blocks_per_sm);
     case 12: return occ_t<4, false, false, 12, true>(smem, blocks_per_sm);
     case 100: return occ_t<0, false, false, 10>(smem, blocks_per_sm);
     default: break;
