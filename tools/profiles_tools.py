@@ -1,4 +1,4 @@
-"""Helpers to summarise ncu reports (run here, no GPU): python profiles_tools.py <rep> [regions]"""
+"""Helpers to summarise ncu reports (run here, no GPU): python tools/profiles_tools.py <rep> [regions]"""
 import csv
 import subprocess
 import sys

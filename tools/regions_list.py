@@ -1,5 +1,5 @@
 import sys
-sys.path.insert(0, "/root/repo")
+sys.path.insert(0, __import__("os").path.dirname(__import__("os").path.abspath(__file__)))
 import profiles_tools as pt
 regions = [(1,100,"helpers"),(100,137,"setup/frame"),(137,171,"beta-climb"),(171,186,"alpha-smem"),(186,223,"alpha-reg"),(223,327,"node"),(327,365,"cand+c1"),(365,384,"publish"),(384,398,"prune"),(398,442,"transfer"),(442,500,"final")]
 agg, tot, totS, per_line = pt.source_regions(sys.argv[1], sys.argv[2], regions)

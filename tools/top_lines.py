@@ -1,7 +1,7 @@
 """Top source lines of an ncu report by instructions and by stall samples
 (python tools/top_lines.py rep.ncu-rep src_suffix [n])."""
 import sys
-sys.path.insert(0, __import__("os").path.dirname(__import__("os").path.dirname(__import__("os").path.abspath(__file__))))
+sys.path.insert(0, __import__("os").path.dirname(__import__("os").path.abspath(__file__)))
 import profiles_tools as pt
 
 rep, src = sys.argv[1], sys.argv[2]
