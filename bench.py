@@ -354,15 +354,15 @@ def run_ours(args, cfg, c):
     roofline_hbm = {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm_peak, "unit": "GB/s",
                     "frac": achieved_gbs / hbm_peak, "traffic": traffic, "algorithmic_bytes": alg_bytes,
                     "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6.65 TB/s"}
-    # ALU roofline: algorithmic lane-ops per frame counted by the oracle (O10) on
-    # a sample of the same workload, scaled to the batch; peak = 148 SMs x 128
-    # FP32/INT lanes x max SM clock
+    # ALU roofline: algorithmic lane-ops per frame (profiles/op_census.json,
+    # counted by the oracle's O10 counters on a sample of the same workload),
+    # scaled to the batch; peak = 148 SMs x 128 FP32/INT lanes x max SM clock
     roofline = roofline_hbm
     roofline_smem = None
     cpu = None
     if rank == 0:
         try:
-            ops_per_frame, smem_bytes_per_frame = oracle_ops_per_frame(c, npts)
+            ops_per_frame, smem_bytes_per_frame = census_per_frame(cfg, c)
             alu_peak = 148 * 128 * sm_max * 1e6 / 1e12       # Tops/s
             achieved_alu = ops_per_frame * frames / kern_s / 1e12
             roofline_alu = {"bound": "alu", "achieved": achieved_alu, "peak": alu_peak, "unit": "Tops/s",
@@ -420,27 +420,19 @@ def run_ours(args, cfg, c):
         dist.destroy_process_group()
 
 
-def oracle_ops_per_frame(c, npts, n_sample=64):
-    """Algorithmic lane-ops per frame (mean over a sample at every Eb/N0 point):
+def census_per_frame(cfg, c):
+    """Algorithmic lane-ops and shared-memory bytes per frame of this workload,
+    from profiles/op_census.json (written by tools/op_census.py from the
+    oracle's O10 counters on a sample of the same workload; the bench itself
+    never runs the oracle outside its cpu_baseline / reference legs):
     f/g evaluations (clean pass + spines) + node elements + BETA XOR bits +
-    stack key compares (the live entries examined by each linear search for
-    the best entry, and for the worst one, L599); for the list
-    decoder the last term is the prune's sort cost (T log2 T per node)."""
-    import oracle as O
-    fr = O.bhattacharyya_mask(c["N"], c["K"], c["design_db"])
-    dec = oracle_decoder(c)
-    cc = O.crc_degree(c["crc_poly"]) if c["crc_poly"] else 0
-    pay = ig.payload_bits(c["seed"], 0, n_sample, c["K"] - cc)
-    nz = ig.unit_normals(c["seed"], 0, n_sample, c["N"])
-    cw = O.encode_systematic(fr, O.crc_attach(pay, c["crc_poly"]))
-    tot = smem = 0
-    for eb in c["ebno"]:
-        r = dec.decode(O.awgn_llr(cw, nz, eb, c["K"] / c["N"]), counters=True, threads=os.cpu_count() or 1)
-        ct = r["counters"]
-        tot += (ct["f_ops"] + ct["g_ops"] + ct["node_elems"] + ct["beta_xor_bits"]
-                + (ct["sel_compares"] if c.get("list") else ct["key_compares"]))
-        smem += 12 * (ct["f_ops"] + ct["g_ops"]) + 4 * ct["node_elems"]
-    return tot / (n_sample * npts), smem / (n_sample * npts)
+    the live entries examined by the stack's linear searches (PAPER.md:L793,
+    L599), or the list prune's T log2 T; smem = 12 B per f/g + 4 B per node
+    element."""
+    key = cfg + ("_list" if c.get("list") else ("_bitlevel" if c.get("bit_level") else ""))
+    with open(os.path.join(ROOT, "profiles", "op_census.json")) as fh:
+        e = json.load(fh)["census"][key]
+    return e["ops_per_frame"], e["smem_bytes_per_frame"]
 
 
 def main():
