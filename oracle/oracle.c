@@ -7,7 +7,14 @@
  * It follows PAPER.md step by step, in the paper's order and notation
  * (lambda = stage, phi = branch, Lambda = 2^lambda, alpha = LLR memory,
  * beta = bit estimates).  Readings of silent/garbled passages: DESIGN.md
- * "Readings" R1..R19 (= SURVEY.md §8(c)).
+ * "Readings" R1..R26 (R1..R19 = SURVEY.md §8(c)).
+ *
+ * Pins (tests/test_oracle*.py): every part is checked against the paper's
+ * worked examples, closed forms, textbook SC, brute-force ML, the DFS optimum
+ * of the candidate tree, and (search counts, PM, bits) an independent plain
+ * SCS / SCL written in Python.  Parity unpinned: the Bhattacharyya set for
+ * N > 16 beyond its partial-order closure (an input both sides share), and
+ * the stack search counts for N > 64 (the pinned engine is the same code).
  *
  * Build: gcc -O2 -std=c11 -ffp-contract=off -fno-fast-math -fPIC -shared.
  */

@@ -10,7 +10,9 @@
  * Stack Decoding of Polar Codes", Aurora & Gross, arXiv:1809.03606); the
  * citation is PAPER.md:L<line> (section / equation / algorithm / figure).
  * Where the paper is silent or garbled the reading is the one listed in
- * SURVEY.md §8(c) and DESIGN.md "Readings" (R1..R19).
+ * SURVEY.md §8(c) and DESIGN.md "Readings" (R1..R26).  Parity unpinned (see
+ * oracle.c): Bhattacharyya sets for N > 16 beyond closure; search counts for
+ * N > 64.
  *
  * Arithmetic: alpha values and path metrics are IEEE float32 (PAPER.md:L968,
  * "alpha ... implemented using 32-bit floating point numbers"); the library is
