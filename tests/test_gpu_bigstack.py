@@ -53,10 +53,11 @@ def test_paper_workload_parity(ebno):
     (1024, 512, 160, 8, 0, False),      # C2 code just above the register stack
     (2048, 1024, 512, 16, 0, False),
     (16, 8, 8192, 256, 0, False),       # N = 16: sub-word beta, huge D
+    (4096, 3072, 300, 16, 0x107, False),  # N = 4096 with a global stack
 ])
 def test_global_stack_parity_edge(N, K, D, L, crc, bit_level):
     fr = P.bhattacharyya_mask(N, K, 2.0)
-    n = 257 if N <= 256 else 60
+    n = 257 if N <= 256 else (60 if N <= 2048 else 24)
     _run(fr, D, L, crc, (-1.0, 1.0, 3.0), n, N + K + D, bit_level=bit_level)
 
 

@@ -82,6 +82,7 @@ def test_list_parity_configs(cfg, L, ebnos, n, lk):
     (8, 4, 8, 0, False), (16, 8, 16, 0, False), (16, 16, 8, 0, False), (16, 1, 8, 0, False),
     (64, 64, 4, 0, False), (128, 1, 4, 0, False), (256, 255, 4, 0, False),
     (2048, 1024, 4, 0, False), (4096, 2048, 2, 0x11021, False),
+    (4096, 3072, 16, 0x107, False),  # packed kernel with most alpha stages in L2
 ])
 @pytest.mark.parametrize("lk", ["cta", "packed"])
 def test_list_parity_edge(N, K, L, crc, bit_level, lk):
