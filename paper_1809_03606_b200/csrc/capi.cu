@@ -14,7 +14,7 @@
 namespace polar {
 cudaError_t launch_decode(const DecodeParams &p, int slots, bool snap_smem, bool chan_smem, int ctas, int smem,
                           cudaStream_t st);
-cudaError_t decode_occupancy(int n, int slots, bool snap_smem, bool chan_smem, bool plain, int smem, int *blocks_per_sm);
+cudaError_t decode_occupancy(int n, int slots, bool snap_smem, bool chan_smem, int mode, int smem, int *blocks_per_sm);
 cudaError_t launch_list(const ListParams &p, int lcap, int ctas, int smem, cudaStream_t st);
 cudaError_t list_occupancy(int lcap, int n, int L, int smem, int *blocks_per_sm);
 cudaError_t launch_list_packed(const ListParams &p, int ctas, int smem, cudaStream_t st);
@@ -225,8 +225,9 @@ int polar_scs_create_ex(polar_scs_t *out, int32_t N, int32_t K, const uint8_t *f
     // the allowed placements take the one with the most resident warps per SM;
     // ties prefer shared memory.
     int best_occ = -1, best_smem = 0, best_ww = 0, best_gst = 0;
-    // no CRC, systematic, more than one node: the compact "plain" kernels
-    const bool plain = (t.c == 0 && !p.nonsys && t.M > 1);
+    // compile-time modes of the specialised kernels (decode.cu): 1 systematic
+    // with more than one node, 2 also without CRC
+    const int mode = (p.nonsys || t.M == 1) ? 0 : (t.c == 0 ? 2 : 1);
     bool best_snap = false, best_chan = false;
     // alpha stages >= n - gst may move to a global (L2) arena; the fewest such
     // stages that reach the best occupancy win (the root-node code keeps its
@@ -252,7 +253,7 @@ int polar_scs_create_ex(polar_scs_t *out, int32_t N, int32_t K, const uint8_t *f
             const int smem = 4 * (sched_words + kDecodeWarps * ww);
             if (smem > optin) continue;
             int occ = 0;
-            if (decode_occupancy(t.n, slots, snap_smem, chan_smem, plain, smem, &occ) != cudaSuccess || occ < 1) continue;
+            if (decode_occupancy(t.n, slots, snap_smem, chan_smem, mode, smem, &occ) != cudaSuccess || occ < 1) continue;
             if (occ > best_occ) {
                 best_occ = occ; best_smem = smem; best_ww = ww; best_snap = snap_smem; best_chan = chan_smem;
                 best_gst = gst;

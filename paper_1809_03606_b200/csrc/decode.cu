@@ -228,7 +228,7 @@ __device__ __forceinline__ int alloc_snapshot_big(uint32_t *used, int &uhint, co
 // launch bound (CTAs of 4 warps per SM) per instantiation: register stacks
 // of 2 or 4 entries per lane need more registers; the N = 2048 and N = 4096
 // specialisations trade registers for warps (measured)
-template <int SLOTS, int NL, bool PLAIN>
+template <int SLOTS, int NL, bool NOCRC>
 constexpr int kDecodeMinBlocksFor() {
     return NL == 11 ? 6 : (NL == 12 ? 5 : (SLOTS == 4 ? 3 : (SLOTS == 2 ? 5 : kDecodeMinBlocks)));
 }
@@ -236,10 +236,11 @@ constexpr int kDecodeMinBlocksFor() {
 // SLOTS = 1, 2, 4: register stack of 32 SLOTS entries (D <= 128).  SLOTS = 0:
 // global stack (D up to 8192, the paper's D = NL): dense unsorted arrays per
 // warp in global memory (L2-resident in practice), scanned by the 32 lanes.
-// PLAIN: compile-time "no CRC, systematic readout, more than one node" (the
-// CRC, re-encoding and whole-code-node paths are left out of the code)
-template <int SLOTS, bool SNAP_SMEM, bool CHAN_SMEM, int NL = 0, bool GA = false, bool PLAIN = false>
-__global__ void __launch_bounds__(kDecodeWarps * 32, kDecodeMinBlocksFor<SLOTS, NL, PLAIN>())
+// MODE (compile time): 0 general; 1 systematic readout and more than one node
+// (re-encoding and whole-code-node paths left out of the code); 2 as 1 and no
+// CRC (the CRC path left out too)
+template <int SLOTS, bool SNAP_SMEM, bool CHAN_SMEM, int NL = 0, bool GA = false, int MODE = 0>
+__global__ void __launch_bounds__(kDecodeWarps * 32, kDecodeMinBlocksFor<SLOTS, NL, MODE == 2>())
 fsscs_decode_kernel(const DecodeParams P) {
     constexpr bool BIG = (SLOTS == 0);
     constexpr int SL = BIG ? 1 : SLOTS;       // register arrays (unused when BIG)
@@ -605,11 +606,11 @@ fsscs_decode_kernel(const DecodeParams P) {
             if (j == M) {
                 // ---- complete path: CRC on the systematic bits
                 bool ok = true;
-                if (!PLAIN && P.c > 0) {
+                if (MODE < 2 && P.c > 0) {
                     // syndrome = XOR of the contributions of the set systematic bits,
                     // looked up per beta byte (tables hold information positions only)
                     const uint32_t *cw = beta;
-                    if (!PLAIN && P.nonsys) {
+                    if (MODE == 0 && P.nonsys) {
                         #pragma unroll 1
                         for (int w = lane; w < nw; w += 32) uhat[w] = beta[w];
                         __syncwarp();
@@ -733,9 +734,9 @@ fsscs_decode_kernel(const DecodeParams P) {
             const int seg = phi << lam;
             float *a = SP(lam);               // node alpha (Lambda > 32)
             if (Lam <= 32) {
-                if (!PLAIN && lam == n) xr = ld1<CHAN_SMEM>(chan + (lane & (Lam - 1)), true);
+                if (MODE == 0 && lam == n) xr = ld1<CHAN_SMEM>(chan + (lane & (Lam - 1)), true);
                 if (lane >= Lam) xr = 0.f;
-            } else if (!PLAIN && lam == n) {
+            } else if (MODE == 0 && lam == n) {
                 // whole code is one node: copy the channel so the sums can work in place
                 #pragma unroll 1
                 for (int i = lane; i < N; i += 32) alpha[i] = ld1<CHAN_SMEM>(chan + i, true);
@@ -1016,7 +1017,7 @@ fsscs_decode_kernel(const DecodeParams P) {
         // (non-systematic) restricted to A, ascending ---------
         {
             const uint32_t *bsrc = from_best ? best : beta;
-            if (!PLAIN && P.nonsys) {
+            if (MODE == 0 && P.nonsys) {
                 #pragma unroll 1
                 for (int w = lane; w < nw; w += 32) uhat[w] = bsrc[w];
                 __syncwarp();
@@ -1042,9 +1043,9 @@ fsscs_decode_kernel(const DecodeParams P) {
     }
 }
 
-template <int SLOTS, bool SM, bool CS, int NL = 0, bool GA = false, bool PLAIN = false>
+template <int SLOTS, bool SM, bool CS, int NL = 0, bool GA = false, int MODE = 0>
 static cudaError_t launch_t(const DecodeParams &p, int ctas, int smem, cudaStream_t st) {
-    auto kern = fsscs_decode_kernel<SLOTS, SM, CS, NL, GA, PLAIN>;
+    auto kern = fsscs_decode_kernel<SLOTS, SM, CS, NL, GA, MODE>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     kern<<<ctas, kDecodeWarps * 32, smem, st>>>(p);
@@ -1075,25 +1076,30 @@ cudaError_t launch_decode(const DecodeParams &p, int slots, bool snap_smem, bool
                           cudaStream_t st) {
     switch (specialised_nl(p.n, slots, snap_smem, chan_smem)) {
     case 7:
-        if (p.c == 0 && !p.nonsys && p.M > 1) return launch_t<1, true, true, 7, false, true>(p, ctas, smem, st);
+        if (p.c == 0 && !p.nonsys && p.M > 1) return launch_t<1, true, true, 7, false, 2>(p, ctas, smem, st);
         return launch_t<1, true, true, 7>(p, ctas, smem, st);
     case 10:
-        if (p.c == 0 && !p.nonsys && p.M > 1) return launch_t<1, false, false, 10, false, true>(p, ctas, smem, st);
+        if (p.c == 0 && !p.nonsys && p.M > 1) return launch_t<1, false, false, 10, false, 2>(p, ctas, smem, st);
+        if (!p.nonsys && p.M > 1) return launch_t<1, false, false, 10, false, 1>(p, ctas, smem, st);
         return launch_t<1, false, false, 10>(p, ctas, smem, st);
     case 11: return launch_t<2, false, false, 11, true>(p, ctas, smem, st);
-    case 12: return launch_t<4, false, false, 12, true>(p, ctas, smem, st);
-    case 100: return launch_t<0, false, false, 10>(p, ctas, smem, st);
+    case 12:
+        if (!p.nonsys && p.M > 1) return launch_t<4, false, false, 12, true, 1>(p, ctas, smem, st);
+        return launch_t<4, false, false, 12, true>(p, ctas, smem, st);
+    case 100:
+        if (!p.nonsys && p.M > 1) return launch_t<0, false, false, 10, false, 1>(p, ctas, smem, st);
+        return launch_t<0, false, false, 10>(p, ctas, smem, st);
     default: break;
     }
     if (snap_smem) return chan_smem ? launch_s<true, true>(p, slots, ctas, smem, st) : launch_s<true, false>(p, slots, ctas, smem, st);
     return chan_smem ? launch_s<false, true>(p, slots, ctas, smem, st) : launch_s<false, false>(p, slots, ctas, smem, st);
 }
 
-template <int S, bool B, bool C, int NL = 0, bool GA = false, bool PLAIN = false>
+template <int S, bool B, bool C, int NL = 0, bool GA = false, int MODE = 0>
 static cudaError_t occ_t(int smem, int *blocks) {
-    cudaError_t e = cudaFuncSetAttribute(fsscs_decode_kernel<S, B, C, NL, GA, PLAIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaError_t e = cudaFuncSetAttribute(fsscs_decode_kernel<S, B, C, NL, GA, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, fsscs_decode_kernel<S, B, C, NL, GA, PLAIN>, kDecodeWarps * 32, smem);
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, fsscs_decode_kernel<S, B, C, NL, GA, MODE>, kDecodeWarps * 32, smem);
 }
 template <bool B, bool C>
 static cudaError_t occ_s(int slots, int smem, int *blocks) {
@@ -1103,14 +1109,17 @@ static cudaError_t occ_s(int slots, int smem, int *blocks) {
     return occ_t<4, B, C>(smem, blocks);
 }
 
-cudaError_t decode_occupancy(int n, int slots, bool snap_smem, bool chan_smem, bool plain, int smem, int *blocks_per_sm) {
+cudaError_t decode_occupancy(int n, int slots, bool snap_smem, bool chan_smem, int mode, int smem, int *blocks_per_sm) {
     switch (specialised_nl(n, slots, snap_smem, chan_smem)) {
-    case 7: return plain ? occ_t<1, true, true, 7, false, true>(smem, blocks_per_sm) : occ_t<1, true, true, 7>(smem, blocks_per_sm);
-    case 10: return plain ? occ_t<1, false, false, 10, false, true>(smem, blocks_per_sm)
-                          : occ_t<1, false, false, 10>(smem, blocks_per_sm);
+    case 7: return mode == 2 ? occ_t<1, true, true, 7, false, 2>(smem, blocks_per_sm) : occ_t<1, true, true, 7>(smem, blocks_per_sm);
+    case 10: return mode == 2 ? occ_t<1, false, false, 10, false, 2>(smem, blocks_per_sm)
+                  : mode == 1 ? occ_t<1, false, false, 10, false, 1>(smem, blocks_per_sm)
+                              : occ_t<1, false, false, 10>(smem, blocks_per_sm);
     case 11: return occ_t<2, false, false, 11, true>(smem, blocks_per_sm);
-    case 12: return occ_t<4, false, false, 12, true>(smem, blocks_per_sm);
-    case 100: return occ_t<0, false, false, 10>(smem, blocks_per_sm);
+    case 12: return mode >= 1 ? occ_t<4, false, false, 12, true, 1>(smem, blocks_per_sm)
+                              : occ_t<4, false, false, 12, true>(smem, blocks_per_sm);
+    case 100: return mode >= 1 ? occ_t<0, false, false, 10, false, 1>(smem, blocks_per_sm)
+                               : occ_t<0, false, false, 10>(smem, blocks_per_sm);
     default: break;
     }
     if (snap_smem) return chan_smem ? occ_s<true, true>(slots, smem, blocks_per_sm) : occ_s<true, false>(slots, smem, blocks_per_sm);
