@@ -1082,7 +1082,9 @@ cudaError_t launch_decode(const DecodeParams &p, int slots, bool snap_smem, bool
         if (p.c == 0 && !p.nonsys && p.M > 1) return launch_t<1, false, false, 10, false, 2>(p, ctas, smem, st);
         if (!p.nonsys && p.M > 1) return launch_t<1, false, false, 10, false, 1>(p, ctas, smem, st);
         return launch_t<1, false, false, 10>(p, ctas, smem, st);
-    case 11: return launch_t<2, false, false, 11, true>(p, ctas, smem, st);
+    case 11:
+        if (!p.nonsys && p.M > 1) return launch_t<2, false, false, 11, true, 1>(p, ctas, smem, st);
+        return launch_t<2, false, false, 11, true>(p, ctas, smem, st);
     case 12:
         if (!p.nonsys && p.M > 1) return launch_t<4, false, false, 12, true, 1>(p, ctas, smem, st);
         return launch_t<4, false, false, 12, true>(p, ctas, smem, st);
@@ -1115,7 +1117,8 @@ cudaError_t decode_occupancy(int n, int slots, bool snap_smem, bool chan_smem, i
     case 10: return mode == 2 ? occ_t<1, false, false, 10, false, 2>(smem, blocks_per_sm)
                   : mode == 1 ? occ_t<1, false, false, 10, false, 1>(smem, blocks_per_sm)
                               : occ_t<1, false, false, 10>(smem, blocks_per_sm);
-    case 11: return occ_t<2, false, false, 11, true>(smem, blocks_per_sm);
+    case 11: return mode >= 1 ? occ_t<2, false, false, 11, true, 1>(smem, blocks_per_sm)
+                              : occ_t<2, false, false, 11, true>(smem, blocks_per_sm);
     case 12: return mode >= 1 ? occ_t<4, false, false, 12, true, 1>(smem, blocks_per_sm)
                               : occ_t<4, false, false, 12, true>(smem, blocks_per_sm);
     case 100: return mode >= 1 ? occ_t<0, false, false, 10, false, 1>(smem, blocks_per_sm)
