@@ -50,7 +50,9 @@ __device__ __forceinline__ float flip_dpm(uint32_t m, const float (&A)[4]) {
 
 }  // namespace
 
-template <int NL>
+// PLAIN: compile-time "no CRC, systematic, more than one node" (the final
+// CRC / re-encoding selection and the whole-code-node path left out)
+template <int NL, bool PLAIN = false>
 __global__ void __launch_bounds__(kListPackedWarps * 32, 8) fsscl_packed_kernel(const ListParams P) {
     extern __shared__ __align__(16) uint32_t smem[];
     const int lane = threadIdx.x & 31;
@@ -250,7 +252,7 @@ __global__ void __launch_bounds__(kListPackedWarps * 32, 8) fsscl_packed_kernel(
                     const int k = k0 + (lane >> lam);
                     const bool valid = k < nL;
                     float xr = 0.f;
-                    if (valid) xr = (lam == n) ? __ldg(chan + i) : nb[(k << lam) + i];
+                    if (valid) xr = (!PLAIN && lam == n) ? __ldg(chan + i) : nb[(k << lam) + i];
                     const bool leader = valid && i == 0;
                     if (sum_kind) {
                         float vn = negpart(xr), vp = pospart(xr);
@@ -332,8 +334,8 @@ __global__ void __launch_bounds__(kListPackedWarps * 32, 8) fsscl_packed_kernel(
                 // Lambda > 32: one path at a time, warp-wide (as the stack decoder)
                 #pragma unroll 1
                 for (int k = 0; k < nL; k++) {
-                    float *a = (lam == n) ? abuf : stage_buf(lam, k);
-                    if (lam == n) {
+                    float *a = (!PLAIN && lam == n) ? abuf : stage_buf(lam, k);
+                    if (!PLAIN && lam == n) {
                         #pragma unroll 1
                         for (int q = lane; q < N; q += 32) a[q] = __ldg(chan + q);
                         __syncwarp();
@@ -496,7 +498,7 @@ __global__ void __launch_bounds__(kListPackedWarps * 32, 8) fsscl_packed_kernel(
         // order whose block passes the CRC
         int pick = 0, status = 0;
         const uint32_t *pick_cw = beta_of(par, 0);
-        if (P.c > 0 || P.nonsys) {
+        if (!PLAIN && (P.c > 0 || P.nonsys)) {
             status = 1;
             #pragma unroll 1
             for (int k = 0; k < nL; k++) {
@@ -542,9 +544,9 @@ __global__ void __launch_bounds__(kListPackedWarps * 32, 8) fsscl_packed_kernel(
     }
 }
 
-template <int NL>
+template <int NL, bool PLAIN = false>
 static cudaError_t launch_packed_t(const ListParams &p, int ctas, int smem, cudaStream_t st) {
-    auto kern = fsscl_packed_kernel<NL>;
+    auto kern = fsscl_packed_kernel<NL, PLAIN>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     kern<<<ctas, p.pwarps * 32, smem, st>>>(p);
@@ -553,7 +555,8 @@ static cudaError_t launch_packed_t(const ListParams &p, int ctas, int smem, cuda
 
 cudaError_t launch_list_packed(const ListParams &p, int ctas, int smem, cudaStream_t st) {
     if (p.n == 7) return launch_packed_t<7>(p, ctas, smem, st);
-    if (p.n == 10) return launch_packed_t<10>(p, ctas, smem, st);
+    if (p.n == 10) return (p.c == 0 && !p.nonsys && p.M > 1) ? launch_packed_t<10, true>(p, ctas, smem, st)
+                                                               : launch_packed_t<10>(p, ctas, smem, st);
     return launch_packed_t<0>(p, ctas, smem, st);
 }
 
