@@ -106,3 +106,30 @@ def test_sequence_constructor_equals_oracle():
     m = np.zeros(8, np.uint8)
     assert P.polar_construct_from_sequence(8, 4, bad.ctypes.data, 8, m.ctypes.data) == P.POLAR_EINVAL
     assert P.polar_construct_from_sequence(8, 4, bad.ctypes.data, 7, m.ctypes.data) == P.POLAR_EINVAL
+
+
+def test_header_is_plain_c_and_example_links():
+    """include/polar_scs.h compiles as C99 and the plain-C example links
+    against libpolarscs.so (no Python, no torch types at the boundary)."""
+    import shutil
+    import subprocess
+    import tempfile
+    import paper_1809_03606_b200 as P
+    gcc = shutil.which("gcc")
+    if gcc is None:
+        pytest.skip("no gcc")
+    inc = os.path.join(ROOT, "include")
+    cuda_inc = "/usr/local/cuda/include"
+    with tempfile.TemporaryDirectory() as td:
+        src = os.path.join(td, "h.c")
+        with open(src, "w") as fh:
+            fh.write('#include "polar_scs.h"\nint main(void) { return polar_scs_strerror(0) == 0; }\n')
+        r = subprocess.run([gcc, "-std=c99", "-Wall", "-Werror", "-I" + inc, "-fsyntax-only", src],
+                           capture_output=True, text=True)
+        assert r.returncode == 0, r.stderr
+        exe = os.path.join(td, "decode_c")
+        libdir = os.path.dirname(P.library_path())
+        r = subprocess.run([gcc, "-std=c99", "-O1", os.path.join(ROOT, "examples", "decode_c.c"), "-I" + inc,
+                            "-I" + cuda_inc, "-L" + libdir, "-lpolarscs", "-L/usr/local/cuda/lib64", "-lcudart",
+                            "-o", exe], capture_output=True, text=True)
+        assert r.returncode == 0, r.stderr
