@@ -28,7 +28,15 @@ def stale() -> bool:
     return any(os.path.getmtime(p) > t for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, debug_out: str = "") -> str:
+    """Build libpolarscs.so; debug_out: build a separate library with device
+    bounds checks (-DPOLAR_DEBUG, asserts) at that path instead."""
+    if debug_out:
+        cmd = [NVCC] + FLAGS + ["-DPOLAR_DEBUG", "-o", debug_out] + [os.path.join(CSRC, s) for s in SOURCES]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError("nvcc failed:\n" + r.stdout + r.stderr)
+        return debug_out
     if not force and not stale():
         return SO
     cmd = [NVCC] + FLAGS + ["-o", SO + ".tmp"] + [os.path.join(CSRC, s) for s in SOURCES]

@@ -125,6 +125,7 @@ __device__ __forceinline__ int alloc_snapshot(const uint32_t (&s_ser)[SLOTS], co
         if (lim < 32) freem &= (1u << lim) - 1u;
         if (slot < 0 && freem) slot = w * 32 + __ffs(freem) - 1;
     }
+    POLAR_DCHECK(slot >= 0 && slot < D);
     return slot;
 }
 
@@ -173,6 +174,7 @@ __device__ __forceinline__ int alloc_snapshot_lazy(uint32_t *used, const uint32_
     __syncwarp();
     if (lane == 0) used[slot >> 5] |= 1u << (slot & 31);
     __syncwarp();
+    POLAR_DCHECK(slot >= 0 && slot < D);
     return slot;
 }
 
@@ -222,6 +224,7 @@ __device__ __forceinline__ int alloc_snapshot_big(uint32_t *used, int &uhint, co
     __syncwarp();
     if (lane == 0) used[slot >> 5] |= 1u << (slot & 31);
     __syncwarp();
+    POLAR_DCHECK(slot >= 0 && slot < D);
     return slot;
 }
 
@@ -299,6 +302,7 @@ fsscs_decode_kernel(const DecodeParams P) {
     auto hdr_at = [&](int k) -> uint2 * { return BIG ? ghdr + k : reinterpret_cast<uint2 *>(shdr) + k; };
     const int sstride = (NL > 0) ? nw : P.snap_stride;
     auto snap_slot = [&](int k) -> uint32_t * {
+        POLAR_DCHECK(k >= 0 && k < D);
         if (SNAP_SMEM) return snap_s + k * sstride;
         return P.snap_global + (size_t)(snap0 + (uint32_t)k) * (size_t)sstride;
     };
@@ -432,6 +436,7 @@ fsscs_decode_kernel(const DecodeParams P) {
                 }
             }
             nS--;
+            POLAR_DCHECK(nS >= 0 && nS < D);
             pops++;
             const float p_pm = __uint_as_float(mpm);
             const uint32_t p_ser = mser;
@@ -929,6 +934,7 @@ fsscs_decode_kernel(const DecodeParams P) {
                     kset(posk, ((unsigned long long)__float_as_uint(p_pm + my_d) << 32) | (ser0 + (uint32_t)lane));
                     sjsm[posk] = jbase | ((mk ^ (uint32_t)m0) << PK::MSH);
                 }
+                POLAR_DCHECK(nA + nfit - (hole >= 0 ? 1 : 0) <= D);
                 c1_slot = pos0;
                 widx = pos0;
                 __syncwarp();

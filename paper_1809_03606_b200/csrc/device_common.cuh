@@ -7,6 +7,13 @@
 
 #include "internal.h"
 
+#ifdef POLAR_DEBUG
+#include <cassert>
+#define POLAR_DCHECK(c) assert(c)
+#else
+#define POLAR_DCHECK(c) ((void)0)
+#endif
+
 namespace polar {
 
 constexpr uint32_t FULL = 0xFFFFFFFFu;

@@ -186,6 +186,7 @@ __global__ void __launch_bounds__(kListPackedWarps * 32, 8) fsscl_packed_kernel(
                             hi = __ldg(reinterpret_cast<const float4 *>(chan + Ls + i));
                         } else {
                             const int kb = first ? prow5(prow_s[par * L + k], s + 1) : k;
+                            POLAR_DCHECK(kb < L && k < nL);
                             const float *src = sb + (kb << (s + 1)) + i;
                             lo = *reinterpret_cast<const float4 *>(src);
                             hi = *reinterpret_cast<const float4 *>(src + Ls);
@@ -465,6 +466,7 @@ __global__ void __launch_bounds__(kListPackedWarps * 32, 8) fsscl_packed_kernel(
             if (lane < nL2) {
                 const int r = lane;
                 const int p = (int)(sel_s[r] >> 3), rk = (int)(sel_s[r] & 7u);
+                POLAR_DCHECK(p < nL && rk < nc);
                 const uint32_t cl = clist_s[p];
                 const uint32_t rel = ((cl >> (4 * rk)) & 15u) ^ (cl & 15u);
                 uint32_t *dst = beta_of(npar, r);
