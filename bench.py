@@ -54,6 +54,9 @@ def parse():
     ap.add_argument("--chan-smem", action="store_true")
     ap.add_argument("--bit-level", action="store_true",
                     help="bit-level SCS-RM (leaf-only schedule; the paper's SCS-RM comparator, PAPER.md:L797-813)")
+    ap.add_argument("--sequence", default="",
+                    help="information set from a reliability-sequence file (one index per line, least reliable "
+                         "first; e.g. the 3GPP sequence of PAPER.md:L966) instead of Bhattacharyya construction")
     ap.add_argument("--list-kernel", default="auto", choices=["auto", "cta", "packed"],
                     help="FSSCL kernel: CTA of L warps per frame, or one warp per frame with packed paths")
     ap.add_argument("--list", action="store_true",
@@ -78,7 +81,9 @@ def workload_name(cfg, c):
     else:
         mode = "bit-level SCS-RM" if c.get("bit_level") else "FSSCS-RM"
         dl = f"D={c['D']}, L={c['L']}"
-    return (f"{cfg}: {mode} PC({c['N']},{c['K']}) Bhattacharyya@{c['design_db']}dB, {crc}, {dl}, "
+    constr = (f"sequence file {os.path.basename(c['sequence'])}" if c.get("sequence")
+              else f"Bhattacharyya@{c['design_db']}dB")
+    return (f"{cfg}: {mode} PC({c['N']},{c['K']}) {constr}, {crc}, {dl}, "
             f"{c['frames']} frames x Eb/N0 {c['ebno']} dB, BPSK-AWGN float32 LLRs, seed {c['seed']}")
 
 
@@ -89,10 +94,20 @@ def metric_name(c):
     return METRIC
 
 
+def oracle_mask(c):
+    """the frozen mask of the workload, built by the oracle (O1 / O1b)"""
+    import oracle as O
+    if c.get("sequence"):
+        with open(c["sequence"], encoding="utf-8") as fh:
+            seq = [int(t.split("#", 1)[0]) for t in fh if t.split("#", 1)[0].strip()]
+        return O.mask_from_sequence(c["N"], c["K"], seq)
+    return O.bhattacharyya_mask(c["N"], c["K"], c["design_db"])
+
+
 def oracle_decoder(c):
     """the oracle decoder matching the bench mode (stack, or list with --list)"""
     import oracle as O
-    fr = O.bhattacharyya_mask(c["N"], c["K"], c["design_db"])
+    fr = oracle_mask(c)
     if c.get("list"):
         return O.SCLDecoder(fr, c["L"], c["crc_poly"], bit_level=bool(c.get("bit_level")))
     return O.SCSDecoder(fr, c["D"], c["L"], c["crc_poly"], bit_level=bool(c.get("bit_level")))
@@ -157,7 +172,7 @@ def oracle_sample(cfg, c, seconds, rank=0):
     workload: the same synthetic frames (inputgen draws, oracle-side encoding)."""
     import oracle as O
     threads = os.cpu_count() or 1
-    fr = O.bhattacharyya_mask(c["N"], c["K"], c["design_db"])
+    fr = oracle_mask(c)
     dec = oracle_decoder(c)
     cc = O.crc_degree(c["crc_poly"]) if c["crc_poly"] else 0
     # calibrate on a small prefix, then size the sample for ~`seconds` of work
@@ -233,7 +248,10 @@ def run_ours(args, cfg, c):
     nf = args.frames or c["frames"]
     npts = len(c["ebno"])
     frames = nf * npts
-    fr = P.bhattacharyya_mask(c["N"], c["K"], c["design_db"])
+    if c.get("sequence"):
+        fr = P.mask_from_sequence(c["N"], c["K"], P.load_reliability_sequence(c["sequence"]))
+    else:
+        fr = P.bhattacharyya_mask(c["N"], c["K"], c["design_db"])
     dec = P.PolarSCS(fr, c["D"], c["L"], c["crc_poly"], bit_level=bool(c.get("bit_level")),
                      snap_global=args.snap_global, snap_smem=args.snap_smem,
                      chan_global=args.chan_global, chan_smem=args.chan_smem, list_kernel=args.list_kernel)
@@ -445,6 +463,8 @@ def main():
         c["bit_level"] = True
     if args.list:
         c["list"] = True
+    if args.sequence:
+        c["sequence"] = args.sequence
     if args.impl == "reference":
         run_reference(args, cfg, c)
     else:

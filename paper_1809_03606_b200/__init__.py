@@ -103,6 +103,21 @@ def mask_from_sequence(N: int, K: int, seq) -> np.ndarray:
     return m
 
 
+def load_reliability_sequence(path: str) -> np.ndarray:
+    """A reliability sequence file (SPEC.md:L106 format: UTF-8 text, one
+    decimal index per line, least reliable first; blank lines and '#'
+    comments ignored), e.g. the 3GPP TS 38.212 sequence the paper uses
+    (PAPER.md:L966), which is not shipped.  Returns int32 indices; validity
+    (a permutation) is checked by polar_construct_from_sequence."""
+    idx = []
+    with open(path, encoding="utf-8") as fh:
+        for line in fh:
+            t = line.split("#", 1)[0].strip()
+            if t:
+                idx.append(int(t))
+    return np.asarray(idx, dtype=np.int32)
+
+
 def _stream_ptr(stream):
     import torch
     s = stream if stream is not None else torch.cuda.current_stream()

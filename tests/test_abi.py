@@ -156,3 +156,17 @@ def test_host_code_under_sanitizers():
         env = dict(os.environ, ASAN_OPTIONS="halt_on_error=1", UBSAN_OPTIONS="halt_on_error=1")
         r = subprocess.run([exe], capture_output=True, text=True, env=env, timeout=300)
         assert r.returncode == 0, r.stdout + r.stderr
+
+
+def test_reliability_sequence_file(tmp_path):
+    """SPEC.md:L106 file format -> information set, equal to the oracle's O1b."""
+    import paper_1809_03606_b200 as P
+    import oracle as O
+    rng = np.random.default_rng(3)
+    seq = rng.permutation(1024)
+    f = tmp_path / "seq.txt"
+    f.write_text("# least reliable first\n" + "\n".join(str(int(v)) for v in seq) + "\n\n")
+    got = P.load_reliability_sequence(str(f))
+    assert np.array_equal(got, seq)
+    for N, K in ((1024, 512), (256, 100), (64, 64)):
+        assert np.array_equal(P.mask_from_sequence(N, K, got), O.mask_from_sequence(N, K, seq))
