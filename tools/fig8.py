@@ -9,7 +9,10 @@ whole batch timed with CUDA events (inputs resident in HBM).  Throughput is
 aggregate over the GPU (K = 512 bits per frame, reading R14); the paper's
 numbers are per CPU thread and are printed beside as context.
 
-  python tools/fig8.py [--frames 20000] [--out profiles/r1/fig8_P.json]
+  python tools/fig8.py [--config P] [--frames 20000] [--out profiles/r1/fig8_P.json]
+
+With --config C2 (etc.) the same table is produced for that BASELINE config's
+code, stack parameters (D, L) and Eb/N0 points.
 """
 import argparse
 import json
@@ -46,9 +49,10 @@ def run(dec, llr, blocks, mode):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--frames", type=int, default=20000)
+    ap.add_argument("--config", default="P")
     ap.add_argument("--out", default="")
     args = ap.parse_args()
-    c = ig.CONFIGS["P"]
+    c = ig.CONFIGS[args.config]
     fr = P.bhattacharyya_mask(c["N"], c["K"], c["design_db"])
     decoders = {
         "FSSCS-RM": (P.PolarSCS(fr, c["D"], c["L"], c["crc_poly"]), "stack"),
@@ -64,14 +68,15 @@ def main():
             ms, fer = run(dec, llr, blocks, mode)
             mbps = args.frames * c["K"] / (ms / 1e3) / 1e6
             row = {"decoder": name, "ebno": eb, "frames": args.frames, "ms": ms, "info_mbps": mbps, "fer": fer}
-            if name in PAPER_TP:
+            if name in PAPER_TP and args.config == "P":
                 row["paper_cpu_mbps_per_thread"] = PAPER_TP[name][pi]
             rows.append(row)
             print(json.dumps(row), flush=True)
     if args.out:
         with open(args.out, "w") as fh:
-            json.dump({"workload": "config P: PC(1024,512) Bhattacharyya@2dB, CRC-24C 0xB2B117, L=8, D=8192, "
-                                   f"{args.frames} frames per point, device generator seed 5",
+            json.dump({"workload": f"config {args.config}: PC({c['N']},{c['K']}) Bhattacharyya@{c['design_db']}dB, "
+                                   f"crc_poly {c['crc_poly']:#x}, D={c['D']}, L={c['L']}, "
+                                   f"{args.frames} frames per point, device generator seed {c['seed']}",
                        "rows": rows}, fh, indent=1)
 
 
