@@ -40,8 +40,9 @@ __device__ __forceinline__ float ld1(const float *p, bool top) {
     return *p;
 }
 
-// src: stage s+1 (or the channel row when s+1 == n); dst: stage s
-template <bool CHAN_SMEM>
+// src: stage s+1 (or the channel row when s+1 == n); dst: stage s.  UNR:
+// unroll the float4 loop (independent iterations; measured on n = 10 only)
+template <bool CHAN_SMEM, bool UNR = false>
 __device__ __forceinline__ void alpha_stage(const float *src, float *dst, const uint32_t *beta,
                                             int n, int s, int psi, int lane) {
     const int Ls = 1 << s;
@@ -61,8 +62,7 @@ __device__ __forceinline__ void alpha_stage(const float *src, float *dst, const 
             dst[32 + lane] = f_minsum(lo1, hi1);
         }
     } else {
-        #pragma unroll 1
-        for (int i = lane * 4; i < Ls; i += 128) {
+        auto chunk = [&](int i) {
             const float4 lo = ld4<CHAN_SMEM>(src + i, top);
             const float4 hi = ld4<CHAN_SMEM>(src + Ls + i, top);
             float4 o;
@@ -75,6 +75,13 @@ __device__ __forceinline__ void alpha_stage(const float *src, float *dst, const 
                 o.z = f_minsum(lo.z, hi.z); o.w = f_minsum(lo.w, hi.w);
             }
             *reinterpret_cast<float4 *>(dst + i) = o;
+        };
+        if constexpr (UNR) {
+            #pragma unroll 4
+            for (int i = lane * 4; i < Ls; i += 128) chunk(i);
+        } else {
+            #pragma unroll 1
+            for (int i = lane * 4; i < Ls; i += 128) chunk(i);
         }
     }
     __syncwarp();
@@ -672,7 +679,7 @@ fsscs_decode_kernel(const DecodeParams P) {
 #define POLAR_SSTAGE(T)                                                                       \
     if constexpr ((T) < NL && (T) >= 6) {                                                     \
         if ((T) < lam) break;                                                                 \
-        alpha_stage<CHAN_SMEM>((T) + 1 == n ? chan : SP((T) + 1), SP(T), beta, n, (T), pl >> (T), lane); \
+        alpha_stage<CHAN_SMEM, (NL == 10 && SLOTS == 1)>((T) + 1 == n ? chan : SP((T) + 1), SP(T), beta, n, (T), pl >> (T), lane); \
     }
                     switch (s_hi) {
                     case 12: POLAR_SSTAGE(12)
