@@ -173,10 +173,13 @@ int polar_scl_decode(polar_scs_t h, const float *llr, int64_t n_frames, uint8_t 
 /*
  * End-to-end decode from HOST buffers: copies llr_host ([n][N] float32) to the
  * device in chunks, decodes, and copies the bits back to out_bits_host
- * ([n][K] uint8), overlapping the copies of one chunk with the decode of the
- * other on internal streams (H2D, two decode slots, D2H).  Blocking: returns when out_bits_host is
- * complete.  Pinned host memory gives full PCIe/C2C speed.  `stream` orders
- * the call after prior work on it.
+ * ([n][K] uint8), overlapping the copies of later chunks with the decode of
+ * earlier ones on internal streams (H2D, two decode slots, D2H).  The device
+ * staging is a ring of up to 8 chunk buffers of 256 MiB of LLRs (plus their
+ * bits), allocated on first use and kept by the handle (POLAR_ENOMEM if an
+ * allocation fails; the call then returns without completing the batch).
+ * Blocking: returns when out_bits_host is complete.  Pinned host memory gives
+ * full PCIe/C2C speed.  `stream` orders the call after prior work on it.
  */
 int polar_scs_decode_host(polar_scs_t h, const float *llr_host, int64_t n_frames,
                           uint8_t *out_bits_host, void *stream);

@@ -45,7 +45,7 @@ void free_handle(polar_scs_t h) {
     if (!h) return;
     cudaFree(h->t.nodes); cudaFree(h->t.info); cudaFree(h->t.crc_tab); cudaFree(h->t.crc_bytes); cudaFree(h->t.info_words);
     cudaFree(h->d_queue); cudaFree(h->d_snap); cudaFree(h->d_keys); cudaFree(h->d_jsm); cudaFree(h->d_hdr); cudaFree(h->d_galpha); cudaFree(h->d_salpha);
-    for (int b = 0; b < 2; b++) {
+    for (int b = 0; b < polar_scs_s::kStageBufs; b++) {
         cudaFree(h->d_stage_llr[b]); cudaFree(h->d_stage_bits[b]);
         if (h->ev_h2d[b]) cudaEventDestroy(h->ev_h2d[b]);
         if (h->ev_dec[b]) cudaEventDestroy(h->ev_dec[b]);
@@ -402,18 +402,14 @@ static int decode_host_impl(polar_scs_t h, bool list, const float *llr_host, int
     const int N = h->t.N, K = h->t.K;
     cudaError_t e = cudaSuccess;
     if (!h->s_comp[0]) {
-        // chunks of up to 256 MiB of LLRs, double-buffered; consecutive chunks
-        // decode on two streams with separate queue/arena slots, so the next
-        // chunk's CTAs fill the SMs while the previous chunk's last frames finish
+        // chunks of up to 256 MiB of LLRs in a ring of up to kStageBufs device
+        // buffers, so the copy engine can run several chunks ahead while the
+        // decode is slow (low-SNR frames) and the decode catches up on fast
+        // stretches; consecutive chunks decode on two streams with separate
+        // queue/arena slots, so the next chunk's CTAs fill the SMs while the
+        // previous chunk's last frames finish
         h->stage_frames = std::max<int64_t>(1, (int64_t)(256ll << 20) / (4ll * N));
-        for (int b = 0; b < 2 && e == cudaSuccess; b++) {
-            e = cudaMalloc(&h->d_stage_llr[b], (size_t)h->stage_frames * N * 4);
-            if (e == cudaSuccess) e = cudaMalloc(&h->d_stage_bits[b], (size_t)h->stage_frames * K);
-            if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_h2d[b], cudaEventDisableTiming);
-            if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_dec[b], cudaEventDisableTiming);
-            if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_d2h[b], cudaEventDisableTiming);
-        }
-        if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->s_h2d, cudaStreamNonBlocking);
+        e = cudaStreamCreateWithFlags(&h->s_h2d, cudaStreamNonBlocking);
         for (int b = 0; b < 2 && e == cudaSuccess; b++) e = cudaStreamCreateWithFlags(&h->s_comp[b], cudaStreamNonBlocking);
         if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&h->s_d2h, cudaStreamNonBlocking);
         if (e != cudaSuccess) return cuda_status(e);
@@ -431,18 +427,31 @@ static int decode_host_impl(polar_scs_t h, bool list, const float *llr_host, int
     // starts after a short copy, to the staging size
     int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(h->stage_frames, (int64_t)(16ll << 20) / (4ll * N)));
     for (int64_t off = 0; off < n && rc == POLAR_OK; off += chunk, chunk = std::min<int64_t>(2 * chunk, h->stage_frames), i++) {
-        const int b = (int)(i & 1);
+        const int b = (int)(i % polar_scs_s::kStageBufs), c = (int)(i & 1);
         const int64_t cnt = std::min<int64_t>(chunk, n - off);
-        cudaStreamWaitEvent(h->s_h2d, h->ev_dec[b], 0);       // buffer b's previous decode has read it
+        if (!h->d_stage_llr[b]) {
+            e = cudaMalloc(&h->d_stage_llr[b], (size_t)h->stage_frames * N * 4);
+            if (e == cudaSuccess) e = cudaMalloc(&h->d_stage_bits[b], (size_t)h->stage_frames * K);
+            if (e == cudaSuccess && !h->ev_h2d[b]) e = cudaEventCreateWithFlags(&h->ev_h2d[b], cudaEventDisableTiming);
+            if (e == cudaSuccess && !h->ev_dec[b]) e = cudaEventCreateWithFlags(&h->ev_dec[b], cudaEventDisableTiming);
+            if (e == cudaSuccess && !h->ev_d2h[b]) e = cudaEventCreateWithFlags(&h->ev_d2h[b], cudaEventDisableTiming);
+            if (e != cudaSuccess) {
+                cudaFree(h->d_stage_llr[b]); cudaFree(h->d_stage_bits[b]);
+                h->d_stage_llr[b] = nullptr; h->d_stage_bits[b] = nullptr;
+                rc = cuda_status(e);
+                break;
+            }
+        }
+        cudaStreamWaitEvent(h->s_h2d, h->ev_dec[b], 0);   // buffer b's previous decode has read it
         e = cudaMemcpyAsync(h->d_stage_llr[b], llr_host + off * N, (size_t)cnt * N * 4, cudaMemcpyHostToDevice, h->s_h2d);
         if (e != cudaSuccess) { rc = cuda_status(e); break; }
         cudaEventRecord(h->ev_h2d[b], h->s_h2d);
-        cudaStreamWaitEvent(h->s_comp[b], h->ev_h2d[b], 0);
-        cudaStreamWaitEvent(h->s_comp[b], h->ev_d2h[b], 0);   // bits buffer b has been copied out
-        rc = list ? list_impl(h, h->d_stage_llr[b], cnt, h->d_stage_bits[b], nullptr, nullptr, h->s_comp[b], b)
+        cudaStreamWaitEvent(h->s_comp[c], h->ev_h2d[b], 0);
+        cudaStreamWaitEvent(h->s_comp[c], h->ev_d2h[b], 0);   // bits buffer b has been copied out
+        rc = list ? list_impl(h, h->d_stage_llr[b], cnt, h->d_stage_bits[b], nullptr, nullptr, h->s_comp[c], c)
                   : decode_impl(h, h->d_stage_llr[b], cnt, h->d_stage_bits[b], nullptr, nullptr, nullptr, nullptr,
-                                h->s_comp[b], b);
-        cudaEventRecord(h->ev_dec[b], h->s_comp[b]);
+                                h->s_comp[c], c);
+        cudaEventRecord(h->ev_dec[b], h->s_comp[c]);
         cudaStreamWaitEvent(h->s_d2h, h->ev_dec[b], 0);
         e = cudaMemcpyAsync(bits_host + off * K, h->d_stage_bits[b], (size_t)cnt * K, cudaMemcpyDeviceToHost, h->s_d2h);
         if (e != cudaSuccess) { rc = cuda_status(e); break; }

@@ -135,9 +135,11 @@ struct polar_scs_s {
     polar::ListParams list{};       // prefilled FSSCL params
     // host-staging for polar_scs_decode_host (lazily allocated)
     cudaStream_t s_h2d = nullptr, s_comp[2] = {nullptr, nullptr}, s_d2h = nullptr;
-    float *d_stage_llr[2] = {nullptr, nullptr};
-    uint8_t *d_stage_bits[2] = {nullptr, nullptr};
-    cudaEvent_t ev_h2d[2] = {nullptr, nullptr}, ev_dec[2] = {nullptr, nullptr}, ev_d2h[2] = {nullptr, nullptr};
+    // host pipeline staging ring (allocated on first use, buffer by buffer)
+    static constexpr int kStageBufs = 8;
+    float *d_stage_llr[kStageBufs] = {};
+    uint8_t *d_stage_bits[kStageBufs] = {};
+    cudaEvent_t ev_h2d[kStageBufs] = {}, ev_dec[kStageBufs] = {}, ev_d2h[kStageBufs] = {};
     int64_t stage_frames = 0;
 };
 

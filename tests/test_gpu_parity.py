@@ -204,6 +204,22 @@ def test_decode_host_matches_device():
     assert torch.equal(out, ref)
 
 
+def test_decode_host_staging_ring_wraps():
+    """The host pipeline's chunks (16 MiB ramping to 256 MiB) wrap its ring of
+    8 staging buffers: 1.6 GB of LLRs = 11 chunks, a ragged last one."""
+    c, fr = _mk("C1")
+    dec = P.PolarSCS(fr, c["D"], c["L"], 0)
+    nf = 3_200_001
+    _, llr = dec.generate(7, 4.0, 0, nf, want_block=False)
+    ref = dec.decode(llr).cpu()
+    host = llr.cpu().pin_memory()
+    del llr
+    out = dec.decode_host(host)
+    assert torch.equal(out, ref)
+    out2 = dec.decode_host(host)              # second call reuses the ring
+    assert torch.equal(out2, ref)
+
+
 def test_full_size_sampled_parity_c2():
     """BASELINE C2 at full size in the bench's launch configuration: one call
     decodes 5 x 100,000 frames; sampled frames are checked against the oracle."""

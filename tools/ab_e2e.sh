@@ -1,0 +1,8 @@
+mkdir -p gpurun_out
+for rep in 1 2; do
+for c in C2 C3 C4 C5 P; do
+for lib in abtest/*.so; do
+  nm=$(basename $lib .so)
+  POLAR_SCS_LIB=$PWD/$lib timeout 900 python bench.py --config $c --no-cpu > gpurun_out/x.log 2>&1
+  python -c "import json;d=json.loads(open('gpurun_out/x.log').read().strip().split(chr(10))[-1]);print('$c','$nm',round(d['value']),round(d['e2e']['value']))"
+done; done; done
