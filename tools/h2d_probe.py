@@ -1,3 +1,4 @@
+"""Pinned host <-> device copy bandwidth (the e2e ceiling of decode_host) and the PCIe link state."""
 import torch, time
 x = torch.empty(2048*1024*1024//4, dtype=torch.float32, pin_memory=True)
 d = torch.empty_like(x, device="cuda")
@@ -16,4 +17,4 @@ dy = torch.empty_like(y, device="cuda")
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 e0.record(); y.copy_(dy, non_blocking=True); e1.record(); torch.cuda.synchronize()
 print("D2H 256MiB", y.numel()/(e0.elapsed_time(e1)/1e3)/1e9)
-import subprocess; print(subprocess.run("nvidia-smi -q | grep -A3 -i 'PCIe Generation\|Link Width'", shell=True, capture_output=True, text=True).stdout)
+import subprocess; print(subprocess.run(r"nvidia-smi -q | grep -A3 -i 'PCIe Generation\|Link Width'", shell=True, capture_output=True, text=True).stdout)
