@@ -171,15 +171,25 @@ int polar_scl_decode(polar_scs_t h, const float *llr, int64_t n_frames, uint8_t 
                      float *pm, uint8_t *status, void *stream);
 
 /*
- * End-to-end decode from HOST buffers: copies llr_host ([n][N] float32) to the
- * device in chunks, decodes, and copies the bits back to out_bits_host
- * ([n][K] uint8), overlapping the copies of later chunks with the decode of
- * earlier ones on internal streams (H2D, two decode slots, D2H).  The device
- * staging is a ring of up to 8 chunk buffers of 256 MiB of LLRs (plus their
- * bits), allocated on first use and kept by the handle (POLAR_ENOMEM if an
- * allocation fails; the call then returns without completing the batch).
- * Blocking: returns when out_bits_host is complete.  Pinned host memory gives
- * full PCIe/C2C speed.  `stream` orders the call after prior work on it.
+ * End-to-end decode from HOST buffers: llr_host ([n][N] float32) in,
+ * out_bits_host ([n][K] uint8) out.  Two internal pipelines:
+ *   - streaming (stack decoder, out_bits_host pinned / device-accessible, at
+ *     least 32 MiB of LLRs, stream memory operations available): one decode
+ *     launch per batch of up to 512 chunks (chunks of 256 KiB .. 8 MiB of
+ *     LLRs), started before the LLRs arrive; each chunk's H2D copy is followed
+ *     by a stream-ordered flag write that releases its frames to the kernel,
+ *     which writes the bits straight into out_bits_host.  Staging: one device
+ *     buffer of up to 4 GiB of LLRs, kept by the handle.
+ *   - chunked (otherwise, and for polar_scl_decode_host): chunks of 16 MiB
+ *     ramping to 256 MiB of LLRs in a ring of up to 8 device buffers, each
+ *     chunk copied in, decoded (two decode slots) and its bits copied out on
+ *     internal streams, later copies overlapping earlier decodes.
+ * Staging is allocated on first use (POLAR_ENOMEM if that fails; the call
+ * then returns without completing the batch).  POLAR_ECUDA if a streaming
+ * chunk's flag never arrives (the kernel gives up after > 17 s).  Blocking:
+ * returns when out_bits_host is complete.  Pinned host memory gives full
+ * PCIe/C2C speed.  `stream` orders the call after prior work on it.
+ * The environment variable POLAR_NO_STREAMING forces the chunked pipeline.
  */
 int polar_scs_decode_host(polar_scs_t h, const float *llr_host, int64_t n_frames,
                           uint8_t *out_bits_host, void *stream);

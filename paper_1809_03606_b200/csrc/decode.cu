@@ -324,7 +324,11 @@ fsscs_decode_kernel(const DecodeParams P) {
 
     #pragma unroll 1
     while (f < nfr) {
-        if (fnext < nfr) {
+        if (P.ready) {                    // streaming: this frame's chunk has landed
+            if (lane == 0) wait_chunk_ready(P.ready, P.err, f, P.chunk_shift);
+            __syncwarp();
+        }
+        if (fnext < nfr && (!P.ready || ld_acquire_u32(P.ready + (fnext >> P.chunk_shift)))) {
             const char *nr = reinterpret_cast<const char *>(P.llr + (size_t)fnext * N);
             #pragma unroll 1
             for (int b = lane * 128; b < N * 4; b += 32 * 128)

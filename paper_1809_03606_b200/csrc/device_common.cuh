@@ -93,4 +93,25 @@ __device__ __forceinline__ void top4_insert(unsigned long long key, unsigned lon
 }
 __device__ __forceinline__ int bitlen(uint32_t x) { return 32 - __clz(x); }
 
+// ---- streaming host pipeline (capi.cu, decode_host_stream): one launch over a
+// batch whose LLR rows are still being copied in.  Chunk i (2^shift frames) may
+// be read once ready[i] != 0, a flag written by a stream memory operation that
+// follows the chunk's H2D copy on the copy stream.
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t *p) {
+    uint32_t v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+// lane 0 only.  A flag that never arrives (a failed copy) sets *err after
+// about 2^26 sleeps of >= 256 ns (> 17 s) and lets the frame through, so the
+// launch ends and the host reports it.
+__device__ __forceinline__ void wait_chunk_ready(const uint32_t *ready, uint32_t *err, unsigned long long f, int shift) {
+    const uint32_t *fl = ready + (f >> shift);
+    #pragma unroll 1
+    for (uint32_t t = 0; !ld_acquire_u32(fl); t++) {
+        if (t >> 26) { atomicExch(err, 1u); return; }
+        __nanosleep(256);
+    }
+}
+
 }  // namespace polar

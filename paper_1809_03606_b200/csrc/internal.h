@@ -68,6 +68,9 @@ struct DecodeParams {
     int sg;                     // first alpha stage kept in the global arena (n: none)
     float *galpha;              // global alpha arena, N floats per resident warp (or null)
     int nonsys;                 // 1: read u_hat = x_hat F restricted to A (non-systematic)
+    const uint32_t *ready;      // streaming host pipeline: per-chunk "LLRs landed" flags (null: all resident)
+    uint32_t *err;              // streaming: set when a flag wait timed out
+    int chunk_shift;            // streaming: log2 frames per chunk
 };
 
 // Kernel parameter block of the FSSCL list decoder (list.cu).  One CTA of
@@ -141,6 +144,13 @@ struct polar_scs_s {
     uint8_t *d_stage_bits[kStageBufs] = {};
     cudaEvent_t ev_h2d[kStageBufs] = {}, ev_dec[kStageBufs] = {}, ev_d2h[kStageBufs] = {};
     int64_t stage_frames = 0;
+    // streaming host pipeline (capi.cu, decode_host_stream)
+    static constexpr int kStreamChunks = 512;   // ready flags per launch (+1 error word)
+    uint32_t *d_ready = nullptr;
+    float *d_sllr = nullptr;                    // staging of one launch's LLRs
+    int64_t stream_cap = 0;                     // frames d_sllr holds
+    int stream_ok = 0;                          // 1: memory operations work, -1: not available
+    cudaEvent_t ev_sreset = nullptr, ev_sdone = nullptr;
 };
 
 // host.cpp — code compilation on the host (validation, schedule, tables)

@@ -194,19 +194,38 @@ def test_decode_degenerate_inputs():
     assert bool((r["pops"] == dec.M + 1).all()) and bool((r["switches"] == 0).all())
 
 
-def test_decode_host_matches_device():
-    c, fr = _mk("C2")
-    dec = P.PolarSCS(fr, c["D"], c["L"], 0)
-    _, llr = dec.generate(1, 1.5, 0, 3000, want_block=False)
-    ref = dec.decode(llr).cpu()
-    host = llr.cpu().pin_memory()
-    out = dec.decode_host(host)
+@pytest.mark.parametrize("cfg", ["C2", "C3"])
+@pytest.mark.parametrize("list_decoder", [False, True])
+@pytest.mark.parametrize("in_pinned,out_pinned", [(True, True), (True, False), (False, True), (False, False)])
+def test_decode_host_matches_device(cfg, list_decoder, in_pinned, out_pinned):
+    """Both host pipelines against the device-resident decode: with a pinned
+    output buffer the stack decoder takes the streaming pipeline (one launch,
+    chunks flagged as they land, bits written straight to host memory; 9001
+    frames = 37 MB of LLRs, above its 32 MiB threshold), otherwise the chunked
+    pipeline runs; pageable inputs are legal in both."""
+    c, fr = _mk(cfg)
+    dec = P.PolarSCS(fr, c["D"], c["L"], c["crc_poly"])
+    _, llr = dec.generate(1, 1.5, 0, 9001, want_block=False)
+    ref = (dec.decode_list(llr, stats=False)["bits"] if list_decoder else dec.decode(llr)).cpu()
+    host = llr.cpu().pin_memory() if in_pinned else llr.cpu()
+    out = torch.empty((host.shape[0], dec.K), dtype=torch.uint8, pin_memory=out_pinned)
+    dec.decode_host(host, out, list_decoder=list_decoder)
     assert torch.equal(out, ref)
 
 
-def test_decode_host_staging_ring_wraps():
-    """The host pipeline's chunks (16 MiB ramping to 256 MiB) wrap its ring of
-    8 staging buffers: 1.6 GB of LLRs = 11 chunks, a ragged last one."""
+@pytest.mark.parametrize("nf", [1, 5, 64, 65])
+def test_decode_host_small(nf):
+    c, fr = _mk("C2")
+    dec = P.PolarSCS(fr, c["D"], c["L"], 0)
+    _, llr = dec.generate(3, 2.0, 0, nf, want_block=False)
+    ref = dec.decode(llr).cpu()
+    out = dec.decode_host(llr.cpu().pin_memory())
+    assert out.is_pinned() and torch.equal(out, ref)
+
+
+def test_decode_host_chunked_ring_wraps():
+    """The chunked pipeline's chunks (16 MiB ramping to 256 MiB) wrap its ring
+    of 8 staging buffers: 1.6 GB of LLRs = 11 chunks, a ragged last one."""
     c, fr = _mk("C1")
     dec = P.PolarSCS(fr, c["D"], c["L"], 0)
     nf = 3_200_001
@@ -214,10 +233,27 @@ def test_decode_host_staging_ring_wraps():
     ref = dec.decode(llr).cpu()
     host = llr.cpu().pin_memory()
     del llr
-    out = dec.decode_host(host)
-    assert torch.equal(out, ref)
-    out2 = dec.decode_host(host)              # second call reuses the ring
-    assert torch.equal(out2, ref)
+    for _ in range(2):                        # the second call reuses the ring
+        out = torch.empty((nf, dec.K), dtype=torch.uint8)     # pageable: chunked pipeline
+        dec.decode_host(host, out)
+        assert torch.equal(out, ref)
+
+
+def test_decode_host_streaming_several_launches():
+    """The streaming pipeline's launches hold 512 chunks of 8 MiB: 4.4 GB of
+    LLRs take two launches (the second waits for the first to free the
+    staging), with a ragged last chunk."""
+    c, fr = _mk("C1")
+    dec = P.PolarSCS(fr, c["D"], c["L"], 0)
+    nf = 8 * 1024 * 1024 + 12_345
+    _, llr = dec.generate(8, 4.0, 0, nf, want_block=False)
+    ref = dec.decode(llr).cpu()
+    host = llr.cpu().pin_memory()
+    del llr
+    for _ in range(2):
+        out = torch.empty((nf, dec.K), dtype=torch.uint8, pin_memory=True)
+        dec.decode_host(host, out)
+        assert torch.equal(out, ref)
 
 
 def test_full_size_sampled_parity_c2():
