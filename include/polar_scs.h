@@ -107,8 +107,9 @@ int polar_construct_from_sequence(int32_t N, int32_t K, const int32_t *seq, int3
  *   frozen, must have exactly N-K ones; D in [1, 8192] (D <= 128: the stack
  *   lives in registers; D > 128, up to the paper's D = NL = 8192 (PAPER.md:
  *   L599, L966): a per-warp stack in global memory, L2-resident in practice,
- *   with its snapshot arena of D x N/8 bytes per resident warp); L >= 1 (values above
- *   65535 are clamped: they never prune); crc_poly: 0 = none, else the full
+ *   with its snapshot arena of D x N/8 bytes per resident warp); L in
+ *   [1, 65536] (16-bit per-depth counters; exact over the whole range since
+ *   the L-th pop at a depth prunes that depth for good); crc_poly: 0 = none, else the full
  *   generator including the x^c term (0x11021 = CRC-16 0x1021, 0x107 = CRC-8
  *   0x07), degree c in [1, 31] and c < K; flags: POLAR_FLAG_*.
  *   On success *out receives the handle (owned by the caller; release with

@@ -187,7 +187,7 @@ int polar_scs_create_ex(polar_scs_t *out, int32_t N, int32_t K, const uint8_t *f
                            POLAR_FLAG_SNAP_SMEM | POLAR_FLAG_CHAN_SMEM | POLAR_FLAG_NONSYSTEMATIC |
                            POLAR_FLAG_LIST_CTA | POLAR_FLAG_LIST_PACKED;
     if ((flags & POLAR_FLAG_LIST_CTA) && (flags & POLAR_FLAG_LIST_PACKED)) return POLAR_EINVAL;
-    if (D < 1 || D > kMaxD || L < 1 || (flags & ~known)) return POLAR_EINVAL;
+    if (D < 1 || D > kMaxD || L < 1 || L > 65536 || (flags & ~known)) return POLAR_EINVAL;
     if ((flags & POLAR_FLAG_SNAP_GLOBAL) && (flags & POLAR_FLAG_SNAP_SMEM)) return POLAR_EINVAL;
     if ((flags & POLAR_FLAG_CHAN_GLOBAL) && (flags & POLAR_FLAG_CHAN_SMEM)) return POLAR_EINVAL;
     HostCode hc;
@@ -198,7 +198,9 @@ int polar_scs_create_ex(polar_scs_t *out, int32_t N, int32_t K, const uint8_t *f
     if (!h) return POLAR_ENOMEM;
     h->flags = flags;
     h->D = D;
-    h->L = std::min(L, 65535);
+    // 16-bit per-depth counters are exact up to L = 65536: the L-th pop at a
+    // depth prunes every entry of that depth or less, so no later pop has it
+    h->L = L;
     cudaError_t e = cudaGetDevice(&h->device);
     CodeTables &t = h->t;
     t.N = hc.N; t.n = hc.n; t.K = hc.K; t.c = hc.c; t.M = hc.M; t.crc_poly = crc_poly;

@@ -18,6 +18,9 @@
 // keys (|alpha| bits, index), candidates sorted by (dPM, mask), stack order
 // (PM, serial).  Built with -fmad=false; no fast-math.
 #include <cuda_runtime.h>
+#ifdef POLAR_TRACE_FRAME
+#include <cstdio>
+#endif
 
 #include "device_common.cuh"
 
@@ -452,6 +455,10 @@ fsscs_decode_kernel(const DecodeParams P) {
             const float p_pm = __uint_as_float(mpm);
             const uint32_t p_ser = mser;
             const int j = (int)jsm_j(p_jsm);
+#ifdef POLAR_TRACE_FRAME
+            if (f == POLAR_TRACE_FRAME && lane == 0)
+                printf("TRACE pop %u: pm %.9g (%#x) ser %u j %d work %u\n", pops, p_pm, mpm, p_ser, j, work);
+#endif
 
             // ---- per-length counter and prune (readings R9, R10)
             const int c_j = (int)cnt[j] + 1;
@@ -645,6 +652,10 @@ fsscs_decode_kernel(const DecodeParams P) {
                     ok = (syn == 0);
                 }
                 if (ok) { out_pm = p_pm; status = 0; break; }
+                // the climb above combined blocks that the alpha memory was
+                // computed from, so beta no longer tells the next switch which
+                // stages are stale: recompute the next spine from the channel
+                lev_mem = n;
                 if (!have_best) {
                     #pragma unroll 1
                     for (int w = lane; w < nw; w += 32) best[w] = beta[w];
@@ -741,6 +752,16 @@ fsscs_decode_kernel(const DecodeParams P) {
                     }
                 }
 #undef POLAR_RSTAGE
+#ifdef POLAR_TRACE_FRAME
+                if (f == POLAR_TRACE_FRAME) {
+                    float v[8];
+#pragma unroll
+                    for (int q = 0; q < 8; q++) v[q] = __shfl_sync(FULL, xr, q);
+                    if (lane == 0)
+                        printf("TRACE   node kind %d lam %d phi %d pl %d s_min %d (lev_mem %d pos_mem %d s_d %d l %d) alpha %.9g %.9g %.9g %.9g %.9g %.9g %.9g %.9g\n",
+                               kind, lam, phi, pl, s_min, lev_mem, pos_mem, s_d, l, v[0], v[1], v[2], v[3], v[4], v[5], v[6], v[7]);
+                }
+#endif
                 pos_mem = pl;
                 lev_mem = lam + 1;
             }

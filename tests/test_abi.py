@@ -80,6 +80,7 @@ def test_create_rejects_bad_arguments():
         (128, 64, ok, 0, 4, 0),          # D < 1
         (128, 64, ok, 8193, 4, 0),       # D > 8192
         (128, 64, ok, 8, 0, 0),          # L < 1
+        (128, 64, ok, 8, 65537, 0),      # L above the 16-bit counters' exact range
         (128, 64, None, 8, 4, 0),        # NULL mask
         (128, 64, ok, 8, 4, 1),          # degenerate polynomial
     ]

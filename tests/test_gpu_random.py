@@ -5,8 +5,11 @@ combinations the fixed cases do not: register stacks (D <= 128) and global
 stacks (D > 128), the FSSCL list decoder, bit-level schedules, non-systematic
 readout and random (generally non-systematic-encodable) information sets.
 Each case decodes the same LLR buffer on both sides and compares bits, status,
-pops/switches exactly and PM within rel 1e-6.
+pops/switches exactly and PM within rel 1e-6.  POLAR_RANDOM_STACK /
+POLAR_RANDOM_LIST widen the sweep (default 200 / 80 seeds).
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -60,7 +63,7 @@ def _inputs(dec, fr, crc, nonsys, ebno, n, seed):
     return gl, ol
 
 
-@pytest.mark.parametrize("seed", range(200))
+@pytest.mark.parametrize("seed", range(int(os.environ.get("POLAR_RANDOM_STACK", "200"))))
 def test_random_stack_parity(seed):
     fr, N, K, D, L, crc, bit_level, nonsys, ebno = _case(seed)
     if not nonsys and not P.PolarSCS(fr, 1, 1, 0).info["systematic_ok"]:
@@ -72,7 +75,26 @@ def test_random_stack_parity(seed):
     _compare(dec.decode_stats(gl), ref, f"seed {seed}: N{N} K{K} D{D} L{L} crc{crc:#x} bit{bit_level} ns{nonsys}")
 
 
-@pytest.mark.parametrize("seed", range(80))
+@pytest.mark.parametrize("seed", [537, 1137])
+def test_random_stack_regressions(seed):
+    """Seeds of a 2500-case sweep (profiles/r1/pytest_random_sweep_before_fix.log)
+    that caught a stale alpha spine: after a complete path failed its CRC, the
+    final BETA climb had combined blocks the alpha memory was computed from,
+    and the next switch's beta comparison missed a changed prefix (one pop
+    fewer than the oracle, same result)."""
+    test_random_stack_parity(seed)
+
+
+@pytest.mark.skipif(not os.environ.get("POLAR_SLOW"), reason="slow oracle (minutes per case); POLAR_SLOW=1")
+@pytest.mark.parametrize("seed", [245, 396, 1361, 2086])
+def test_random_stack_regressions_visit_limit(seed):
+    """Seeds of the same sweep that caught the handle clamping L = 65536 to
+    65535: a depth reaching 65535 pops was pruned one pop before the oracle's
+    (PAPER.md:L595).  Searches of ~10^6 pops: the oracle needs minutes."""
+    test_random_stack_parity(seed)
+
+
+@pytest.mark.parametrize("seed", range(int(os.environ.get("POLAR_RANDOM_LIST", "80"))))
 def test_random_list_parity(seed):
     fr, N, K, D, L, crc, bit_level, nonsys, ebno = _case(seed + 500)
     L = min(L, 32)
