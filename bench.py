@@ -115,61 +115,29 @@ def oracle_decoder(c):
 
 # ------------------------------------------------------------------ clocks
 class ClockSampler:
-    """SM clocks and clock-event (throttle) reasons sampled during the timed
-    region: NVML polled every 2 ms from a thread (the first sample is taken
-    before the region starts, so even a ~1 ms region is covered), else
-    nvidia-smi -lms 100."""
+    """nvidia-smi clocks/throttle reasons sampled during the timed region
+    (-lms 100).  A region too short for one sample (C1: ~1 ms) gets one
+    one-shot query right after it, flagged in the summary."""
 
     Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
-    # NVML clocks-event reason bits
-    BITS = {"sw_power_cap": 0x4, "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40}
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, index):
         self.index = index
-        self.rows = []           # (sm_mhz, max_mhz, set of reasons)
+        self.rows = []           # (sm_mhz, max_mhz, set of active reasons)
         self.proc = None
-        self.nvml = None
-        self.stop = threading.Event()
+        self.post = False
 
-    def _nvml_handle(self):
-        import pynvml
-        pynvml.nvmlInit()
+    def _parse(self, line):
+        r = [x.strip() for x in line.split(",")]
         try:
-            import torch
-            bus = torch.cuda.get_device_properties(self.index).pci_bus_id
-            return pynvml, pynvml.nvmlDeviceGetHandleByPciBusId(bus)
-        except Exception:
-            return pynvml, pynvml.nvmlDeviceGetHandleByIndex(self.index)
-
-    def _nvml_sample(self):
-        nv, h = self.nvml
-        sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
-        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
-        try:
-            bits = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
-        except AttributeError:
-            bits = nv.nvmlDeviceGetCurrentClocksThrottleReasons(h)
-        self.rows.append((float(sm), float(mx), {k for k, v in self.BITS.items() if bits & v}))
-
-    def _nvml_loop(self):
-        while not self.stop.wait(0.002):
-            try:
-                self._nvml_sample()
-            except Exception:
-                return
+            return (float(r[0]), float(r[1]), {nm for nm, v in zip(self.NAMES, r[4:8]) if v.lower() == "active"})
+        except (ValueError, IndexError):
+            return None
 
     def __enter__(self):
-        try:
-            self.nvml = self._nvml_handle()
-            self._nvml_sample()
-            self.t = threading.Thread(target=self._nvml_loop, daemon=True)
-            self.t.start()
-            return self
-        except Exception:
-            self.nvml = None
-            self.rows = []
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
@@ -181,38 +149,39 @@ class ClockSampler:
         return self
 
     def _read(self):
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for line in self.proc.stdout:
-            r = [x.strip() for x in line.split(",")]
-            try:
-                self.rows.append((float(r[0]), float(r[1]),
-                                  {nm for nm, v in zip(names, r[4:8]) if v.lower() == "active"}))
-            except (ValueError, IndexError):
-                continue
+            row = self._parse(line)
+            if row:
+                self.rows.append(row)
 
     def __exit__(self, *a):
-        if self.nvml:
-            try:
-                self._nvml_sample()          # the region's last moment
-            except Exception:
-                pass
-            self.stop.set()
-            self.t.join(timeout=1)
         if self.proc:
             self.proc.terminate()
             try:
                 self.proc.wait(timeout=5)
             except subprocess.TimeoutExpired:
                 self.proc.kill()
+        if not self.rows:
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=30).stdout
+                row = self._parse(out.strip().split("\n")[0]) if out.strip() else None
+                if row:
+                    self.rows.append(row)
+                    self.post = True
+            except (OSError, subprocess.SubprocessError):
+                pass
 
     def summary(self):
         rows = list(self.rows)
         if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
-        reasons = set().union(*(r[2] for r in rows))
-        return {"sm_mhz": statistics.median(r[0] for r in rows), "sm_max_mhz": max(r[1] for r in rows),
-                "reasons": sorted(reasons), "samples": len(rows),
-                "source": "nvml" if self.nvml else "nvidia-smi"}
+        out = {"sm_mhz": statistics.median(r[0] for r in rows), "sm_max_mhz": max(r[1] for r in rows),
+               "reasons": sorted(set().union(*(r[2] for r in rows))), "samples": len(rows)}
+        if self.post:
+            out["note"] = "timed region shorter than the 100 ms sampling period: one query right after it"
+        return out
 
 
 # ------------------------------------------------------------------ CPU oracle leg
