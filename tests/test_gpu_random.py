@@ -6,7 +6,8 @@ stacks (D > 128), the FSSCL list decoder, bit-level schedules, non-systematic
 readout and random (generally non-systematic-encodable) information sets.
 Each case decodes the same LLR buffer on both sides and compares bits, status,
 pops/switches exactly and PM within rel 1e-6.  POLAR_RANDOM_STACK /
-POLAR_RANDOM_LIST widen the sweep (default 200 / 80 seeds).
+POLAR_RANDOM_LIST widen the sweep (default 200 / 80 seeds), POLAR_RANDOM_OFFSET
+shifts its first seed.
 """
 import os
 
@@ -63,7 +64,10 @@ def _inputs(dec, fr, crc, nonsys, ebno, n, seed):
     return gl, ol
 
 
-@pytest.mark.parametrize("seed", range(int(os.environ.get("POLAR_RANDOM_STACK", "200"))))
+_OFF = int(os.environ.get("POLAR_RANDOM_OFFSET", "0"))
+
+
+@pytest.mark.parametrize("seed", range(_OFF, _OFF + int(os.environ.get("POLAR_RANDOM_STACK", "200"))))
 def test_random_stack_parity(seed):
     fr, N, K, D, L, crc, bit_level, nonsys, ebno = _case(seed)
     if not nonsys and not P.PolarSCS(fr, 1, 1, 0).info["systematic_ok"]:
@@ -94,7 +98,7 @@ def test_random_stack_regressions_visit_limit(seed):
     test_random_stack_parity(seed)
 
 
-@pytest.mark.parametrize("seed", range(int(os.environ.get("POLAR_RANDOM_LIST", "80"))))
+@pytest.mark.parametrize("seed", range(_OFF, _OFF + int(os.environ.get("POLAR_RANDOM_LIST", "80"))))
 def test_random_list_parity(seed):
     fr, N, K, D, L, crc, bit_level, nonsys, ebno = _case(seed + 500)
     L = min(L, 32)
