@@ -570,7 +570,10 @@ static int decode_host_impl(polar_scs_t h, bool list, const float *llr_host, int
     int64_t i = 0;
     // chunk sizes ramp up geometrically from ~16 MiB, so the first decode
     // starts after a short copy, to the staging size
+    // (a batch under 32 MiB starts with half of it, so its two copies overlap
+    // the first half's decode)
     int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(h->stage_frames, (int64_t)(16ll << 20) / (4ll * N)));
+    if (n * 4ll * N < (32ll << 20)) chunk = std::max<int64_t>(1, std::min<int64_t>(chunk, (n + 1) / 2));
     for (int64_t off = 0; off < n && rc == POLAR_OK; off += chunk, chunk = std::min<int64_t>(2 * chunk, h->stage_frames), i++) {
         const int b = (int)(i % polar_scs_s::kStageBufs), c = (int)(i & 1);
         const int64_t cnt = std::min<int64_t>(chunk, n - off);
