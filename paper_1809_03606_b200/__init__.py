@@ -219,9 +219,17 @@ class PolarSCS:
             llr_host = torch.from_numpy(np.ascontiguousarray(llr_host, dtype=np.float32))
         if llr_host.is_cuda or llr_host.dtype != torch.float32 or not llr_host.is_contiguous():
             raise TypeError("llr_host: contiguous CPU float32 tensor expected")
+        if llr_host.dim() != 2 or llr_host.shape[1] != self.N:
+            raise ValueError(f"llr_host: shape (n, {self.N}) expected, got {tuple(llr_host.shape)}")
         n = llr_host.shape[0]
         if out_host is None:
             out_host = torch.empty((n, self.K), dtype=torch.uint8, pin_memory=llr_host.is_pinned())
+        elif isinstance(out_host, np.ndarray):
+            raise TypeError("out_host: CPU uint8 tensor expected (use torch.from_numpy)")
+        if out_host.is_cuda or out_host.dtype != torch.uint8 or not out_host.is_contiguous():
+            raise TypeError("out_host: contiguous CPU uint8 tensor expected")
+        if tuple(out_host.shape) != (n, self.K):
+            raise ValueError(f"out_host: shape ({n}, {self.K}) expected, got {tuple(out_host.shape)}")
         fn = polar_scl_decode_host if list_decoder else polar_scs_decode_host
         _check(fn(self._h, llr_host.data_ptr(), n, out_host.data_ptr(), _stream_ptr(stream)), fn.__name__)
         return out_host

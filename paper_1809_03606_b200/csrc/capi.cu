@@ -77,6 +77,24 @@ CodecParams codec_params(polar_scs_t h, int64_t n) {
 
 int cuda_status(cudaError_t e) { return e == cudaSuccess ? POLAR_OK : (e == cudaErrorMemoryAllocation ? POLAR_ENOMEM : POLAR_ECUDA); }
 
+// Every entry point that touches device memory runs on the handle's device:
+// switch to it on entry, restore the caller's device on return.
+struct DeviceGuard {
+    int prev = -1;
+    bool ok = true;
+    explicit DeviceGuard(polar_scs_t h) {
+        if (!h) return;
+        int cur = 0;
+        if (cudaGetDevice(&cur) != cudaSuccess) { ok = false; return; }
+        if (cur == h->device) return;
+        if (cudaSetDevice(h->device) != cudaSuccess) { ok = false; return; }
+        prev = cur;
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+};
+
 // slot: which frame-queue counter / snapshot arena the launch uses; two slots
 // let the host pipeline overlap one chunk's decode with the next one's
 // streaming host pipeline: per-chunk ready flags, error word, log2 frames per chunk
@@ -370,6 +388,7 @@ int polar_scs_create(polar_scs_t *out, int32_t N, int32_t K, const uint8_t *froz
 
 void polar_scs_destroy(polar_scs_t h) {
     if (!h) return;
+    DeviceGuard g(h);
     cudaDeviceSynchronize();
     free_handle(h);
 }
@@ -389,6 +408,8 @@ int polar_scs_decode_stats(polar_scs_t h, const float *llr, int64_t n, uint8_t *
                            uint32_t *sw, uint8_t *status, void *stream) {
     if (!h || n < 0) return POLAR_EINVAL;
     if (n == 0) return POLAR_OK;
+    DeviceGuard g(h);
+    if (!g.ok) return POLAR_ECUDA;
     if (!llr || !bits) return POLAR_EINVAL;
     if (h->t.N >= 4 && (reinterpret_cast<uintptr_t>(llr) & 15u)) return POLAR_EINVAL;
     return decode_impl(h, llr, n, bits, pm, pops, sw, status, static_cast<cudaStream_t>(stream));
@@ -403,6 +424,8 @@ int polar_scl_decode(polar_scs_t h, const float *llr, int64_t n, uint8_t *bits, 
     if (!h || n < 0) return POLAR_EINVAL;
     if (h->list_ctas == 0) return POLAR_ENOTSYS;
     if (n == 0) return POLAR_OK;
+    DeviceGuard g(h);
+    if (!g.ok) return POLAR_ECUDA;
     if (!llr || !bits) return POLAR_EINVAL;
     if (h->t.N >= 4 && (reinterpret_cast<uintptr_t>(llr) & 15u)) return POLAR_EINVAL;
     return list_impl(h, llr, n, bits, pm, status, static_cast<cudaStream_t>(stream));
@@ -439,6 +462,13 @@ static int decode_host_stream(polar_scs_t h, const float *llr_host, int64_t n, u
                               cudaStream_t stream) {
     WriteValue32Fn wv = write_value32();
     if (!wv) return 1;
+    // the launch waits for copies queued after it: with blocking launches
+    // (CUDA_LAUNCH_BLOCKING=1) they would only be issued once it returned
+    static const bool blocking = [] {
+        const char *v = std::getenv("CUDA_LAUNCH_BLOCKING");
+        return v && v[0] && v[0] != '0';
+    }();
+    if (blocking) return 1;
     const int N = h->t.N, K = h->t.K;
     cudaError_t e = cudaSuccess;
     if (!h->d_ready) {
@@ -483,6 +513,7 @@ static int decode_host_stream(polar_scs_t h, const float *llr_host, int64_t n, u
     cudaStreamWaitEvent(h->s_h2d, start, 0);
     cudaStreamWaitEvent(h->s_comp[0], start, 0);
     int rc = POLAR_OK;
+    bool launched = false;
     e = cudaMemsetAsync(err, 0, sizeof(uint32_t), h->s_h2d);
     for (int64_t off = 0; off < n && rc == POLAR_OK && e == cudaSuccess; off += batch) {
         const int64_t m = std::min<int64_t>(batch, n - off);
@@ -491,23 +522,30 @@ static int decode_host_stream(polar_scs_t h, const float *llr_host, int64_t n, u
         e = cudaMemsetAsync(ready, 0, (size_t)nch * sizeof(uint32_t), h->s_h2d);
         if (e != cudaSuccess) break;
         cudaEventRecord(h->ev_sreset, h->s_h2d);
-        cudaStreamWaitEvent(h->s_comp[0], h->ev_sreset, 0);
-        rc = decode_impl(h, h->d_sllr, m, bits_dev + off * K, nullptr, nullptr, nullptr, nullptr, h->s_comp[0], 0, &sa);
-        if (rc != POLAR_OK) break;
-        cudaEventRecord(h->ev_sdone, h->s_comp[0]);
-        for (int64_t i = 0; i < nch && e == cudaSuccess; i++) {
+        // chunk i: H2D copy, then its ready flag (a stream memory operation)
+        auto land = [&](int64_t i) {
             const int64_t cnt = std::min<int64_t>(cf, m - i * cf);
             e = cudaMemcpyAsync(h->d_sllr + (size_t)(i * cf) * N, llr_host + (size_t)(off + i * cf) * N, (size_t)cnt * N * 4,
                                 cudaMemcpyHostToDevice, h->s_h2d);
             if (e == cudaSuccess && wv(reinterpret_cast<CUstream>(h->s_h2d), reinterpret_cast<CUdeviceptr>(ready + i), 1u, 0) != CUDA_SUCCESS)
                 e = cudaErrorUnknown;
-        }
+        };
+        land(0);                          // the first chunk is queued before the launch that waits for it
+        if (e != cudaSuccess) break;
+        cudaStreamWaitEvent(h->s_comp[0], h->ev_sreset, 0);
+        rc = decode_impl(h, h->d_sllr, m, bits_dev + off * K, nullptr, nullptr, nullptr, nullptr, h->s_comp[0], 0, &sa);
+        if (rc != POLAR_OK) break;
+        launched = true;
+        cudaEventRecord(h->ev_sdone, h->s_comp[0]);
+        for (int64_t i = 1; i < nch && e == cudaSuccess; i++) land(i);
     }
     if (rc == POLAR_OK && e != cudaSuccess) rc = cuda_status(e);
-    if (e != cudaSuccess) {
-        // a launch may be waiting for flags that will not come: release it
-        // (its frames then fail with *err set, reported below)
-        cudaMemsetAsync(ready, 0xFF, polar_scs_s::kStreamChunks * sizeof(uint32_t), h->s_h2d);
+    if (e != cudaSuccess && launched) {
+        // a launch may be waiting for flags that will not come: release it by
+        // setting the error word with a stream memory operation (done by the
+        // GPU front end, so it needs no free SM); every wait of the launch then
+        // returns at once and the host reports the failure below
+        wv(reinterpret_cast<CUstream>(h->s_h2d), reinterpret_cast<CUdeviceptr>(err), 1u, 0);
     }
     cudaError_t e2 = cudaStreamSynchronize(h->s_h2d);
     const cudaError_t e3 = cudaStreamSynchronize(h->s_comp[0]);
@@ -527,6 +565,8 @@ static int decode_host_impl(polar_scs_t h, bool list, const float *llr_host, int
     if (!h || n < 0) return POLAR_EINVAL;
     if (list && h->list_ctas == 0) return POLAR_ENOTSYS;
     if (n == 0) return POLAR_OK;
+    DeviceGuard g(h);
+    if (!g.ok) return POLAR_ECUDA;
     if (!llr_host || !bits_host) return POLAR_EINVAL;
     const int N = h->t.N, K = h->t.K;
     cudaError_t e = cudaSuccess;
@@ -627,6 +667,8 @@ int polar_scl_decode_host(polar_scs_t h, const float *llr_host, int64_t n, uint8
 int polar_crc_attach_batch(polar_scs_t h, const uint8_t *payload, int64_t n, uint8_t *block, void *stream) {
     if (!h || n < 0) return POLAR_EINVAL;
     if (n == 0) return POLAR_OK;
+    DeviceGuard g(h);
+    if (!g.ok) return POLAR_ECUDA;
     if (!payload || !block) return POLAR_EINVAL;
     CodecParams p = codec_params(h, n);
     p.payload = payload; p.block_out = block;
@@ -637,6 +679,8 @@ int polar_encode_batch(polar_scs_t h, const uint8_t *block, int64_t n, uint8_t *
     if (!h || n < 0) return POLAR_EINVAL;
     if (!h->t.systematic_ok && !(h->flags & POLAR_FLAG_NONSYSTEMATIC)) return POLAR_ENOTSYS;
     if (n == 0) return POLAR_OK;
+    DeviceGuard g(h);
+    if (!g.ok) return POLAR_ECUDA;
     if (!block || !codeword) return POLAR_EINVAL;
     CodecParams p = codec_params(h, n);
     p.block_in = block; p.codeword = codeword;
@@ -647,6 +691,8 @@ int polar_modulate_batch(polar_scs_t h, const uint8_t *codeword, const float *no
                          float *llr, void *stream) {
     if (!h || n < 0) return POLAR_EINVAL;
     if (n == 0) return POLAR_OK;
+    DeviceGuard g(h);
+    if (!g.ok) return POLAR_ECUDA;
     if (!codeword || !noise || !llr) return POLAR_EINVAL;
     CodecParams p = codec_params(h, n);
     const double var = sigma2_of(ebno_db, (double)h->t.K / (double)h->t.N);
@@ -661,6 +707,8 @@ int polar_generate_batch(polar_scs_t h, uint64_t seed, double ebno_db, int64_t f
     if (!h || n < 0 || first_frame < 0) return POLAR_EINVAL;
     if (!h->t.systematic_ok && !(h->flags & POLAR_FLAG_NONSYSTEMATIC)) return POLAR_ENOTSYS;
     if (n == 0) return POLAR_OK;
+    DeviceGuard g(h);
+    if (!g.ok) return POLAR_ECUDA;
     if (!llr) return POLAR_EINVAL;
     if (h->t.N >= 4 && (reinterpret_cast<uintptr_t>(llr) & 15u)) return POLAR_EINVAL;
     CodecParams p = codec_params(h, n);

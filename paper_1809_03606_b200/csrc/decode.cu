@@ -31,15 +31,15 @@ constexpr uint32_t NO_SNAP = 0xFFFFu;
 
 // ALPHA(s, psi): alpha_s from alpha_{s+1} (Eq. 4, Alg. 1) for stages s >= 6
 // (Lambda >= 64) held in shared memory at alpha[2^s, 2^{s+1}).  Stage n is the
-// channel row: shared memory (CHAN_SMEM) or the LLR input read through L1/L2.
+// channel row: shared memory (CHAN_SMEM) or the LLR input read through L1/L2
+// with coherent loads (never the non-coherent path: the streaming host
+// pipeline lands rows while the kernel runs, ordered by the chunk flags).
 template <bool CHAN_SMEM>
-__device__ __forceinline__ float4 ld4(const float *p, bool top) {
-    if (!CHAN_SMEM && top) return __ldg(reinterpret_cast<const float4 *>(p));
+__device__ __forceinline__ float4 ld4(const float *p, bool) {
     return *reinterpret_cast<const float4 *>(p);
 }
 template <bool CHAN_SMEM>
-__device__ __forceinline__ float ld1(const float *p, bool top) {
-    if (!CHAN_SMEM && top) return __ldg(p);
+__device__ __forceinline__ float ld1(const float *p, bool) {
     return *p;
 }
 
@@ -260,7 +260,11 @@ fsscs_decode_kernel(const DecodeParams P) {
     using PK = Pk<BIG>;
     extern __shared__ __align__(16) uint32_t smem[];
     const int lane = threadIdx.x & 31;
-    const int warp = threadIdx.x >> 5;
+    // warp index as a warp reduction: ptxas then knows it (and every shared-
+    // memory address derived from it) is warp-uniform, so branches on values
+    // loaded from this warp's shared memory compile as uniform branches, with
+    // no reconvergence barriers or divergence checks around the warp intrinsics
+    const int warp = (int)__reduce_max_sync(FULL, threadIdx.x >> 5);
     const int n = (NL > 0) ? NL : P.n;
     const int N = 1 << n;
     const int nw = (NL > 0) ? (NL >= 5 ? (1 << NL) / 32 : 1) : P.nw;
@@ -327,11 +331,8 @@ fsscs_decode_kernel(const DecodeParams P) {
 
     #pragma unroll 1
     while (f < nfr) {
-        if (P.ready) {                    // streaming: this frame's chunk has landed
-            if (lane == 0) wait_chunk_ready(P.ready, P.err, f, P.chunk_shift);
-            __syncwarp();
-        }
-        if (fnext < nfr && (!P.ready || ld_acquire_u32(P.ready + (fnext >> P.chunk_shift)))) {
+        if (P.ready) wait_chunk_ready(P.ready, P.err, f, P.chunk_shift);   // streaming: this frame's chunk has landed
+        if (fnext < nfr && (!P.ready || __reduce_or_sync(FULL, ld_acquire_u32(P.ready + (fnext >> P.chunk_shift))))) {
             const char *nr = reinterpret_cast<const char *>(P.llr + (size_t)fnext * N);
             #pragma unroll 1
             for (int b = lane * 128; b < N * 4; b += 32 * 128)
@@ -651,15 +652,20 @@ fsscs_decode_kernel(const DecodeParams P) {
                     syn = __reduce_xor_sync(FULL, syn);
                     ok = (syn == 0);
                 }
+                // best effort (reading R13): the first complete path popped.  Its
+                // copy is taken before the exit test (stores on the path after a
+                // data-dependent loop exit made ptxas treat the loop as divergent)
+                if (!have_best) {
+                    #pragma unroll 1
+                    for (int w = lane; w < nw; w += 32) best[w] = beta[w];
+                    __syncwarp();
+                }
                 if (ok) { out_pm = p_pm; status = 0; break; }
                 // the climb above combined blocks that the alpha memory was
                 // computed from, so beta no longer tells the next switch which
                 // stages are stale: recompute the next spine from the channel
                 lev_mem = n;
                 if (!have_best) {
-                    #pragma unroll 1
-                    for (int w = lane; w < nw; w += 32) best[w] = beta[w];
-                    __syncwarp();
                     have_best = true;
                     best_pm = p_pm;
                 }

@@ -102,14 +102,23 @@ __device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t *p) {
     asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
-// lane 0 only.  A flag that never arrives (a failed copy) sets *err after
-// about 2^26 sleeps of >= 256 ns (> 17 s) and lets the frame through, so the
-// launch ends and the host reports it.
+// Whole warp (every lane reads the flag; the loop condition is a warp
+// reduction, so the wait keeps the warp provably converged — a lane-0 spin
+// here made ptxas treat the whole decode loop as divergent).  A flag that
+// never arrives (a failed copy) sets *err after about 2^26 sleeps of
+// >= 256 ns (> 17 s) and lets the frame through, so the launch ends and the
+// host reports it.  Once *err is set (by that timeout, or by the host
+// releasing the launch after a failed copy) every later wait of the launch
+// returns at once: a stalled batch costs one timeout, not one per frame.
 __device__ __forceinline__ void wait_chunk_ready(const uint32_t *ready, uint32_t *err, unsigned long long f, int shift) {
     const uint32_t *fl = ready + (f >> shift);
     #pragma unroll 1
-    for (uint32_t t = 0; !ld_acquire_u32(fl); t++) {
-        if (t >> 26) { atomicExch(err, 1u); return; }
+    for (uint32_t t = 0; !__reduce_or_sync(FULL, ld_acquire_u32(fl)); t++) {
+        if (__reduce_or_sync(FULL, ld_acquire_u32(err))) return;
+        if (t >> 26) {
+            if ((threadIdx.x & 31) == 0) atomicExch(err, 1u);
+            return;
+        }
         __nanosleep(256);
     }
 }

@@ -223,6 +223,53 @@ def test_decode_host_small(nf):
     assert out.is_pinned() and torch.equal(out, ref)
 
 
+def test_decode_host_rejects_bad_buffers():
+    """decode_host validates what the C side would copy: n x N float32 in,
+    n x K uint8 out, contiguous CPU tensors (a wrong size would make the
+    library read or write past the caller's buffers)."""
+    c, fr = _mk("C1")
+    dec = P.PolarSCS(fr, c["D"], c["L"], 0)
+    good = torch.zeros((4, dec.N), dtype=torch.float32)
+    with pytest.raises(ValueError):
+        dec.decode_host(torch.zeros((4, dec.N - 1), dtype=torch.float32))
+    with pytest.raises(ValueError):
+        dec.decode_host(torch.zeros(4 * dec.N, dtype=torch.float32))
+    with pytest.raises(ValueError):
+        dec.decode_host(good, torch.empty((3, dec.K), dtype=torch.uint8))
+    with pytest.raises(ValueError):
+        dec.decode_host(good, torch.empty((4, dec.K + 1), dtype=torch.uint8))
+    with pytest.raises(TypeError):
+        dec.decode_host(good, torch.empty((4, dec.K), dtype=torch.int32))
+    with pytest.raises(TypeError):
+        dec.decode_host(good, torch.empty((4, dec.K), dtype=torch.uint8, device="cuda"))
+    with pytest.raises(TypeError):
+        dec.decode_host(good, torch.empty((dec.K, 4), dtype=torch.uint8).t())
+    out = dec.decode_host(good, torch.empty((4, dec.K), dtype=torch.uint8))
+    assert out.shape == (4, dec.K)
+
+
+def test_decode_host_blocking_launches(tmp_path):
+    """With CUDA_LAUNCH_BLOCKING=1 the streaming pipeline (whose launch waits
+    for copies queued after it) is not used: the decode finishes promptly and
+    matches the device-resident decode."""
+    import subprocess
+    import sys
+    import os
+    code = (
+        "import sys, torch; sys.path.insert(0, %r)\n"
+        "import inputgen as ig, paper_1809_03606_b200 as P\n"
+        "c = ig.CONFIGS['C2']; fr = P.bhattacharyya_mask(c['N'], c['K'], c['design_db'])\n"
+        "dec = P.PolarSCS(fr, c['D'], c['L'], 0)\n"
+        "_, llr = dec.generate(1, 2.0, 0, 9001, want_block=False)\n"
+        "ref = dec.decode(llr).cpu()\n"
+        "out = torch.empty((9001, dec.K), dtype=torch.uint8, pin_memory=True)\n"
+        "dec.decode_host(llr.cpu().pin_memory(), out)\n"
+        "assert torch.equal(out, ref); print('ok')\n") % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, CUDA_LAUNCH_BLOCKING="1")
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
 def test_decode_host_chunked_ring_wraps():
     """The chunked pipeline's chunks (16 MiB ramping to 256 MiB) wrap its ring
     of 8 staging buffers: 1.6 GB of LLRs = 11 chunks, a ragged last one."""
