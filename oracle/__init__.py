@@ -46,7 +46,7 @@ class Counters(C.Structure):
     _fields_ = [(n, C.c_uint64) for n in (
         "pops", "switches", "f_ops", "g_ops", "spine_elems", "beta_xor_bits", "node_elems",
         "node_visits", "cand_created", "cand_inserted", "cand_replaced", "cand_dropped",
-        "pruned", "crc_checks", "sel_compares", "stack_peak", "key_compares")]
+        "pruned", "crc_checks", "sel_compares", "stack_peak", "key_compares", "fg_reuse")]
 
     def as_dict(self):
         return {n: int(getattr(self, n)) for n, _ in self._fields_}

@@ -438,10 +438,36 @@ static int key_less(const entry_t *a, const entry_t *b)
     return (a->pm < b->pm) || (a->pm == b->pm && a->serial < b->serial);
 }
 
+/* Reuse model (O10, counter fg_reuse only; no effect on any result): the f/g
+ * a decoder must evaluate if it keeps every alpha stage and recomputes a stage
+ * only when its inputs changed.  ALPHA(lam, phi) reads alpha_{lam+1} (node
+ * (lam+1, phi>>1)) and, for odd phi, the beta segment of its left sibling
+ * (Eq. 4); its result is identical to the stage's current
+ * content when the stage holds the same node, computed from the same version
+ * of stage lam+1 and the same beta segment.  Each stage is tagged with the
+ * node it holds, the version of its parent it was computed from, that beta
+ * segment and its own version (bumped on every evaluation).  Stage n (the
+ * channel) never changes.  A lower bound on the f/g of any stage-reusing
+ * decoder; Alg. 4's whole-spine recompute (f_ops + g_ops) is the upper one. */
+typedef struct {
+    int *node;          /* [n] phi held by stage s, -1 = none */
+    uint64_t *pver;     /* [n] version of stage s+1 it was computed from */
+    uint64_t *ver;      /* [n+1] current version of stage s (ver[n] = 0) */
+    uint8_t **bseg;     /* [n] beta segment used (odd phi) */
+    uint64_t next;
+} reuse_t;
+
+static void reuse_reset(reuse_t *rm, int n)
+{
+    for (int s = 0; s < n; s++) { rm->node[s] = -1; rm->pver[s] = 0; rm->ver[s] = 0; }
+    rm->ver[n] = 0;
+    rm->next = 1;
+}
+
 /* ALPHA(lam, phi) from stage lam+1 (Eq. 4, Alg. 1): f for even phi, g for odd
  * phi with beta_u = left-sibling segment of the flat beta.  */
 static void alpha_op(const orc_scs_t *h, float **alpha, const float *chan, const uint8_t *beta,
-                     int lam, int phi, orc_counters_t *ct, int spine)
+                     int lam, int phi, orc_counters_t *ct, int spine, reuse_t *rm)
 {
     int Lam = 1 << lam;
     const float *p = (lam + 1 == h->n) ? chan : alpha[lam + 1];
@@ -453,6 +479,18 @@ static void alpha_op(const orc_scs_t *h, float **alpha, const float *chan, const
     if (ct) {
         if (phi & 1) ct->g_ops += (uint64_t)Lam; else ct->f_ops += (uint64_t)Lam;
         if (spine) ct->spine_elems += (uint64_t)Lam;
+    }
+    if (rm) {
+        const uint8_t *b = beta + (size_t)(phi - 1) * (size_t)Lam;
+        int same = rm->node[lam] == phi && rm->pver[lam] == rm->ver[lam + 1] &&
+                   (!(phi & 1) || memcmp(rm->bseg[lam], b, (size_t)Lam) == 0);
+        if (!same) {
+            if (ct) ct->fg_reuse += (uint64_t)Lam;
+            rm->node[lam] = phi;
+            rm->pver[lam] = rm->ver[lam + 1];
+            rm->ver[lam] = rm->next++;
+            if (phi & 1) memcpy(rm->bseg[lam], b, (size_t)Lam);
+        }
     }
 }
 
@@ -472,7 +510,7 @@ static void read_block(const orc_scs_t *h, const uint8_t *xhat, uint8_t *tmp, ui
 static int decode_one(const orc_scs_t *h, const float *chan, uint8_t *block, uint8_t *xhat,
                       float *pm_out, uint32_t *pops_out, uint32_t *sw_out, uint8_t *st_out,
                       orc_counters_t *ct, float **alpha, entry_t *S, uint8_t *beta_work,
-                      uint8_t *best_beta, int *cnt, float *tmp, uint8_t *seg_base, uint8_t *seg)
+                      uint8_t *best_beta, int *cnt, float *tmp, uint8_t *seg_base, uint8_t *seg, reuse_t *rm)
 {
     const int N = h->N, D = h->D;
     int nS = 0;
@@ -480,6 +518,7 @@ static int decode_one(const orc_scs_t *h, const float *chan, uint8_t *block, uin
     int have_best = 0;
     float best_pm = 0.0f;
     for (int j = 0; j <= h->M; j++) cnt[j] = 0;
+    if (rm) reuse_reset(rm, h->n);
 
     /* Init: the root path (PM 0, serial 0, k 0, j 0, PL 0) */
     S[0].pm = 0.0f; S[0].serial = 0; S[0].k = 0; S[0].j = 0; S[0].pl = 0;
@@ -543,11 +582,11 @@ static int decode_one(const orc_scs_t *h, const float *chan, uint8_t *block, uin
                     /* Alg. 4 (typos per R12): recompute the
                      * ancestors of (lam, phi) from the channel downwards */
                     for (int s = h->n - 1; s > lam; s--)
-                        alpha_op(h, alpha, chan, beta_work, s, phi >> (s - lam), ct, 1);
+                        alpha_op(h, alpha, chan, beta_work, s, phi >> (s - lam), ct, 1, rm);
                     spine_dirty = 0;
-                    alpha_op(h, alpha, chan, beta_work, lam, phi, ct, 1);
+                    alpha_op(h, alpha, chan, beta_work, lam, phi, ct, 1, rm);
                 } else {
-                    alpha_op(h, alpha, chan, beta_work, lam, phi, ct, 0);
+                    alpha_op(h, alpha, chan, beta_work, lam, phi, ct, 0, rm);
                 }
             }
             k++;
@@ -635,16 +674,28 @@ int orc_scs_decode(const orc_scs_t *h, const float *llr, int64_t n_frames,
     float *tmp = (float *)malloc(sizeof(float) * (size_t)N);
     uint8_t *seg_base = (uint8_t *)malloc((size_t)N);
     uint8_t *seg = (uint8_t *)malloc((size_t)N);
+    reuse_t rm = { 0 }, *rmp = NULL;
     int ok = alpha && S && beta_work && best_beta && cnt && tmp && seg_base && seg;
     for (int l = 0; ok && l < h->n; l++) ok = (alpha[l] = (float *)malloc(sizeof(float) * ((size_t)1 << l))) != NULL;
+    if (ok && counters) {
+        rm.node = (int *)calloc((size_t)h->n + 1, sizeof(int));
+        rm.pver = (uint64_t *)calloc((size_t)h->n + 1, sizeof(uint64_t));
+        rm.ver = (uint64_t *)calloc((size_t)h->n + 1, sizeof(uint64_t));
+        rm.bseg = (uint8_t **)calloc((size_t)h->n + 1, sizeof(uint8_t *));
+        ok = rm.node && rm.pver && rm.ver && rm.bseg;
+        for (int l = 0; ok && l < h->n; l++) ok = (rm.bseg[l] = (uint8_t *)malloc((size_t)1 << l)) != NULL;
+        rmp = &rm;
+    }
     for (int e = 0; ok && e < D + 1; e++) ok = (S[e].beta = (uint8_t *)malloc((size_t)N)) != NULL;
     if (!ok) rc = -1;
     for (int64_t f = 0; ok && f < n_frames; f++) {
         decode_one(h, llr + f * N, block ? block + f * h->K : NULL, xhat ? xhat + f * N : NULL,
                    pm ? pm + f : NULL, pops ? pops + f : NULL, switches ? switches + f : NULL,
                    status ? status + f : NULL, counters, alpha, S, beta_work, best_beta, cnt, tmp,
-                   seg_base, seg);
+                   seg_base, seg, rmp);
     }
+    if (rm.bseg) for (int l = 0; l < h->n; l++) free(rm.bseg[l]);
+    free(rm.node); free(rm.pver); free(rm.ver); free(rm.bseg);
     if (alpha) for (int l = 0; l < h->n; l++) free(alpha[l]);
     if (S) for (int e = 0; e < D + 1; e++) free(S[e].beta);
     free(alpha); free(S); free(beta_work); free(best_beta); free(cnt); free(tmp); free(seg_base); free(seg);

@@ -93,7 +93,11 @@ typedef struct {
     uint64_t sel_compares;
     uint64_t stack_peak;            /* stack decoder: max live entries seen (a max, not a sum) */
     uint64_t key_compares;          /* stack decoder: entries examined by the linear searches
-                                       (selection, L793, and worst-entry search, L599) */          /* list decoder: prune cost, sum over nodes of T ceil(log2 T), T = candidates */
+                                       (selection, L793, and worst-entry search, L599) */
+    uint64_t fg_reuse;              /* stack decoder: f/g of the stage-reuse model (alpha_op in
+                                       oracle.c): a lower bound on what a decoder that keeps the
+                                       alpha stages must evaluate; f_ops + g_ops (Alg. 4 spines)
+                                       is the upper bound */
 } orc_counters_t;
 
 orc_scs_t *orc_scs_create(int N, const uint8_t *frozen, int D, int L, uint32_t crc_poly, int bit_level);

@@ -389,6 +389,77 @@ def test_engine_noiseless(cfg, bit_level):
     assert (r["pm"] == 0).all() and (r["status"] == 0).all()
 
 
+# ------------------------------------------------------------------ O10 counters
+# SURVEY.md §8(d) census (a scratch script independent of the oracle): M,
+# clean-pass f/g elements (sum of Lambda over ALPHA ops), BETA bits
+CENSUS = {"C1": (14, 416, 208), "C2": (74, 5252, 2626), "C4": (119, 11332, 5666), "C5": (181, 23896, 11948)}
+
+
+@pytest.mark.parametrize("cfg", ["C1", "C2", "C4", "C5"])
+def test_counters_noiseless_closed_forms(cfg):
+    """O10 on noiseless frames: one clean pass (Fig. 5): f+g =
+    the ALPHA census, BETA bits = the BETA census, no spine recompute (no
+    switch), node elements = N (the nodes partition [0, N)), pops = M+1, and
+    the stage-reuse model evaluates exactly the clean pass."""
+    c = ig.CONFIGS[cfg]
+    M, fg, bb = CENSUS[cfg]
+    fr = O.bhattacharyya_mask(c["N"], c["K"], c["design_db"])
+    dec = O.SCSDecoder(fr, c["D"], c["L"], c["crc_poly"])
+    cc = O.crc_degree(c["crc_poly"]) if c["crc_poly"] else 0
+    nf = 3
+    blk = O.crc_attach(ig.payload_bits(9, 0, nf, c["K"] - cc), c["crc_poly"])
+    cw = O.encode_systematic(fr, blk)
+    ct = dec.decode(4.0 * (1 - 2 * cw.astype(np.float32)), counters=True)["counters"]
+    assert ct["f_ops"] + ct["g_ops"] == nf * fg
+    assert ct["beta_xor_bits"] == nf * bb
+    assert ct["spine_elems"] == 0 and ct["switches"] == 0
+    assert ct["node_elems"] == nf * c["N"] and ct["node_visits"] == nf * M
+    assert ct["pops"] == nf * (M + 1)
+    assert ct["fg_reuse"] == nf * fg
+    assert ct["crc_checks"] == (nf if cc else 0)
+
+
+@pytest.mark.parametrize("D,key_compares,dropped", [(16, 12, 0), (4, 27, 5)])
+def test_counters_hand_traced_pc8(D, key_compares, dropped):
+    """O10 on one hand-traced frame: PC(8,4), A = {3,5,6,7},
+    schedule ALPHA(2,0) REP(2,0) ALPHA(2,1) SPC(2,1) BETA(2,1) (Fig. 5), all
+    LLRs = +1.  Pop 1 (root, 1 live entry): 4 f -> alpha = (1,1,1,1); REP
+    candidates 0000 (dPM 0) and 1111 (dPM 4).  Pop 2 (2 live): 4 g with
+    beta = 0000 -> alpha = (2,2,2,2); SPC: parity 0, 8 candidates {} (0), six
+    pairs (4 each), all four (8).  c1 takes the freed slot; with D = 16 all
+    fit; with D = 4 two siblings fit and the other five each scan the 4 live
+    entries (L599) and are dropped (4 < 4 is false).  Pop 3 (complete path,
+    D = 16: 9 live; D = 4: 4 live): BETA(2,1), 4 bits.  key_compares =
+    1 + 2 + 9 = 12 (D = 16) and 1 + 2 + 5 x 4 + 4 = 27 (D = 4)."""
+    fr = np.array([1, 1, 1, 0, 1, 0, 0, 0], np.uint8)
+    assert np.array_equal(O.bhattacharyya_mask(8, 4, 2.0), fr)
+    r = O.SCSDecoder(fr, D, 8, 0).decode(np.ones((1, 8), np.float32), counters=True)
+    ct = r["counters"]
+    assert r["pops"][0] == 3 and r["switches"][0] == 0 and r["pm"][0] == 0
+    assert (ct["f_ops"], ct["g_ops"], ct["spine_elems"], ct["fg_reuse"]) == (4, 4, 0, 8)
+    assert (ct["node_visits"], ct["node_elems"], ct["beta_xor_bits"]) == (2, 8, 4)
+    assert ct["cand_created"] == 10 and ct["cand_dropped"] == dropped and ct["cand_replaced"] == 0
+    assert ct["cand_inserted"] == 10 - dropped
+    assert ct["key_compares"] == key_compares
+    assert ct["stack_peak"] == (9 if D == 16 else 4)
+
+
+def test_counters_reuse_model_bounds():
+    """fg_reuse (the stage-reuse model) lies between the clean pass and the
+    Alg. 4 count (f+g, whole-spine recomputes) on noisy
+    frames, and equals f+g minus the spines exactly when nothing switches."""
+    c = ig.CONFIGS["C2"]
+    fr = O.bhattacharyya_mask(c["N"], c["K"], c["design_db"])
+    dec = O.SCSDecoder(fr, c["D"], c["L"], 0)
+    _, _, llr = _noisy(fr, 0, 1.0, 24, 3)
+    for i in range(llr.shape[0]):
+        r = dec.decode(llr[i:i + 1], counters=True)
+        ct = r["counters"]
+        assert CENSUS["C2"][1] <= ct["fg_reuse"] <= ct["f_ops"] + ct["g_ops"]
+        if ct["switches"] == 0:
+            assert ct["fg_reuse"] == ct["f_ops"] + ct["g_ops"] - ct["spine_elems"]
+
+
 @pytest.mark.parametrize("cfg", ["C1", "C2"])
 def test_bit_level_D1_and_L1_equal_textbook_sc(cfg):
     """SCS with D=1 (and with L=1) is plain SC: bit-exact vs O6 (north-star check 2)."""

@@ -158,9 +158,47 @@ def _crc_ok(block, poly):
     return [(reg >> (c - 1 - i)) & 1 for i in range(c)] == [int(x) for x in block[-c:]]
 
 
-def scs_reference(frozen, llr, D, L, poly, bit_level):
+def _work_of_pop(nodes, n, j, switched):
+    """What the reduced-memory engine (SCS-RM with Alg. 4)
+    evaluates when it pops a path of depth j, derived here from the node
+    positions alone: the BETA ops that finish node j-1 (it climbs while it is
+    a right child), then the ALPHA ops from the lowest common ancestor of
+    nodes j-1 and j down to node j; on a path switch the first of them
+    recomputes the whole spine from the channel (Alg. 4).  Returns
+    (f, g, spine, beta_bits)."""
+    beta_bits = 0
+    if j > 0:
+        _, plam, pphi = nodes[j - 1]
+        l, ph = plam, pphi
+        while ph & 1 and l < n:
+            beta_bits += 1 << l
+            ph >>= 1
+            l += 1
+    if j == len(nodes):
+        return 0, 0, 0, beta_bits
+    _, lam, phi = nodes[j]
+    start = phi << lam
+    top = n if start == 0 else (start ^ (start - 1)).bit_length()   # level of the LCA of bits start-1, start
+    f = g = spine = 0
+    first = top - 1
+    hi = n - 1 if switched else first
+    for s in range(hi, lam - 1, -1):
+        psi = phi >> (s - lam)
+        if psi & 1:
+            g += 1 << s
+        else:
+            f += 1 << s
+        if switched and s >= first:
+            spine += 1 << s
+    return f, g, spine, beta_bits
+
+
+def scs_reference(frozen, llr, D, L, poly, bit_level, counters=None):
     """plain SCS: entries keep their decided node words; returns
-    (bits, pm, pops, switches, status)"""
+    (bits, pm, pops, switches, status).  counters (a dict) receives the O10
+    work counts of the reduced-memory engine, computed independently:
+    f, g, spine, beta_bits (_work_of_pop), node_elems, key_compares (live
+    entries examined by the linear searches)."""
     n = frozen.size.bit_length() - 1
     nodes = _nodes(frozen, bit_level)
     M = len(nodes)
@@ -169,18 +207,25 @@ def scs_reference(frozen, llr, D, L, poly, bit_level):
     cnt = [0] * (M + 1)
     next_serial, work, pops, switches = 1, 0, 0, 0
     best = None
+    ct = counters if counters is not None else {}
+    for k in ("f", "g", "spine", "beta_bits", "node_elems", "key_compares"):
+        ct[k] = 0
     while True:
         if not S:                                          # reading R13
             return best[0], best[1], pops, switches, 1
+        ct["key_compares"] += len(S)
         w = min(range(len(S)), key=lambda e: (S[e][0], S[e][1]))
         pm, ser, j, words = S.pop(w)
         pops += 1
         cnt[j] += 1
         if cnt[j] == L:                                    # PAPER.md:L595 (R9)
             S = [e for e in S if e[2] > j]
-        if ser != work:
+        switched = ser != work
+        if switched:
             switches += 1
             work = ser
+        for k, v in zip(("f", "g", "spine", "beta_bits"), _work_of_pop(nodes, n, j, switched)):
+            ct[k] += v
         if j == M:
             blk = _beta(words, n, 0)[info]
             if _crc_ok(blk, poly):
@@ -189,6 +234,7 @@ def scs_reference(frozen, llr, D, L, poly, bit_level):
                 best = (blk, pm)
             continue
         kind, lam, phi = nodes[j]
+        ct["node_elems"] += 1 << lam
         cands = _candidates(kind, _node_alpha(llr, words, lam, phi))
         ser0 = next_serial
         next_serial += len(cands)
@@ -203,6 +249,7 @@ def scs_reference(frozen, llr, D, L, poly, bit_level):
             if len(S) < D:
                 S.append(e)
             else:
+                ct["key_compares"] += len(S)
                 wi = max(range(len(S)), key=lambda k: (S[k][0], S[k][1]))
                 if e[0] < S[wi][0]:
                     S[wi] = e
@@ -231,6 +278,33 @@ def test_scs_rm_equals_plain_scs(N, K, db, bit_level):
             assert st == ref["status"][i], ctx
             assert F32(pm) == ref["pm"][i], ctx
             assert np.array_equal(bits, ref["bits"][i]), ctx
+
+
+@pytest.mark.parametrize("N,K,db", CASES)
+@pytest.mark.parametrize("bit_level", [True, False])
+def test_o10_counters_equal_plain_scs_work(N, K, db, bit_level):
+    """O10 pin: the oracle's per-frame work counters equal the work of the
+    same search derived independently from the node positions
+    (_work_of_pop) and the plain stack's live entries: f and g evaluations
+    (clean pass + Alg. 4 spines), spine elements, BETA
+    bits, node elements and key compares (PAPER.md:L793,
+    L599)."""
+    fr = O.bhattacharyya_mask(N, K, db)
+    for D, L, poly in [(4, 2, 0), (3, 64, 0), (16, 2, 0x107 if K > 8 else 0), (64, 1 << 16, 0)]:
+        pay = ig.payload_bits(3 * N + K + D, 0, 24, K - (O.crc_degree(poly) if poly else 0))
+        cw = O.encode_systematic(fr, O.crc_attach(pay, poly))
+        llr = O.awgn_llr(cw, ig.unit_normals(3 * N + K + D, 0, 24, N), 0.5, K / N)
+        dec = O.SCSDecoder(fr, D, L, poly, bit_level=bit_level)
+        for i in range(llr.shape[0]):
+            oc = dec.decode(llr[i:i + 1], counters=True)["counters"]
+            rc = {}
+            scs_reference(fr, llr[i], D, L, poly, bit_level, counters=rc)
+            ctx = f"N{N} K{K} D{D} L{L} poly{poly:#x} bit{bit_level} frame {i}"
+            assert (oc["f_ops"], oc["g_ops"], oc["spine_elems"]) == (rc["f"], rc["g"], rc["spine"]), ctx
+            assert oc["beta_xor_bits"] == rc["beta_bits"], ctx
+            assert oc["node_elems"] == rc["node_elems"], ctx
+            assert oc["key_compares"] == rc["key_compares"], ctx
+            assert oc["fg_reuse"] <= oc["f_ops"] + oc["g_ops"], ctx
 
 
 def scl_reference(frozen, llr, L, poly, bit_level):
