@@ -150,6 +150,22 @@ int polar_scs_decode_stats(polar_scs_t h, const float *llr, int64_t n_frames, ui
                            void *stream);
 
 /*
+ * Instrumented decode for roofline accounting: the same decode as
+ * polar_scs_decode (identical out_bits) by an instance of the kernel that
+ * also counts, per frame, the work it executed:
+ *   counts: device [n_frames][4] uint32, 16-byte aligned:
+ *     [0] f/g evaluations (Eq. 4; Alg. 4 spines after a switch start at the
+ *         first alpha stage whose node or beta prefix changed, reading R12),
+ *     [1] bits XOR-ed by BETA ops,
+ *     [2] node elements (sum of Lambda over decision-node visits, L846),
+ *     [3] 32-bit words moved into or out of beta snapshots (L854).
+ * Slower than polar_scs_decode (a generic, unspecialised instance): for
+ * measurement, not for throughput.  Errors as polar_scs_decode.
+ */
+int polar_scs_decode_counts(polar_scs_t h, const float *llr, int64_t n_frames, uint8_t *out_bits,
+                            uint32_t *counts, void *stream);
+
+/*
  * Decode n_frames independent frames with the FSSCL LIST decoder (PAPER.md:
  * L505-519 SCL; L521-587 fast-simplified node path creation; L772-780 list
  * memory with lazy copy), list size = the handle's L (the visit limit that

@@ -56,6 +56,7 @@ _SIGS = {
     "polar_scs_strerror": ([C.c_int], C.c_char_p),
     "polar_scs_decode": ([_vp, _vp, _i64, _vp, _vp], C.c_int),
     "polar_scs_decode_stats": ([_vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _vp], C.c_int),
+    "polar_scs_decode_counts": ([_vp, _vp, _i64, _vp, _vp, _vp], C.c_int),
     "polar_scs_decode_host": ([_vp, _vp, _i64, _vp, _vp], C.c_int),
     "polar_scl_decode": ([_vp, _vp, _i64, _vp, _vp, _vp, _vp], C.c_int),
     "polar_scl_decode_host": ([_vp, _vp, _i64, _vp, _vp], C.c_int),
@@ -195,6 +196,18 @@ class PolarSCS:
                                       bits.data_ptr(), pm.data_ptr(), pops.data_ptr(), sw.data_ptr(),
                                       st.data_ptr(), _stream_ptr(stream)), "polar_scs_decode_stats")
         return {"bits": bits, "pm": pm, "pops": pops, "switches": sw, "status": st}
+
+    def decode_counts(self, llr, stream=None):
+        """Instrumented decode (polar_scs_decode_counts): bits plus the work the
+        kernel executed per frame, int32 [n, 4] = (f/g evaluations, BETA XOR
+        bits, node elements, snapshot words)."""
+        import torch
+        n = llr.shape[0]
+        bits = torch.empty((n, self.K), dtype=torch.uint8, device=llr.device)
+        counts = torch.empty((n, 4), dtype=torch.int32, device=llr.device)
+        _check(polar_scs_decode_counts(self._h, _dev(llr, torch.float32, (n, self.N), "llr"), n, bits.data_ptr(),
+                                       counts.data_ptr(), _stream_ptr(stream)), "polar_scs_decode_counts")
+        return {"bits": bits, "counts": counts}
 
     def decode_list(self, llr, out=None, stats=True, stream=None):
         """FSSCL list decoding with list size L (polar_scl_decode).

@@ -17,6 +17,7 @@ namespace polar {
 cudaError_t launch_decode(const DecodeParams &p, int slots, bool snap_smem, bool chan_smem, int ctas, int smem,
                           cudaStream_t st);
 cudaError_t decode_occupancy(int n, int slots, bool snap_smem, bool chan_smem, int mode, int smem, int *blocks_per_sm);
+cudaError_t launch_decode_counts(const DecodeParams &p, int slots, int ctas, int smem, cudaStream_t st);
 cudaError_t launch_list(const ListParams &p, int lcap, int ctas, int smem, cudaStream_t st);
 cudaError_t list_occupancy(int lcap, int n, int L, int smem, int *blocks_per_sm);
 cudaError_t launch_list_packed(const ListParams &p, int ctas, int smem, cudaStream_t st);
@@ -105,7 +106,8 @@ struct StreamArgs {
 };
 
 int decode_impl(polar_scs_t h, const float *llr, int64_t n, uint8_t *bits, float *pm, uint32_t *pops,
-                uint32_t *sw, uint8_t *status, cudaStream_t st, int slot = 0, const StreamArgs *sa = nullptr) {
+                uint32_t *sw, uint8_t *status, cudaStream_t st, int slot = 0, const StreamArgs *sa = nullptr,
+                uint32_t *counts = nullptr) {
     DecodeParams p = h->base;
     if (sa) { p.ready = sa->ready; p.err = sa->err; p.chunk_shift = sa->shift; }
     p.llr = llr; p.n_frames = n; p.out_bits = bits;
@@ -117,6 +119,12 @@ int decode_impl(polar_scs_t h, const float *llr, int64_t n, uint8_t *bits, float
     if (h->d_hdr) p.hdr_global = h->d_hdr + h->hdr_count * (size_t)slot;
     cudaError_t e = cudaMemsetAsync(p.queue, 0, sizeof(unsigned long long), st);
     if (e != cudaSuccess) return cuda_status(e);
+    if (counts) {
+        p.counts = counts;
+        p.chan_in_smem = h->chan_in_smem;
+        p.snap_in_smem = h->snap_in_smem;
+        return cuda_status(launch_decode_counts(p, slots_for(h->D), h->ctas, h->smem_per_cta, st));
+    }
     return cuda_status(launch_decode(p, slots_for(h->D), h->snap_in_smem != 0, h->chan_in_smem != 0, h->ctas,
                                      h->smem_per_cta, st));
 }
@@ -417,6 +425,19 @@ int polar_scs_decode_stats(polar_scs_t h, const float *llr, int64_t n, uint8_t *
 
 int polar_scs_decode(polar_scs_t h, const float *llr, int64_t n, uint8_t *bits, void *stream) {
     return polar_scs_decode_stats(h, llr, n, bits, nullptr, nullptr, nullptr, nullptr, stream);
+}
+
+int polar_scs_decode_counts(polar_scs_t h, const float *llr, int64_t n, uint8_t *bits, uint32_t *counts,
+                            void *stream) {
+    if (!h || n < 0) return POLAR_EINVAL;
+    if (n == 0) return POLAR_OK;
+    DeviceGuard g(h);
+    if (!g.ok) return POLAR_ECUDA;
+    if (!llr || !bits || !counts) return POLAR_EINVAL;
+    if (h->t.N >= 4 && (reinterpret_cast<uintptr_t>(llr) & 15u)) return POLAR_EINVAL;
+    if (reinterpret_cast<uintptr_t>(counts) & 15u) return POLAR_EINVAL;
+    return decode_impl(h, llr, n, bits, nullptr, nullptr, nullptr, nullptr, static_cast<cudaStream_t>(stream), 0,
+                       nullptr, counts);
 }
 
 int polar_scl_decode(polar_scs_t h, const float *llr, int64_t n, uint8_t *bits, float *pm, uint8_t *status,

@@ -243,7 +243,7 @@ __device__ __forceinline__ int alloc_snapshot_big(uint32_t *used, int &uhint, co
 // specialisations trade registers for warps (measured)
 template <int SLOTS, int NL, bool NOCRC>
 constexpr int kDecodeMinBlocksFor() {
-    return NL == 11 ? 6 : (NL == 12 ? 5 : (SLOTS == 4 ? 3 : (SLOTS == 2 ? 5 : kDecodeMinBlocks)));
+    return NL == 11 ? 6 : (NL == 12 ? 5 : (SLOTS == 4 ? 3 : (SLOTS == 2 ? 5 : (NOCRC && SLOTS == 1 ? 9 : kDecodeMinBlocks))));
 }
 
 // SLOTS = 1, 2, 4: register stack of 32 SLOTS entries (D <= 128).  SLOTS = 0:
@@ -252,7 +252,10 @@ constexpr int kDecodeMinBlocksFor() {
 // MODE (compile time): 0 general; 1 systematic readout and more than one node
 // (re-encoding and whole-code-node paths left out of the code); 2 as 1 and no
 // CRC (the CRC path left out too)
-template <int SLOTS, bool SNAP_SMEM, bool CHAN_SMEM, int NL = 0, bool GA = false, int MODE = 0>
+// CNT: the instrumented instance behind polar_scs_decode_counts — the same
+// decode, placement read from the parameters, and per frame the work it
+// executed: f/g evaluations, BETA XOR bits, node elements, snapshot words
+template <int SLOTS, bool SNAP_SMEM, bool CHAN_SMEM, int NL = 0, bool GA = false, int MODE = 0, bool CNT = false>
 __global__ void __launch_bounds__(kDecodeWarps * 32, kDecodeMinBlocksFor<SLOTS, NL, MODE == 2>())
 fsscs_decode_kernel(const DecodeParams P) {
     constexpr bool BIG = (SLOTS == 0);
@@ -283,15 +286,17 @@ fsscs_decode_kernel(const DecodeParams P) {
     // BIG: the first KW stack keys live in shared memory (the rest in global)
     constexpr int KW = 128;
     unsigned long long *wkey = reinterpret_cast<unsigned long long *>(wb);
-    float *chan_s = reinterpret_cast<float *>(wb + P.win_words);   // channel row (CHAN_SMEM)
-    float *alpha = CHAN_SMEM ? chan_s + N : chan_s;                // stages >= 6 (+ scratch)
+    const bool chan_sm = CNT ? (P.chan_in_smem != 0) : CHAN_SMEM;
+    const bool snap_sm = CNT ? (P.snap_in_smem != 0) : SNAP_SMEM;
+    float *chan_s = reinterpret_cast<float *>(wb + P.win_words);   // channel row (chan_sm)
+    float *alpha = chan_sm ? chan_s + N : chan_s;                  // stages >= 6 (+ scratch)
     uint32_t *beta = reinterpret_cast<uint32_t *>(alpha + P.alpha_words);
     // stage t lives at [2^t, 2^{t+1}) of the shared alpha memory, or of this
     // warp's global (L2) arena for t >= sg (sg = n: everything in shared memory)
     const int sg = P.sg;
     float *galpha = P.galpha ? P.galpha + (size_t)(blockIdx.x * kDecodeWarps + warp) * (size_t)N : alpha;
     auto SP = [&](int t) -> float * {
-        if constexpr (GA) return (t >= sg ? galpha : alpha) + (1 << t);
+        if constexpr (GA || CNT) return (t >= sg ? galpha : alpha) + (1 << t);
         return alpha + (1 << t);
     };
     uint32_t *best = beta + nw;
@@ -317,7 +322,7 @@ fsscs_decode_kernel(const DecodeParams P) {
     const int sstride = (NL > 0) ? nw : P.snap_stride;
     auto snap_slot = [&](int k) -> uint32_t * {
         POLAR_DCHECK(k >= 0 && k < D);
-        if (SNAP_SMEM) return snap_s + k * sstride;
+        if (snap_sm) return snap_s + k * sstride;
         return P.snap_global + (size_t)(snap0 + (uint32_t)k) * (size_t)sstride;
     };
 
@@ -343,8 +348,8 @@ fsscs_decode_kernel(const DecodeParams P) {
 
         // ---- the channel row (the only mandatory HBM read) -----------------
         const float *row = P.llr + (size_t)f * N;
-        const float *chan = CHAN_SMEM ? chan_s : row;
-        if (CHAN_SMEM) {
+        const float *chan = chan_sm ? chan_s : row;
+        if (chan_sm) {
             if (N >= 4) {
                 #pragma unroll 1
                 for (int i = lane * 4; i < N; i += 128)
@@ -375,6 +380,7 @@ fsscs_decode_kernel(const DecodeParams P) {
         }
         __syncwarp();
         uint32_t work = 0, next_serial = 1, pops = 0, switches = 0;
+        uint32_t c_fg = 0, c_bb = 0, c_ne = 0, c_sw = 0;     // CNT: executed work of this frame
         int work_pl = 0;
         // alpha memory content: stages s >= lev_mem hold the node (s, pos_mem >> s)
         // for the working path's beta (partial-spine reuse, reading R12)
@@ -520,6 +526,7 @@ fsscs_decode_kernel(const DecodeParams P) {
                             const int slot = alloc_snapshot_big(snap_used, uhint, sjsm, nA, D, hole, PK::snap(p_jsm), lane);
                             uint32_t *dst = snap_slot(slot);
                             const int nwords = (work_pl + 31) >> 5;
+                            if constexpr (CNT) c_sw += (uint32_t)nwords;
                             #pragma unroll 1
                             for (int w = lane; w < nwords; w += 32) dst[w] = beta[w];
                             if (lane == 0) sjsm[wi] = PK::make(PK::j(wj), (uint32_t)slot, 0);
@@ -542,6 +549,7 @@ fsscs_decode_kernel(const DecodeParams P) {
                         const int slot = alloc_snapshot_lazy<SL>(snap_used, s_ser, s_jsm, D, -1, 0, jsm_snap(p_jsm), lane);
                         uint32_t *dst = snap_slot(slot);
                         const int nwords = (work_pl + 31) >> 5;
+                        if constexpr (CNT) c_sw += (uint32_t)nwords;
                         #pragma unroll 1
                         for (int w = lane; w < nwords; w += 32) dst[w] = beta[w];
                         if (lane == wl) {
@@ -556,13 +564,14 @@ fsscs_decode_kernel(const DecodeParams P) {
                 const uint32_t ps = PK::snap(p_jsm), rel = PK::mask(p_jsm);
                 const uint32_t *src = snap_slot((int)ps);
                 const int nwords = (pl + 31) >> 5;
+                if constexpr (CNT) c_sw += (uint32_t)nwords;
                 int d = 0x7FFFFFFF;
                 #pragma unroll 1
                 for (int w0 = 0; w0 < nwords; w0 += 32) {
                     const int w = w0 + lane;
                     uint32_t x = 0;
                     if (w < nwords) {
-                        const uint32_t nv = SNAP_SMEM ? src[w] : __ldcg(src + w);
+                        const uint32_t nv = snap_sm ? src[w] : __ldcg(src + w);
                         x = nv ^ beta[w];
                         if (w == nwords - 1 && (pl & 31)) x &= (1u << (pl & 31)) - 1u;
                         beta[w] = nv;
@@ -617,6 +626,7 @@ fsscs_decode_kernel(const DecodeParams P) {
                     while ((ph & 1) && l < 5) {
                         const int o = ((ph - 1) << l) & 31, Lm = 1 << l;
                         x ^= ((x >> (o + Lm)) & ((1u << Lm) - 1u)) << o;
+                        if constexpr (CNT) c_bb += (uint32_t)Lm;
                         ph >>= 1;
                         l++;
                     }
@@ -624,7 +634,12 @@ fsscs_decode_kernel(const DecodeParams P) {
                     __syncwarp();
                 }
                 #pragma unroll 1
-                while (ph & 1) { beta_op(beta, l, ph, lane); ph >>= 1; l++; }
+                while (ph & 1) {
+                    beta_op(beta, l, ph, lane);
+                    if constexpr (CNT) c_bb += 1u << l;
+                    ph >>= 1;
+                    l++;
+                }
             }
 
             if (j == M) {
@@ -700,6 +715,7 @@ fsscs_decode_kernel(const DecodeParams P) {
 #define POLAR_SSTAGE(T)                                                                       \
     if constexpr ((T) < NL && (T) >= 6) {                                                     \
         if ((T) < lam) break;                                                                 \
+        if constexpr (CNT) c_fg += 1u << (T);                                                 \
         alpha_stage<CHAN_SMEM, (NL == 10 && SLOTS == 1)>((T) + 1 == n ? chan : SP((T) + 1), SP(T), beta, n, (T), pl >> (T), lane); \
     }
                     switch (s_hi) {
@@ -715,8 +731,10 @@ fsscs_decode_kernel(const DecodeParams P) {
 #undef POLAR_SSTAGE
                 } else {
                     #pragma unroll 1
-                    for (int s = s_hi; s >= max(lam, 6); s--)
+                    for (int s = s_hi; s >= max(lam, 6); s--) {
+                        if constexpr (CNT) c_fg += 1u << s;
                         alpha_stage<CHAN_SMEM>(s + 1 == n ? chan : SP(s + 1), SP(s), beta, n, s, pl >> s, lane);
+                    }
                 }
                 // register stages (Lambda <= 32): lo = element i, hi = element i + Lambda
                 // by shuffle; enter the cascade at the first stage to compute, leave
@@ -744,6 +762,7 @@ fsscs_decode_kernel(const DecodeParams P) {
             r[T] = f_minsum(lo, hi);                                                       \
         }                                                                                  \
         xr = r[T];                                                                         \
+        if constexpr (CNT) c_fg += Lt;                                                     \
         if (lam == (T)) break;                                                             \
     }
                 if (lam <= 5) {
@@ -774,6 +793,7 @@ fsscs_decode_kernel(const DecodeParams P) {
 
             // ---- decision node ----------
             const int Lam = 1 << lam;
+            if constexpr (CNT) c_ne += (uint32_t)Lam;
             const int seg = phi << lam;
             float *a = SP(lam);               // node alpha (Lambda > 32)
             if (Lam <= 32) {
@@ -956,6 +976,7 @@ fsscs_decode_kernel(const DecodeParams P) {
                 else fslot = alloc_snapshot_lazy<SL>(snap_used, s_ser, s_jsm, D, victim_lane, victim_slot, SNAP_NONE, lane);
                 uint32_t *dst = snap_slot(fslot);
                 const int nwords = (npl + 31) >> 5;
+                if constexpr (CNT) c_sw += (uint32_t)nwords;
                 #pragma unroll 1
                 for (int w = lane; w < nwords; w += 32) dst[w] = beta[w];
                 if (lane == 0) *hdr_at(fslot) = make_uint2(mi[0] | (mi[1] << 16), mi[2] | (mi[3] << 16));
@@ -1079,6 +1100,11 @@ fsscs_decode_kernel(const DecodeParams P) {
                 if (P.pops) P.pops[f] = pops;
                 if (P.switches) P.switches[f] = switches;
                 if (P.status) P.status[f] = (uint8_t)status;
+                if constexpr (CNT) {
+                    uint4 cw;
+                    cw.x = c_fg; cw.y = c_bb; cw.z = c_ne; cw.w = c_sw;
+                    reinterpret_cast<uint4 *>(P.counts)[f] = cw;
+                }
             }
             __syncwarp();
         }
@@ -1087,9 +1113,9 @@ fsscs_decode_kernel(const DecodeParams P) {
     }
 }
 
-template <int SLOTS, bool SM, bool CS, int NL = 0, bool GA = false, int MODE = 0>
+template <int SLOTS, bool SM, bool CS, int NL = 0, bool GA = false, int MODE = 0, bool CNT = false>
 static cudaError_t launch_t(const DecodeParams &p, int ctas, int smem, cudaStream_t st) {
-    auto kern = fsscs_decode_kernel<SLOTS, SM, CS, NL, GA, MODE>;
+    auto kern = fsscs_decode_kernel<SLOTS, SM, CS, NL, GA, MODE, CNT>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     kern<<<ctas, kDecodeWarps * 32, smem, st>>>(p);
@@ -1139,6 +1165,15 @@ cudaError_t launch_decode(const DecodeParams &p, int slots, bool snap_smem, bool
     }
     if (snap_smem) return chan_smem ? launch_s<true, true>(p, slots, ctas, smem, st) : launch_s<true, false>(p, slots, ctas, smem, st);
     return chan_smem ? launch_s<false, true>(p, slots, ctas, smem, st) : launch_s<false, false>(p, slots, ctas, smem, st);
+}
+
+// polar_scs_decode_counts: the generic instance with CNT (placement from the
+// parameters, any layout the handle chose)
+cudaError_t launch_decode_counts(const DecodeParams &p, int slots, int ctas, int smem, cudaStream_t st) {
+    if (slots == 0) return launch_t<0, false, false, 0, false, 0, true>(p, ctas, smem, st);
+    if (slots == 1) return launch_t<1, false, false, 0, false, 0, true>(p, ctas, smem, st);
+    if (slots == 2) return launch_t<2, false, false, 0, false, 0, true>(p, ctas, smem, st);
+    return launch_t<4, false, false, 0, false, 0, true>(p, ctas, smem, st);
 }
 
 template <int S, bool B, bool C, int NL = 0, bool GA = false, int MODE = 0>

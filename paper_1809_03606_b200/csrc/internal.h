@@ -71,6 +71,8 @@ struct DecodeParams {
     const uint32_t *ready;      // streaming host pipeline: per-chunk "LLRs landed" flags (null: all resident)
     uint32_t *err;              // streaming: set when a flag wait timed out
     int chunk_shift;            // streaming: log2 frames per chunk
+    uint32_t *counts;           // polar_scs_decode_counts: [n_frames] x 4 executed-work counters
+    int chan_in_smem, snap_in_smem;   // placement (read by the counting instance only)
 };
 
 // Kernel parameter block of the FSSCL list decoder (list.cu).  One CTA of
