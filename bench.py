@@ -45,7 +45,9 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--frames", type=int, default=0, help="override frames per Eb/N0 point")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the oracle leg (parity, cpu_baseline, census)")
+    ap.add_argument("--parity-frames", type=int, default=0,
+                    help="frames per Eb/N0 point the oracle checks (0: all that fit ~6e8 LLRs)")
     ap.add_argument("--cpu-seconds", type=float, default=15.0,
                     help="oracle sample length (s) of the cpu_baseline; with --impl reference, per timed step")
     ap.add_argument("--snap-global", action="store_true")
@@ -216,9 +218,11 @@ def oracle_sample(cfg, c, seconds, rank=0):
             break
         per_point = min(c["frames"], int(per_point * min(8.0, max(2.0, 0.5 * seconds / max(dt, 1e-3)))))
     fps = total_frames / total_t
+    cc = O.crc_degree(c["crc_poly"]) if c["crc_poly"] else 0
     return {
         "value": fps * c["K"] / 1e6, "unit": "Mbps", "cores": threads, "kind": "oracle",
-        "frames_per_s": fps, "seconds": total_t,
+        "frames_per_s": fps, "seconds": total_t, "cpu_model": cpu_model(),
+        "per_thread_Mbps": fps * c["K"] / 1e6 / threads, "payload_Mbps": fps * (c["K"] - cc) / 1e6,
         "sample": f"{total_frames // len(c['ebno'])} frames (ids 0..) at each of {len(c['ebno'])} Eb/N0 points "
                   f"of {cfg}, same draws as the GPU workload recipe, {threads} threads, decode only",
     }
@@ -334,16 +338,44 @@ def run_ours(args, cfg, c):
     # quality (outside the timed region): FER per Eb/N0 point and search stats
     stats = dec.decode_list(llr) if is_list else dec.decode_stats(llr)
     torch.cuda.synchronize()
+    assert torch.equal(stats["bits"], out), "decode and decode_stats disagree"
     fer = []
     for p in range(npts):
         errs = int((stats["bits"][p * nf:(p + 1) * nf] != blocks).any(1).sum().item())
         tot = shard.reduce_counters({"frames": nf, "frame_errors": errs}, device="cuda")
         fer.append(tot["frame_errors"] / tot["frames"])
-    pops_mean = sw_mean = None
+    search = None
     if not is_list:
-        pops_mean = [float(stats["pops"][p * nf:(p + 1) * nf].float().mean().item()) for p in range(npts)]
-        sw_mean = [float(stats["switches"][p * nf:(p + 1) * nf].float().mean().item()) for p in range(npts)]
-    assert torch.equal(stats["bits"], out), "decode and decode_stats disagree"
+        search = {}
+        for p, eb in enumerate(c["ebno"]):
+            pp = stats["pops"][p * nf:(p + 1) * nf].to(torch.int64).cpu().numpy()
+            ss = stats["switches"][p * nf:(p + 1) * nf].to(torch.int64).cpu().numpy()
+            search[str(eb)] = {"pops": distribution(pp), "switches": distribution(ss)}
+
+    # per-Eb/N0 device rate: each point's frames in a launch of their own
+    per_point = {}
+    for p, eb in enumerate(c["ebno"]):
+        sl = llr[p * nf:(p + 1) * nf]
+        o2 = out[p * nf:(p + 1) * nf]
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        (dec.decode_list(sl, out=o2, stats=False, stream=stream) if is_list else dec.decode(sl, out=o2, stream=stream))
+        b.record(stream)
+        torch.cuda.synchronize()
+        ms = a.elapsed_time(b)
+        per_point[str(eb)] = {"Mbps": nf * K / (ms / 1e3) / 1e6, "ms": ms, "fer": fer[p]}
+
+    # executed work of the decode kernel (instrumented instance, same frames)
+    executed = None
+    if not is_list:
+        rc = dec.decode_counts(llr)
+        torch.cuda.synchronize()
+        assert torch.equal(rc["bits"], out), "instrumented decode differs"
+        tot = rc["counts"].to(torch.int64).sum(0).tolist()
+        executed = {"fg": tot[0] / frames, "beta_bits": tot[1] / frames, "node_elems": tot[2] / frames,
+                    "snapshot_words": tot[3] / frames, "source": "polar_scs_decode_counts over the whole workload"}
+        del rc
 
     # e2e through the public host-buffer API (H2D + decode + D2H in the timed region)
     e2e = None
@@ -375,8 +407,6 @@ def run_ours(args, cfg, c):
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
     sm_max = float(peaks.get("sm_max_mhz", 1965.0))
     kern_s = statistics.median(launch_ms) / 1e3
-    alg_bytes = frames * (4 * N + K)
-    achieved_gbs = alg_bytes / kern_s / 1e9
     # ncu evidence of the dominant kernel for this workload (committed capture):
     # DRAM bytes per frame (scaled to this launch) and the issue-slot utilisation
     traffic, ncu_ev = None, None
@@ -387,40 +417,56 @@ def run_ours(args, cfg, c):
             ncu_ev = json.load(fh).get(ekey)
         if ncu_ev:
             traffic = ncu_ev["dram_bytes_per_frame"] * frames
-    roofline_hbm = {"bound": "hbm", "achieved": achieved_gbs, "peak": hbm_peak, "unit": "GB/s",
-                    "frac": achieved_gbs / hbm_peak, "traffic": traffic, "algorithmic_bytes": alg_bytes,
-                    "peak_source": "MEASURED_PEAKS.json hbm_gbs" if "hbm_gbs" in peaks else "fallback 6.65 TB/s"}
-    # ALU roofline: algorithmic lane-ops per frame (profiles/op_census.json,
-    # counted by the oracle's O10 counters on a sample of the same workload),
-    # scaled to the batch; peak = 148 SMs x 128 FP32/INT lanes x max SM clock
-    roofline = roofline_hbm
-    roofline_smem = None
-    cpu = None
-    if rank == 0:
+
+    # the CPU oracle on this run's own LLR buffer: parity of every frame (or a
+    # bounded prefix of every point), the cpu_baseline timing and the O10
+    # census of the workload (rank 0 only)
+    oleg = None
+    if rank == 0 and not args.no_cpu:
+        oleg = oracle_leg(cfg, c, llr, stats, nf, npts, is_list, args)
+    cpu = oleg["cpu_baseline"] if oleg else None
+    parity = oleg["parity"] if oleg else None
+    census = oleg["census"] if oleg else None
+    if census is None:
         try:
-            ops_per_frame, smem_bytes_per_frame = census_per_frame(cfg, c)
-            alu_peak = 148 * 128 * sm_max * 1e6 / 1e12       # Tops/s
-            achieved_alu = ops_per_frame * frames / kern_s / 1e12
-            roofline_alu = {"bound": "alu", "achieved": achieved_alu, "peak": alu_peak, "unit": "Tops/s",
-                            "frac": achieved_alu / alu_peak, "traffic": traffic,
-                            "ops_per_frame": ops_per_frame,
-                            "ncu_issue_active_pct": ncu_ev and ncu_ev["issue_active_pct"],
-                            "peak_source": "148 SM x 128 lanes x sm_max_mhz (MEASURED_PEAKS.json)"}
-            roofline = roofline_alu if roofline_alu["frac"] > roofline_hbm["frac"] else roofline_hbm
-            roofline_other = roofline_hbm if roofline is roofline_alu else roofline_alu
-            # shared-memory roofline: 12 B per f/g (two loads, one
-            # store) + 4 B per node element, against 148 SM x 128 B/clk
-            smem_alg = smem_bytes_per_frame * frames
-            smem_peak = 148 * 128 * sm_max * 1e6 / 1e9                  # GB/s
-            roofline_smem = {"bound": "smem", "achieved": smem_alg / kern_s / 1e9, "peak": smem_peak,
-                             "unit": "GB/s", "frac": smem_alg / kern_s / 1e9 / smem_peak,
-                             "bytes_per_frame": smem_bytes_per_frame}
-        except Exception as e:  # noqa: BLE001
-            roofline_other = {"error": str(e)}
-        if not args.no_cpu:
-            cpu = oracle_sample(cfg, c, args.cpu_seconds)
+            cen = census_file(cfg, c)
+            census = {"ops_per_frame": cen["ops_per_frame"], "smem_bytes_per_frame": cen["smem_bytes_per_frame"],
+                      "source": "profiles/op_census.json (oracle O10 on a sample; the oracle leg did not run)"}
+        except (OSError, KeyError):
+            census = None
+
+    # rooflines of the decode kernel (all from this launch's median duration)
+    alu_peak = 148 * 128 * sm_max * 1e6 / 1e12                    # lane-ops: Tops/s
+    smem_peak = 148 * 128 * sm_max * 1e6 / 1e9                    # shared memory: GB/s (128 B/clk/SM)
+    alg_bytes = frames * (4 * N + K)
+    fr = {"hbm": alg_bytes / kern_s / 1e9 / hbm_peak}
+    roofline = {"bound": "hbm", "achieved": alg_bytes / kern_s / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                "frac": fr["hbm"], "traffic": traffic}
+    if census:
+        a_alu = census["ops_per_frame"] * frames / kern_s / 1e12
+        fr["alu_algorithmic"] = a_alu / alu_peak
+        fr["smem_algorithmic"] = census["smem_bytes_per_frame"] * frames / kern_s / 1e9 / smem_peak
+        roofline = {"bound": "alu", "achieved": a_alu, "peak": alu_peak, "unit": "Tops/s",
+                    "frac": fr["alu_algorithmic"], "traffic": traffic}
+    if executed:
+        ex_ops = executed["fg"] + executed["beta_bits"] + executed["node_elems"]
+        fr["alu_executed"] = ex_ops * frames / kern_s / 1e12 / alu_peak
+        fr["smem_executed"] = (12 * executed["fg"] + 4 * executed["node_elems"]) * frames / kern_s / 1e9 / smem_peak
+    roofline["fractions"] = fr
+    roofline["peaks"] = {"hbm_GBps": hbm_peak, "alu_Tops": alu_peak, "smem_GBps": smem_peak,
+                         "source": "hbm: MEASURED_PEAKS.json hbm_gbs" + ("" if "hbm_gbs" in peaks else " (fallback)") +
+                                   "; alu/smem: 148 SM x 128 lanes (x 4 B) x sm_max_mhz"}
+    roofline["kernel_ms"] = kern_s * 1e3
+    if census:
+        roofline["census"] = census
+    if executed:
+        roofline["executed"] = executed
+    if ncu_ev:
+        roofline["ncu"] = ncu_ev
+
     clocks = clk.summary()
     info = dec.info
+    payload_bits = K - (dec.c or 0)
     res = {
         "metric": metric_name(c), "value": value, "unit": "Mbps", "n_gpus": world, "steps": args.steps,
         "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
@@ -437,38 +483,145 @@ def run_ours(args, cfg, c):
                                "chan_in_smem": info["chan_in_smem"]})},
         "frames_per_s": world * frames / (ms_per_step / 1e3),
         "frames_per_s_per_gpu": fps_rank,
+        "payload_Mbps": world * frames * payload_bits / (ms_per_step / 1e3) / 1e6,
         "roofline": roofline,
         "e2e": e2e, "gpu_launches": args.steps, "clocks": clocks,
         "kernel_ms_median": statistics.median(launch_ms),
-        "fer": dict(zip([str(e) for e in c["ebno"]], fer)),
-        "pops_mean": dict(zip([str(e) for e in c["ebno"]], pops_mean)) if pops_mean else None,
-        "switches_mean": dict(zip([str(e) for e in c["ebno"]], sw_mean)) if sw_mean else None,
+        "per_ebno": per_point,
+        "search": search,
         "gen_s": gen_s,
     }
     if rank == 0:
-        res["roofline_other"] = roofline_other
-        res["roofline_smem"] = roofline_smem
-        res["ncu_evidence"] = ncu_ev
+        res["parity"] = parity
         res["cpu_baseline"] = cpu
+        res["paper_context"] = PAPER_CONTEXT
         print(json.dumps(res), flush=True)
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()
 
 
-def census_per_frame(cfg, c):
-    """Algorithmic lane-ops and shared-memory bytes per frame of this workload,
-    from profiles/op_census.json (written by tools/op_census.py from the
-    oracle's O10 counters on a sample of the same workload; the bench itself
-    never runs the oracle outside its cpu_baseline / reference legs):
-    f/g evaluations (clean pass + spines) + node elements + BETA XOR bits +
-    the live entries examined by the stack's linear searches (PAPER.md:L793,
-    L599), or the list prune's T log2 T; smem = 12 B per f/g + 4 B per node
-    element."""
+PAPER_CONTEXT = {
+    "FSSCS-RM_Mbps_per_thread_3dB": 0.925, "FSSCS-RM_Mbps_per_thread_0dB": 0.169,
+    "FSSCL_Mbps_per_thread_3dB": 1.22,
+    "conditions": "the paper's own CPU software: AMD Ryzen 5 1600 @ 3.2 GHz, 6 threads, T/P averaged per thread, "
+                  "information bits only; PC(1024,512), 3GPP sequence, CRC-24C, L=8, D=8192 (a different "
+                  "workload: context, not the target)",
+    "source": "PAPER.md:L966-968, L1100-1106, L1116",
+}
+
+
+def distribution(x):
+    """summary of a per-frame count: quantiles and a log2 histogram"""
+    import numpy as np
+    x = np.asarray(x)
+    if x.size == 0:
+        return None
+    h = np.bincount(np.floor(np.log2(np.maximum(x, 1))).astype(np.int64))
+    return {"mean": float(x.mean()), "p50": float(np.percentile(x, 50)), "p90": float(np.percentile(x, 90)),
+            "p99": float(np.percentile(x, 99)), "max": int(x.max()),
+            "log2_hist": {f"[{1 << k},{1 << (k + 1)})": int(v) for k, v in enumerate(h) if v}}
+
+
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+def oracle_leg(cfg, c, llr, stats, nf, npts, is_list, args):
+    """The oracle (as it stands) decodes the frames this run decoded, from the
+    GPU-generated LLR buffer copied to the host: every frame when the workload
+    fits the time budget (C2: 500,000 frames, ~13 s on 16 threads), else the
+    same-length prefix of every Eb/N0 point.  Returns parity (bits, status,
+    pops, switches exact; PM rel 1e-6, the north star's contract), the
+    cpu_baseline (aggregate, per-thread average as the paper reports it
+    (PAPER.md:L968), a 1-thread figure on a ~10^4-frame prefix) and the O10
+    census of those frames (the roofline's algorithmic numerator)."""
+    import numpy as np
+    threads = os.cpu_count() or 1
+    N, K = c["N"], c["K"]
+    cap = args.parity_frames if args.parity_frames > 0 else max(1, int(6e8 // (N * max(1, npts))))
+    per = min(nf, cap)
+    dec = oracle_decoder(c)
+    rows = np.concatenate([np.arange(p * nf, p * nf + per) for p in range(npts)])
+    llr_h = llr.cpu().numpy() if per == nf else llr[torch_index(rows, llr.device)].cpu().numpy()
+    t0 = time.perf_counter()
+    ref = dec.decode(llr_h, threads=threads)          # timed: the oracle as it stands
+    dt = time.perf_counter() - t0
+    g = {k: v[torch_index(rows, v.device)].cpu().numpy() if per < nf else v.cpu().numpy()
+         for k, v in stats.items() if v is not None}
+    n = rows.size
+    bad_bits = int((g["bits"] != ref["bits"]).any(1).sum())
+    bad_status = int((g["status"] != ref["status"]).sum())
+    pm_rel = np.abs(g["pm"].astype(np.float64) - ref["pm"]) / np.maximum(np.abs(ref["pm"].astype(np.float64)), 1e-30)
+    pm_rel[(g["pm"] == ref["pm"])] = 0.0
+    parity = {"frames": n, "of": nf * npts, "mismatched_bits": bad_bits, "mismatched_status": bad_status,
+              "pm_max_rel": float(pm_rel.max()) if n else 0.0, "pm_over_1e-6": int((pm_rel > 1e-6).sum()),
+              "contract": "bits, status" + ("" if is_list else ", pops, switches") + " exact; PM rel 1e-6 "
+                          "(BASELINE.json north_star)",
+              "frames_checked": "all" if per == nf else f"first {per} of each Eb/N0 point"}
+    if not is_list:
+        parity["mismatched_pops"] = int((g["pops"].astype(np.uint32) != ref["pops"]).sum())
+        parity["mismatched_switches"] = int((g["switches"].astype(np.uint32) != ref["switches"]).sum())
+    parity["mismatched"] = (bad_bits + bad_status + parity["pm_over_1e-6"] + parity.get("mismatched_pops", 0)
+                            + parity.get("mismatched_switches", 0))
+    fps = n / dt
+    payload = K - (O_crc_degree(c["crc_poly"]))
+    # 1 thread on a ~10^4-frame prefix (the same share of every point), cut to
+    # ~8 s of work by the measured multi-thread rate
+    k1 = max(1, min(per, int(min(10_000, 8.0 * fps / threads)) // npts))
+    sel1 = np.concatenate([np.arange(p * per, p * per + k1) for p in range(npts)])
+    t0 = time.perf_counter()
+    dec.decode(llr_h[sel1], threads=1)
+    dt1 = time.perf_counter() - t0
+    cpu = {"value": fps * K / 1e6, "unit": "Mbps", "cores": threads, "kind": "oracle",
+           "frames_per_s": fps, "seconds": dt, "cpu_model": cpu_model(),
+           "per_thread_Mbps": fps * K / 1e6 / threads, "payload_Mbps": fps * payload / 1e6,
+           "one_thread": {"Mbps": sel1.size / dt1 * K / 1e6, "frames": int(sel1.size), "seconds": dt1,
+                          "sample": f"first {sel1.size // npts} frames of each Eb/N0 point"},
+           "sample": (f"all {n} frames of this run's workload" if per == nf else
+                      f"first {per} frames of each of the {npts} Eb/N0 points ({n} of {nf * npts})") +
+                     f", this run's GPU-generated LLRs copied to the host, {threads} threads, decode only"}
+    census = None
+    if not is_list:
+        # O10 counters over the same frames (a second, untimed pass: counting
+        # slows the oracle down)
+        ct = dec.decode(llr_h, threads=threads, counters=True)["counters"]
+        fg_alg = ct["f_ops"] + ct["g_ops"]
+        census = {"ops_per_frame": (fg_alg + ct["node_elems"] + ct["beta_xor_bits"] + ct["key_compares"]) / n,
+                  "smem_bytes_per_frame": (12 * fg_alg + 4 * ct["node_elems"]) / n,
+                  "fg_per_frame": {"alg4_total": fg_alg / n, "alg4_spines": ct["spine_elems"] / n,
+                                   "clean_pass_part": (fg_alg - ct["spine_elems"]) / n,
+                                   "stage_reuse_model": ct["fg_reuse"] / n},
+                  "node_elems_per_frame": ct["node_elems"] / n, "beta_bits_per_frame": ct["beta_xor_bits"] / n,
+                  "key_compares_per_frame": ct["key_compares"] / n,
+                  "source": f"oracle O10 counters over the {n} parity frames"}
+    return {"parity": parity, "cpu_baseline": cpu, "census": census}
+
+
+def torch_index(rows, device):
+    import torch
+    return torch.from_numpy(rows).to(device)
+
+
+def O_crc_degree(poly):
+    import oracle as O
+    return O.crc_degree(poly) if poly else 0
+
+
+def census_file(cfg, c):
+    """fallback census (profiles/op_census.json, tools/op_census.py: oracle O10
+    counters on a sample of the workload) when the oracle leg is skipped"""
     key = cfg + ("_list" if c.get("list") else ("_bitlevel" if c.get("bit_level") else ""))
     with open(os.path.join(ROOT, "profiles", "op_census.json")) as fh:
-        e = json.load(fh)["census"][key]
-    return e["ops_per_frame"], e["smem_bytes_per_frame"]
+        return json.load(fh)["census"][key]
 
 
 def main():
