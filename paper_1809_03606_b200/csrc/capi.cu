@@ -46,7 +46,7 @@ int round4(int w) { return (w + 3) & ~3; }
 
 void free_handle(polar_scs_t h) {
     if (!h) return;
-    cudaFree(h->t.nodes); cudaFree(h->t.info); cudaFree(h->t.crc_tab); cudaFree(h->t.crc_bytes); cudaFree(h->t.info_words);
+    cudaFree(h->t.nodes); cudaFree(h->t.recs); cudaFree(h->t.info); cudaFree(h->t.crc_tab); cudaFree(h->t.crc_bytes); cudaFree(h->t.info_words);
     cudaFree(h->d_queue); cudaFree(h->d_snap); cudaFree(h->d_keys); cudaFree(h->d_jsm); cudaFree(h->d_hdr); cudaFree(h->d_galpha); cudaFree(h->d_salpha);
     for (int b = 0; b < polar_scs_s::kStageBufs; b++) {
         cudaFree(h->d_stage_llr[b]); cudaFree(h->d_stage_bits[b]);
@@ -233,6 +233,7 @@ int polar_scs_create_ex(polar_scs_t *out, int32_t N, int32_t K, const uint8_t *f
     t.systematic_ok = hc.systematic_ok;
     t.nops = (int)hc.ops.size();
     if (e == cudaSuccess) e = upload(&t.nodes, hc.nodes);
+    if (e == cudaSuccess) e = upload(&t.recs, hc.recs);
     if (e == cudaSuccess) e = upload(&t.info, hc.info);
     if (e == cudaSuccess) e = upload(&t.crc_tab, hc.crc_tab);
     if (e == cudaSuccess) e = upload(&t.crc_bytes, hc.crc_bytes);
@@ -247,11 +248,11 @@ int polar_scs_create_ex(polar_scs_t *out, int32_t N, int32_t K, const uint8_t *f
     const int nw = std::max(1, N / 32);
     const int cnt_words = (((t.M + 1) * 2 + 3) / 4 + 1) & ~1;   // even: the fork headers that follow are uint2
     const int sstride = nw;                       // snapshot slot: beta words (headers live in smem)
-    const int sched_words = (t.M * 4 <= 16384) ? round4(t.M) : 0;
+    const int sched_words = ((t.M + 1) * 32 <= 16384) ? 8 * (t.M + 1) : 0;   // per-depth records in smem
     const int slots = slots_for(D);
 
     DecodeParams &p = h->base;
-    p.nodes = t.nodes; p.info = t.info; p.crc_tab = t.crc_tab; p.crc_bytes = t.crc_bytes; p.queue = h->d_queue;
+    p.nodes = t.nodes; p.recs = reinterpret_cast<const uint4 *>(t.recs); p.info = t.info; p.crc_tab = t.crc_tab; p.crc_bytes = t.crc_bytes; p.queue = h->d_queue;
     p.N = N; p.n = t.n; p.K = K; p.c = t.c; p.D = D; p.L = h->L; p.M = t.M;
     p.nw = nw; p.snap_stride = sstride; p.sched_words = sched_words; p.cnt_words = cnt_words;
     p.nonsys = (flags & POLAR_FLAG_NONSYSTEMATIC) ? 1 : 0;

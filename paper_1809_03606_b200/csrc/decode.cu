@@ -273,15 +273,19 @@ fsscs_decode_kernel(const DecodeParams P) {
     const int nw = (NL > 0) ? (NL >= 5 ? (1 << NL) / 32 : 1) : P.nw;
     const int K = P.K, D = P.D, M = P.M;
 
-    // node table (kind, lambda, phi of every decision node, schedule order) in
-    // shared memory when it fits: the schedule walk is derived from it
-    const bool nodes_smem = (NL > 0) || P.sched_words > 0;   // NL kernels: always staged (M*4 <= 16 KiB)
-    if (nodes_smem) {
+    // per-depth records (host.cpp: node j and the node j-1 that ends a path of
+    // depth j, unpacked), staged in shared memory when they fit; the schedule
+    // walk between nodes is derived from them
+    const bool recs_smem = P.sched_words > 0;
+    if (recs_smem) {
         #pragma unroll 1
-        for (int i = threadIdx.x; i < M; i += blockDim.x) smem[i] = P.nodes[i];
+        for (int i = threadIdx.x; i < P.sched_words / 4; i += blockDim.x)
+            reinterpret_cast<uint4 *>(smem)[i] = P.recs[i];
         __syncthreads();
     }
-    auto node_rec = [&](int jj) -> uint32_t { return nodes_smem ? smem[jj] : __ldg(P.nodes + jj); };
+    auto rec_at = [&](int jj, int half) -> uint4 {
+        return recs_smem ? reinterpret_cast<const uint4 *>(smem)[2 * jj + half] : __ldg(P.recs + 2 * jj + half);
+    };
     uint32_t *wb = smem + P.sched_words + warp * P.warp_words;
     // BIG: the first KW stack keys live in shared memory (the rest in global)
     constexpr int KW = 128;
@@ -505,13 +509,11 @@ fsscs_decode_kernel(const DecodeParams P) {
                 nS = cntv;
             }
 
-            // position after the node that created p (its path length)
-            int pl = 0, plam = 0, pphi = 0, pkind = 0;
-            if (j > 0) {
-                const uint32_t pn = node_rec(j - 1);
-                pkind = (int)op_kind(pn); plam = (int)op_lam(pn); pphi = (int)op_phi(pn);
-                pl = (pphi + 1) << plam;
-            }
+            // the record of depth j: p's path length (= the start of node j,
+            // PAPER.md:L784-791), node j, and the node j-1 that created p
+            const uint4 ra = rec_at(j, 0), rb = rec_at(j, 1);
+            const int pl = (int)ra.x;
+            const int plam = (int)rb.x, pphi = (int)rb.y, pkind = (int)rb.z;   // j = 0: (n, 0, 0)
 
             // ---- path switch ---------------------
             int s_d = 0;
@@ -614,10 +616,9 @@ fsscs_decode_kernel(const DecodeParams P) {
 
             // ---- pending BETA ops of p: climb from its
             // last node while it is a right child
-            int l = n;
-            if (j > 0) {
+            int l = plam;
+            {
                 int ph = pphi;
-                l = plam;
                 if ((ph & 1) && l < 5) {
                     // every BETA with 2*Lambda <= 32 acts inside one word: one RMW
                     const int w = ((ph - 1) << l) >> 5;
@@ -702,8 +703,7 @@ fsscs_decode_kernel(const DecodeParams P) {
 
             // ---- ALPHA ops down to node j (Eq. 4, Alg. 1 / Alg. 4): stage s
             // holds node (s, pl >> s); stages >= s_min are still valid
-            const uint32_t nd = node_rec(j);
-            const int kind = (int)op_kind(nd), lam = (int)op_lam(nd), phi = (int)op_phi(nd);
+            const int kind = (int)ra.w, lam = (int)ra.z;
             float xr = 0.f;                    // node alpha element of this lane (Lambda <= 32)
             {
                 int s_min = max(max(lev_mem, bitlen((uint32_t)(pos_mem ^ pl))), max(s_d, l + 1));
@@ -784,7 +784,7 @@ fsscs_decode_kernel(const DecodeParams P) {
                     for (int q = 0; q < 8; q++) v[q] = __shfl_sync(FULL, xr, q);
                     if (lane == 0)
                         printf("TRACE   node kind %d lam %d phi %d pl %d s_min %d (lev_mem %d pos_mem %d s_d %d l %d) alpha %.9g %.9g %.9g %.9g %.9g %.9g %.9g %.9g\n",
-                               kind, lam, phi, pl, s_min, lev_mem, pos_mem, s_d, l, v[0], v[1], v[2], v[3], v[4], v[5], v[6], v[7]);
+                               kind, lam, pl >> lam, pl, s_min, lev_mem, pos_mem, s_d, l, v[0], v[1], v[2], v[3], v[4], v[5], v[6], v[7]);
                 }
 #endif
                 pos_mem = pl;
@@ -792,9 +792,9 @@ fsscs_decode_kernel(const DecodeParams P) {
             }
 
             // ---- decision node ----------
-            const int Lam = 1 << lam;
+            const int Lam = (int)rb.w;
             if constexpr (CNT) c_ne += (uint32_t)Lam;
-            const int seg = phi << lam;
+            const int seg = pl;
             float *a = SP(lam);               // node alpha (Lambda > 32)
             if (Lam <= 32) {
                 if (MODE == 0 && lam == n) xr = ld1<CHAN_SMEM>(chan + (lane & (Lam - 1)), true);
@@ -961,7 +961,7 @@ fsscs_decode_kernel(const DecodeParams P) {
                 }
                 __syncwarp();
             }
-            const int jn = j + 1, npl = (phi + 1) << lam;
+            const int jn = j + 1, npl = (int)ra.y;
             const uint32_t ser0 = next_serial;
             next_serial += (uint32_t)nc;
 

@@ -119,6 +119,27 @@ int build_host_code(int N, int K, const uint8_t *frozen, uint32_t crc_poly, bool
     if (hc.ops.size() > 65535 || hc.M > 8191) return POLAR_EINVAL;
     for (uint32_t op : hc.ops)
         if (op_kind(op) >= OP_R0) hc.nodes.push_back(op);
+    // per-depth records of the stack decoder (decode.cu): a path of depth j
+    // (j nodes decided) resumes at node j, after the BETA climb that finishes
+    // node j-1; everything the pop needs about both nodes,
+    // unpacked: {start of node j (= end of node j-1; N at j = M), end of node
+    // j, lambda_j, kind_j, lambda_{j-1}, phi_{j-1}, kind_{j-1}, Lambda_j}
+    hc.recs.assign(8 * (size_t)(hc.M + 1), 0u);
+    for (int j = 0; j <= hc.M; j++) {
+        uint32_t *r = &hc.recs[8 * (size_t)j];
+        if (j < hc.M) {
+            const uint32_t nd = hc.nodes[j], lam = op_lam(nd), phi = op_phi(nd);
+            r[0] = phi << lam; r[1] = (phi + 1) << lam; r[2] = lam; r[3] = op_kind(nd); r[7] = 1u << lam;
+        } else {
+            r[0] = r[1] = (uint32_t)N;
+        }
+        if (j > 0) {
+            const uint32_t pn = hc.nodes[j - 1];
+            r[4] = op_lam(pn); r[5] = op_phi(pn); r[6] = op_kind(pn);
+        } else {
+            r[4] = (uint32_t)n;
+        }
+    }
 
     // CRC syndrome table: block bit k < P = K-c is the
     // payload coefficient of x^(P-1-k); its contribution to the remainder of

@@ -31,6 +31,7 @@ struct CodeTables {
     uint32_t crc_poly = 0;
     bool systematic_ok = false;
     uint32_t *nodes = nullptr;  int nops = 0;   // decision nodes (kind, lambda, phi) in schedule order
+    uint32_t *recs = nullptr;                   // [M+1][8] per-depth records (host.cpp)
     uint16_t *info = nullptr;                   // A ascending, [K]
     uint32_t *crc_tab = nullptr;                // [K] syndrome contribution of block bit k
     uint32_t *crc_bytes = nullptr;              // [nw][4][256] per beta byte (CRC codes)
@@ -46,6 +47,7 @@ struct DecodeParams {
     uint32_t *pops, *switches;
     uint8_t *status;
     const uint32_t *nodes;      // [M] node records; the BETA/ALPHA walk between them is implied
+    const uint4 *recs;          // [M+1][2] per-depth records (host.cpp build_host_code)
     const uint16_t *info;
     const uint32_t *crc_tab;
     const uint32_t *crc_bytes;  // [nw][4][256] syndrome contribution of each beta byte (CRC codes)
@@ -57,7 +59,7 @@ struct DecodeParams {
     int N, n, K, c, D, L, M;
     int nw;                     // beta words = max(1, N/32)
     int snap_stride;            // words per snapshot slot = nw (headers m1..m4 in shared memory)
-    int sched_words;            // node-table words staged in shared memory (0 = read global)
+    int sched_words;            // per-depth record words staged in shared memory (0 = read global)
     int warp_words;             // shared-memory words per warp
     int cnt_words;              // words of the per-length counters (u16 each)
     int hdr_words;              // shared-memory fork headers: 2 D (register stacks) or 0
@@ -163,6 +165,7 @@ struct HostCode {
     bool systematic_ok = false;
     std::vector<uint32_t> ops;      // full FSSC schedule (ALPHA/BETA/nodes), Fig. 5
     std::vector<uint32_t> nodes;    // its decision nodes only
+    std::vector<uint32_t> recs;     // [M+1][8] per-depth records of the stack decoder
     std::vector<uint16_t> info;
     std::vector<uint32_t> crc_tab;
     std::vector<uint32_t> crc_bytes;
