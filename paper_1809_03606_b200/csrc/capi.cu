@@ -16,7 +16,8 @@
 namespace polar {
 cudaError_t launch_decode(const DecodeParams &p, int slots, bool snap_smem, bool chan_smem, int ctas, int smem,
                           cudaStream_t st);
-cudaError_t decode_occupancy(int n, int slots, bool snap_smem, bool chan_smem, int mode, int smem, int *blocks_per_sm);
+cudaError_t decode_occupancy(int n, int slots, bool snap_smem, bool chan_smem, int mode, bool recs_smem, int smem,
+                             int *blocks_per_sm);
 cudaError_t launch_decode_counts(const DecodeParams &p, int slots, int ctas, int smem, cudaStream_t st);
 cudaError_t launch_list(const ListParams &p, int lcap, int ctas, int smem, cudaStream_t st);
 cudaError_t list_occupancy(int lcap, int n, int L, int smem, int *blocks_per_sm);
@@ -248,8 +249,10 @@ int polar_scs_create_ex(polar_scs_t *out, int32_t N, int32_t K, const uint8_t *f
     const int nw = std::max(1, N / 32);
     const int cnt_words = (((t.M + 1) * 2 + 3) / 4 + 1) & ~1;   // even: the fork headers that follow are uint2
     const int sstride = nw;                       // snapshot slot: beta words (headers live in smem)
-    const int sched_words = ((t.M + 1) * 32 <= 16384) ? 8 * (t.M + 1) : 0;   // per-depth records in smem
     const int slots = slots_for(D);
+    // per-depth records in shared memory when they fit (not for the global
+    // stack, whose occupancy is shared-memory bound: it reads them through L1)
+    const int sched_words = (slots != 0 && (t.M + 1) * 64 <= 16384) ? 16 * (t.M + 1) : 0;
 
     DecodeParams &p = h->base;
     p.nodes = t.nodes; p.recs = reinterpret_cast<const uint4 *>(t.recs); p.info = t.info; p.crc_tab = t.crc_tab; p.crc_bytes = t.crc_bytes; p.queue = h->d_queue;
@@ -295,7 +298,9 @@ int polar_scs_create_ex(polar_scs_t *out, int32_t N, int32_t K, const uint8_t *f
             const int smem = 4 * (sched_words + kDecodeWarps * ww);
             if (smem > optin) continue;
             int occ = 0;
-            if (decode_occupancy(t.n, slots, snap_smem, chan_smem, mode, smem, &occ) != cudaSuccess || occ < 1) continue;
+            if (decode_occupancy(t.n, slots, snap_smem, chan_smem, mode, sched_words > 0, smem, &occ) != cudaSuccess ||
+                occ < 1)
+                continue;
             if (occ > best_occ) {
                 best_occ = occ; best_smem = smem; best_ww = ww; best_snap = snap_smem; best_chan = chan_smem;
                 best_gst = gst;

@@ -276,15 +276,17 @@ fsscs_decode_kernel(const DecodeParams P) {
     // per-depth records (host.cpp: node j and the node j-1 that ends a path of
     // depth j, unpacked), staged in shared memory when they fit; the schedule
     // walk between nodes is derived from them
-    const bool recs_smem = P.sched_words > 0;
+    // (register-stack specialised kernels are only launched when they fit; the
+    // global-stack kernel reads them through L1: their shared memory costs it a CTA)
+    const bool recs_smem = (NL > 0 && !BIG) || P.sched_words > 0;
     if (recs_smem) {
         #pragma unroll 1
         for (int i = threadIdx.x; i < P.sched_words / 4; i += blockDim.x)
             reinterpret_cast<uint4 *>(smem)[i] = P.recs[i];
         __syncthreads();
     }
-    auto rec_at = [&](int jj, int half) -> uint4 {
-        return recs_smem ? reinterpret_cast<const uint4 *>(smem)[2 * jj + half] : __ldg(P.recs + 2 * jj + half);
+    auto rec_at = [&](int jj, int q) -> uint4 {
+        return recs_smem ? reinterpret_cast<const uint4 *>(smem)[4 * jj + q] : __ldg(P.recs + 4 * jj + q);
     };
     uint32_t *wb = smem + P.sched_words + warp * P.warp_words;
     // BIG: the first KW stack keys live in shared memory (the rest in global)
@@ -511,9 +513,9 @@ fsscs_decode_kernel(const DecodeParams P) {
 
             // the record of depth j: p's path length (= the start of node j,
             // PAPER.md:L784-791), node j, and the node j-1 that created p
-            const uint4 ra = rec_at(j, 0), rb = rec_at(j, 1);
+            const uint4 ra = rec_at(j, 0), rb = rec_at(j, 1), rc = rec_at(j, 2), rd = rec_at(j, 3);
             const int pl = (int)ra.x;
-            const int plam = (int)rb.x, pphi = (int)rb.y, pkind = (int)rb.z;   // j = 0: (n, 0, 0)
+            const int pkind = (int)rb.z, plam = (int)rd.z;
 
             // ---- path switch ---------------------
             int s_d = 0;
@@ -588,7 +590,7 @@ fsscs_decode_kernel(const DecodeParams P) {
                 if (pl > d) s_d = bitlen((uint32_t)pl ^ (uint32_t)d);
                 __syncwarp();
                 if (rel != 0u) {
-                    const int seg = pphi << plam, Lam = 1 << plam;
+                    const int Lam = 1 << plam, seg = pl - Lam;      // node j-1
                     if (pkind == OP_REP) {
                         if (Lam >= 32) {
                             #pragma unroll 1
@@ -615,31 +617,27 @@ fsscs_decode_kernel(const DecodeParams P) {
             work_pl = pl;
 
             // ---- pending BETA ops of p: climb from its
-            // last node while it is a right child
-            int l = plam;
+            // last node while it is a right child.  The levels with 2 Lambda <= 32
+            // act inside one word: one RMW with the record's masks, each level
+            // x ^= (x >> Lambda) & mask; the rest word by word.
+            const int l = (int)rb.w;                 // level where the climb ends
+            if (rc.x != 0xFFFFFFFFu) {
+                uint32_t x = beta[rc.x];
+                x ^= (x >> 1) & rc.y;
+                x ^= (x >> 2) & rc.z;
+                x ^= (x >> 4) & rc.w;
+                x ^= (x >> 8) & rd.x;
+                x ^= (x >> 16) & rd.y;
+                if (lane == 0) beta[rc.x] = x;
+                __syncwarp();
+                if constexpr (CNT) c_bb += (uint32_t)(__popc(rc.y) + __popc(rc.z) + __popc(rc.w) + __popc(rd.x) + __popc(rd.y));
+            }
             {
-                int ph = pphi;
-                if ((ph & 1) && l < 5) {
-                    // every BETA with 2*Lambda <= 32 acts inside one word: one RMW
-                    const int w = ((ph - 1) << l) >> 5;
-                    uint32_t x = beta[w];
-                    #pragma unroll 1
-                    while ((ph & 1) && l < 5) {
-                        const int o = ((ph - 1) << l) & 31, Lm = 1 << l;
-                        x ^= ((x >> (o + Lm)) & ((1u << Lm) - 1u)) << o;
-                        if constexpr (CNT) c_bb += (uint32_t)Lm;
-                        ph >>= 1;
-                        l++;
-                    }
-                    if (lane == 0) beta[w] = x;
-                    __syncwarp();
-                }
+                int ph = (int)rb.y;
                 #pragma unroll 1
-                while (ph & 1) {
-                    beta_op(beta, l, ph, lane);
-                    if constexpr (CNT) c_bb += 1u << l;
-                    ph >>= 1;
-                    l++;
+                for (int lw = (int)rb.x; ph & 1; ph >>= 1, lw++) {
+                    beta_op(beta, lw, ph, lane);
+                    if constexpr (CNT) c_bb += 1u << lw;
                 }
             }
 
@@ -792,7 +790,7 @@ fsscs_decode_kernel(const DecodeParams P) {
             }
 
             // ---- decision node ----------
-            const int Lam = (int)rb.w;
+            const int Lam = 1 << lam;
             if constexpr (CNT) c_ne += (uint32_t)Lam;
             const int seg = pl;
             float *a = SP(lam);               // node alpha (Lambda > 32)
@@ -1133,7 +1131,8 @@ static cudaError_t launch_s(const DecodeParams &p, int slots, int ctas, int smem
 // code-length-specialised instantiations: the BASELINE configs in the
 // placements create() picks for them (n = 12 with the top alpha stage(s) in a
 // global arena when that raises the occupancy: GA)
-int specialised_nl(int n, int slots, bool snap_smem, bool chan_smem) {
+int specialised_nl(int n, int slots, bool snap_smem, bool chan_smem, bool recs_smem) {
+    if (!recs_smem && slots != 0) return 0;
     if (n == 7 && slots == 1 && snap_smem && chan_smem) return 7;
     if (n == 10 && slots == 1 && !snap_smem && !chan_smem) return 10;
     if (n == 11 && slots == 2 && !snap_smem && !chan_smem) return 11;
@@ -1144,7 +1143,7 @@ int specialised_nl(int n, int slots, bool snap_smem, bool chan_smem) {
 
 cudaError_t launch_decode(const DecodeParams &p, int slots, bool snap_smem, bool chan_smem, int ctas, int smem,
                           cudaStream_t st) {
-    switch (specialised_nl(p.n, slots, snap_smem, chan_smem)) {
+    switch (specialised_nl(p.n, slots, snap_smem, chan_smem, p.sched_words > 0)) {
     case 7:
         if (p.c == 0 && !p.nonsys && p.M > 1) return launch_t<1, true, true, 7, false, 2>(p, ctas, smem, st);
         return launch_t<1, true, true, 7>(p, ctas, smem, st);
@@ -1190,8 +1189,9 @@ static cudaError_t occ_s(int slots, int smem, int *blocks) {
     return occ_t<4, B, C>(smem, blocks);
 }
 
-cudaError_t decode_occupancy(int n, int slots, bool snap_smem, bool chan_smem, int mode, int smem, int *blocks_per_sm) {
-    switch (specialised_nl(n, slots, snap_smem, chan_smem)) {
+cudaError_t decode_occupancy(int n, int slots, bool snap_smem, bool chan_smem, int mode, bool recs_smem, int smem,
+                             int *blocks_per_sm) {
+    switch (specialised_nl(n, slots, snap_smem, chan_smem, recs_smem)) {
     case 7: return mode == 2 ? occ_t<1, true, true, 7, false, 2>(smem, blocks_per_sm) : occ_t<1, true, true, 7>(smem, blocks_per_sm);
     case 10: return mode == 2 ? occ_t<1, false, false, 10, false, 2>(smem, blocks_per_sm)
                   : mode == 1 ? occ_t<1, false, false, 10, false, 1>(smem, blocks_per_sm)

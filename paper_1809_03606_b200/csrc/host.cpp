@@ -119,28 +119,49 @@ int build_host_code(int N, int K, const uint8_t *frozen, uint32_t crc_poly, bool
     if (hc.ops.size() > 65535 || hc.M > 8191) return POLAR_EINVAL;
     for (uint32_t op : hc.ops)
         if (op_kind(op) >= OP_R0) hc.nodes.push_back(op);
-    // per-depth records of the stack decoder (decode.cu): a path of depth j
-    // (j nodes decided) resumes at node j, after the BETA climb that finishes
-    // node j-1; everything the pop needs about both nodes,
-    // unpacked: {start of node j (= end of node j-1; N at j = M), end of node
-    // j, lambda_j, kind_j, lambda_{j-1}, phi_{j-1}, kind_{j-1}, Lambda_j}
-    hc.recs.assign(8 * (size_t)(hc.M + 1), 0u);
+    // per-depth records of the stack decoder (decode.cu), 16 words each: a path
+    // of depth j (j nodes decided) resumes at node j after the BETA climb that
+    // finishes node j-1; everything the pop needs about
+    // both nodes and that climb, unpacked:
+    //   [0] start of node j (= p's path length; N at j = M), [1] end of node j,
+    //   [2] lambda_j, [3] kind_j,
+    //   [4] level lw where the word-level part of the climb starts, [5] its phi,
+    //   [6] kind_{j-1}, [7] level where the climb ends,
+    //   [8] word of the in-word part (levels < 5, 2 Lambda <= 32; ~0u: none),
+    //   [9..13] its masks: level l XORs (x >> 2^l) & mask_l into x (0: level
+    //   not climbed), [14] lambda_{j-1}, [15] 0
+    hc.recs.assign(16 * (size_t)(hc.M + 1), 0u);
     for (int j = 0; j <= hc.M; j++) {
-        uint32_t *r = &hc.recs[8 * (size_t)j];
+        uint32_t *r = &hc.recs[16 * (size_t)j];
         if (j < hc.M) {
             const uint32_t nd = hc.nodes[j], lam = op_lam(nd), phi = op_phi(nd);
-            r[0] = phi << lam; r[1] = (phi + 1) << lam; r[2] = lam; r[3] = op_kind(nd); r[7] = 1u << lam;
+            r[0] = phi << lam; r[1] = (phi + 1) << lam; r[2] = lam; r[3] = op_kind(nd);
         } else {
             r[0] = r[1] = (uint32_t)N;
         }
-        if (j > 0) {
-            const uint32_t pn = hc.nodes[j - 1];
-            r[4] = op_lam(pn); r[5] = op_phi(pn); r[6] = op_kind(pn);
-        } else {
-            r[4] = (uint32_t)n;
+        r[8] = ~0u;
+        if (j == 0) {
+            r[4] = (uint32_t)n; r[5] = 0; r[7] = (uint32_t)n; r[14] = (uint32_t)n;
+            continue;
         }
+        const uint32_t pn = hc.nodes[j - 1];
+        int l = (int)op_lam(pn);
+        uint32_t ph = op_phi(pn);
+        r[6] = op_kind(pn);
+        r[14] = (uint32_t)l;
+        if ((ph & 1) && l < 5) {
+            r[8] = ((ph - 1) << l) >> 5;
+            while ((ph & 1) && l < 5) {
+                const uint32_t o = ((ph - 1) << l) & 31, Lm = 1u << l;
+                r[9 + l] = ((1u << Lm) - 1u) << o;    // left segment [o, o + Lm) ^= right [o + Lm, o + 2 Lm)
+                ph >>= 1;
+                l++;
+            }
+        }
+        r[4] = (uint32_t)l; r[5] = ph;
+        while (ph & 1) { ph >>= 1; l++; }
+        r[7] = (uint32_t)l;
     }
-
     // CRC syndrome table: block bit k < P = K-c is the
     // payload coefficient of x^(P-1-k); its contribution to the remainder of
     // payload * x^c is x^(P-1-k+c) mod g.  A received CRC bit k >= P weighs

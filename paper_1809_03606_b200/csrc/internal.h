@@ -31,7 +31,7 @@ struct CodeTables {
     uint32_t crc_poly = 0;
     bool systematic_ok = false;
     uint32_t *nodes = nullptr;  int nops = 0;   // decision nodes (kind, lambda, phi) in schedule order
-    uint32_t *recs = nullptr;                   // [M+1][8] per-depth records (host.cpp)
+    uint32_t *recs = nullptr;                   // [M+1][16] per-depth records (host.cpp)
     uint16_t *info = nullptr;                   // A ascending, [K]
     uint32_t *crc_tab = nullptr;                // [K] syndrome contribution of block bit k
     uint32_t *crc_bytes = nullptr;              // [nw][4][256] per beta byte (CRC codes)
@@ -47,7 +47,7 @@ struct DecodeParams {
     uint32_t *pops, *switches;
     uint8_t *status;
     const uint32_t *nodes;      // [M] node records; the BETA/ALPHA walk between them is implied
-    const uint4 *recs;          // [M+1][2] per-depth records (host.cpp build_host_code)
+    const uint4 *recs;          // [M+1][4] per-depth records (host.cpp build_host_code)
     const uint16_t *info;
     const uint32_t *crc_tab;
     const uint32_t *crc_bytes;  // [nw][4][256] syndrome contribution of each beta byte (CRC codes)
@@ -165,7 +165,7 @@ struct HostCode {
     bool systematic_ok = false;
     std::vector<uint32_t> ops;      // full FSSC schedule (ALPHA/BETA/nodes), Fig. 5
     std::vector<uint32_t> nodes;    // its decision nodes only
-    std::vector<uint32_t> recs;     // [M+1][8] per-depth records of the stack decoder
+    std::vector<uint32_t> recs;     // [M+1][16] per-depth records of the stack decoder
     std::vector<uint16_t> info;
     std::vector<uint32_t> crc_tab;
     std::vector<uint32_t> crc_bytes;
