@@ -59,8 +59,8 @@ def parse():
     ap.add_argument("--sequence", default="",
                     help="information set from a reliability-sequence file (one index per line, least reliable "
                          "first; e.g. the 3GPP sequence of PAPER.md:L966) instead of Bhattacharyya construction")
-    ap.add_argument("--list-kernel", default="auto", choices=["auto", "cta", "packed"],
-                    help="FSSCL kernel: CTA of L warps per frame, or one warp per frame with packed paths")
+    ap.add_argument("--list-kernel", default="auto", choices=["auto", "packed"],
+                    help="FSSCL kernel (one warp per frame with the L paths packed across its lanes)")
     ap.add_argument("--list", action="store_true",
                     help="FSSCL list decoder with list size = the config's L (the paper's FSSCL comparator, "
                          "PAPER.md:L521-587); with --bit-level: plain SCL")
@@ -475,8 +475,8 @@ def run_ours(args, cfg, c):
         "config": {"workload": workload_name(cfg, c), "frames_per_step_per_gpu": frames,
                    "l2": f"inputs {frames * N * 4 / 1e9:.2f} GB per step > 126 MB L2 (no flush needed)",
                    "launch": ({"ctas": info["list_ctas"],
-                               "kernel": "packed (warp per frame)" if info["list_packed"] else "cta (warp per path)",
-                               "warps_per_cta": info["list_warps_per_cta"] if info["list_packed"] else c["L"],
+                               "kernel": "packed (warp per frame)",
+                               "warps_per_cta": info["list_warps_per_cta"],
                                "smem_per_cta": info["list_smem_per_cta"]} if is_list else
                               {"ctas": info["ctas"], "warps_per_cta": info["warps_per_cta"],
                                "smem_per_cta": info["smem_per_cta"], "snap_in_smem": info["snap_in_smem"],

@@ -53,10 +53,12 @@ extern "C" {
 #define POLAR_FLAG_NONSYSTEMATIC 0x40u /* non-systematic code: encoders emit c = u F,
                                           decoders read u_hat = x_hat F restricted to A
                                           (PAPER.md:L503); any mask is allowed */
-#define POLAR_FLAG_LIST_CTA     0x80u /* polar_scl_decode: one CTA of L warps per frame
-                                         (warp = path) instead of the automatic choice */
+#define POLAR_FLAG_LIST_CTA     0x80u /* reserved: the CTA-per-frame list kernel was removed
+                                         (slower than the packed kernel on every config);
+                                         create returns POLAR_EINVAL */
 #define POLAR_FLAG_LIST_PACKED  0x100u /* polar_scl_decode: one warp per frame with the L
-                                          paths packed across its lanes */
+                                          paths packed across its lanes (the only list
+                                          kernel; accepted for compatibility) */
 
 typedef struct polar_scs_s *polar_scs_t;
 

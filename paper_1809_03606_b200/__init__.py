@@ -139,14 +139,15 @@ class PolarSCS:
 
     def __init__(self, frozen_mask, D: int, L: int, crc_poly: int = 0, bit_level: bool = False,
                  snap_global: bool = False, chan_global: bool = False, snap_smem: bool = False,
-                 chan_smem: bool = False, nonsystematic: bool = False, list_kernel: str = "auto"):
+                 chan_smem: bool = False, nonsystematic: bool = False, list_kernel: str = "auto",
+                 flags_extra: int = 0):
         fm = np.ascontiguousarray(frozen_mask, dtype=np.uint8)
         self.N = int(fm.size)
         self.K = int(self.N - int(fm.sum()))
         flags = ((POLAR_FLAG_BIT_LEVEL if bit_level else 0) | (POLAR_FLAG_SNAP_GLOBAL if snap_global else 0)
                  | (POLAR_FLAG_CHAN_GLOBAL if chan_global else 0) | (POLAR_FLAG_SNAP_SMEM if snap_smem else 0)
                  | (POLAR_FLAG_CHAN_SMEM if chan_smem else 0) | (POLAR_FLAG_NONSYSTEMATIC if nonsystematic else 0)
-                 | {"auto": 0, "cta": POLAR_FLAG_LIST_CTA, "packed": POLAR_FLAG_LIST_PACKED}[list_kernel])
+                 | {"auto": 0, "packed": POLAR_FLAG_LIST_PACKED}[list_kernel] | int(flags_extra))
         h = _vp()
         _check(polar_scs_create_ex(C.byref(h), self.N, self.K, fm.ctypes.data, int(D), int(L),
                                    int(crc_poly), flags), "polar_scs_create")

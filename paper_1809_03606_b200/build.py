@@ -7,7 +7,7 @@ import subprocess
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 SO = os.path.join(HERE, "libpolarscs.so")
-SOURCES = ["host.cpp", "capi.cu", "decode.cu", "list.cu", "list_packed.cu", "codec.cu"]
+SOURCES = ["host.cpp", "capi.cu", "decode.cu", "list_packed.cu", "codec.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -19,8 +19,6 @@ cudaError_t launch_decode(const DecodeParams &p, int slots, bool snap_smem, bool
 cudaError_t decode_occupancy(int n, int slots, bool snap_smem, bool chan_smem, int mode, bool recs_smem, int smem,
                              int *blocks_per_sm);
 cudaError_t launch_decode_counts(const DecodeParams &p, int slots, int ctas, int smem, cudaStream_t st);
-cudaError_t launch_list(const ListParams &p, int lcap, int ctas, int smem, cudaStream_t st);
-cudaError_t list_occupancy(int lcap, int n, int L, int smem, int *blocks_per_sm);
 cudaError_t launch_list_packed(const ListParams &p, int ctas, int smem, cudaStream_t st);
 cudaError_t list_packed_occupancy(int n, int pwarps, int smem, int *blocks_per_sm);
 cudaError_t launch_crc_attach(const CodecParams &p, cudaStream_t st);
@@ -138,12 +136,8 @@ int list_impl(polar_scs_t h, const float *llr, int64_t n, uint8_t *bits, float *
     if (p.galpha) p.galpha += (size_t)h->list_ctas * p.pwarps * p.gstride * (size_t)slot;
     cudaError_t e = cudaMemsetAsync(p.queue, 0, sizeof(unsigned long long), st);
     if (e != cudaSuccess) return cuda_status(e);
-    if (h->list_packed) {
-        const int ctas = (int)std::min<int64_t>(h->list_ctas, (n + p.pwarps - 1) / p.pwarps);
-        return cuda_status(launch_list_packed(p, ctas, h->list_smem, st));
-    }
-    const int ctas = (int)std::min<int64_t>(h->list_ctas, n);
-    return cuda_status(launch_list(p, h->list_lcap, ctas, h->list_smem, st));
+    const int ctas = (int)std::min<int64_t>(h->list_ctas, (n + p.pwarps - 1) / p.pwarps);
+    return cuda_status(launch_list_packed(p, ctas, h->list_smem, st));
 }
 
 // packed FSSCL layout (list_packed.cu): node table, then one block per warp
@@ -169,28 +163,6 @@ int list_packed_layout(ListParams &p) {
     return p.o_warp0 + p.pwarps * o;
 }
 
-// FSSCL shared-memory layout (list.cu): offsets in 32-bit words, each area
-// 16-byte aligned.  Returns the total words.
-int list_layout(ListParams &p) {
-    const int L = p.L, N = p.N, n = p.n;
-    int o = round4(p.M);                                      // node table
-    p.o_alpha = o;
-    const int alpha_words = (p.M == 1 && n > 5) ? L * N : (n > 6 ? L * (N - 64) : 0);
-    o += round4(alpha_words);
-    p.o_beta = o;  o += round4(2 * L * p.nw);
-    p.o_reg = o;   o += 2 * L * 64;
-    p.o_clist = o; o += round4(2 * L);
-    p.o_mi = o;    o += round4(4 * L);
-    p.o_prow = o;  o += round4(4 * L);
-    p.o_cand = o;  o += round4(16 * L);
-    p.o_sel = o;   o += round4(L);
-    p.o_selpm = o; o += round4(L);
-    p.o_ok = o;    o += round4(L);
-    p.o_misc = o;  o += 4;
-    p.words = o;
-    return o;
-}
-
 }  // namespace
 
 extern "C" {
@@ -213,7 +185,7 @@ int polar_scs_create_ex(polar_scs_t *out, int32_t N, int32_t K, const uint8_t *f
     const uint32_t known = POLAR_FLAG_BIT_LEVEL | POLAR_FLAG_SNAP_GLOBAL | POLAR_FLAG_CHAN_GLOBAL |
                            POLAR_FLAG_SNAP_SMEM | POLAR_FLAG_CHAN_SMEM | POLAR_FLAG_NONSYSTEMATIC |
                            POLAR_FLAG_LIST_CTA | POLAR_FLAG_LIST_PACKED;
-    if ((flags & POLAR_FLAG_LIST_CTA) && (flags & POLAR_FLAG_LIST_PACKED)) return POLAR_EINVAL;
+    if (flags & POLAR_FLAG_LIST_CTA) return POLAR_EINVAL;     // the CTA list kernel was removed (slower everywhere)
     if (D < 1 || D > kMaxD || L < 1 || L > 65536 || (flags & ~known)) return POLAR_EINVAL;
     if ((flags & POLAR_FLAG_SNAP_GLOBAL) && (flags & POLAR_FLAG_SNAP_SMEM)) return POLAR_EINVAL;
     if ((flags & POLAR_FLAG_CHAN_GLOBAL) && (flags & POLAR_FLAG_CHAN_SMEM)) return POLAR_EINVAL;
@@ -344,21 +316,15 @@ int polar_scs_create_ex(polar_scs_t *out, int32_t N, int32_t K, const uint8_t *f
         p.stack_jsm = h->d_jsm;
         p.hdr_global = h->d_hdr;
     }
-    // ---- FSSCL launch (polar_scl_decode): a CTA of L warps per frame, or one
-    // warp per frame with the paths packed across its lanes; automatic choice:
-    // the packed kernel when it keeps at least 4 frames per SM in flight
-    // (DESIGN.md §Kernels), else the CTA kernel
+    // ---- FSSCL launch (polar_scl_decode): one warp per frame with the paths
+    // packed across its lanes (list_packed.cu)
     if (h->L <= 32) {
         ListParams base{};
         base.nodes = t.nodes; base.info = t.info; base.crc_bytes = t.crc_bytes; base.queue = h->d_queue;
         base.N = N; base.n = t.n; base.K = K; base.c = t.c; base.L = h->L; base.M = t.M; base.nw = nw;
         base.nonsys = p.nonsys;
-        ListParams lc = base, lpk = base;
-        const int smem_c = 4 * list_layout(lc);
-        const int lcap = h->L <= 8 ? 8 : (h->L <= 16 ? 16 : 32);
-        int occ_c = 0, occ_p = 0;
-        if (smem_c > optin || list_occupancy(lcap, t.n, h->L, smem_c, &occ_c) != cudaSuccess) occ_c = 0;
-        cudaGetLastError();
+        ListParams lpk = base;
+        int occ_p = 0;
         // packed: 4, 2 or 1 warps per CTA, whichever keeps the most warps resident
         int smem_p = 0, pw_best = 0;
         // the top alpha stages move to a global (L2-resident) arena while that
@@ -376,10 +342,7 @@ int polar_scs_create_ex(polar_scs_t *out, int32_t N, int32_t K, const uint8_t *f
                 if (oc * pw > occ_p * pw_best) { occ_p = oc; pw_best = pw; smem_p = sm; lpk = tp; }
             }
         }
-        bool packed = occ_p >= 1;                 // measured faster on C1-C4
-        if (flags & POLAR_FLAG_LIST_CTA) packed = false;
-        if (flags & POLAR_FLAG_LIST_PACKED) packed = true;
-        if (packed && occ_p >= 1) {
+        if (occ_p >= 1) {
             h->list = lpk; h->list_packed = 1; h->list_ctas = occ_p * sms; h->list_smem = smem_p;
             if (lpk.gstride > 0) {
                 const size_t per = (size_t)h->list_ctas * lpk.pwarps * lpk.gstride;
@@ -387,8 +350,6 @@ int polar_scs_create_ex(polar_scs_t *out, int32_t N, int32_t K, const uint8_t *f
                 if (e != cudaSuccess) { free_handle(h); return cuda_status(e); }
                 h->list.galpha = h->d_galpha;
             }
-        } else if (!packed && occ_c >= 1) {
-            h->list = lc; h->list_packed = 0; h->list_ctas = occ_c * sms; h->list_smem = smem_c; h->list_lcap = lcap;
         }
     }
     *out = h;

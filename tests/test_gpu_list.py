@@ -37,8 +37,7 @@ def _run(fr, L, crc, ebnos, n, seed, bit_level=False, nonsys=False, D=8, lk="aut
     dec = P.PolarSCS(fr, D, L, crc, bit_level=bit_level, nonsystematic=nonsys, list_kernel=lk)
     if dec.info["list_ctas"] == 0:
         pytest.skip(f"{lk} list kernel does not fit shared memory")
-    if lk != "auto":
-        assert dec.info["list_packed"] == int(lk == "packed")
+    assert dec.info["list_packed"] == 1
     K = dec.K
     for ebno in ebnos:
         pay = ig.payload_bits(seed, 0, n, K - dec.c)
@@ -64,8 +63,7 @@ def _run(fr, L, crc, ebnos, n, seed, bit_level=False, nonsys=False, D=8, lk="aut
     ("C5", 8, (3.0, 4.0), 40),
     ("C5", 32, (3.0,), 24),          # the config's L = 32: packed kernel only (alpha stages in L2)
 ])
-@pytest.mark.parametrize("lk", ["cta", "packed"])
-def test_list_parity_configs(cfg, L, ebnos, n, lk):
+def test_list_parity_configs(cfg, L, ebnos, n, lk="packed"):
     c = ig.CONFIGS[cfg]
     fr = P.bhattacharyya_mask(c["N"], c["K"], c["design_db"])
     _run(fr, L, c["crc_poly"], ebnos, n, c["seed"], lk=lk)
@@ -84,8 +82,7 @@ def test_list_parity_configs(cfg, L, ebnos, n, lk):
     (2048, 1024, 4, 0, False), (4096, 2048, 2, 0x11021, False),
     (4096, 3072, 16, 0x107, False),  # packed kernel with most alpha stages in L2
 ])
-@pytest.mark.parametrize("lk", ["cta", "packed"])
-def test_list_parity_edge(N, K, L, crc, bit_level, lk):
+def test_list_parity_edge(N, K, L, crc, bit_level, lk="packed"):
     fr = P.bhattacharyya_mask(N, K, 2.0)
     if K == 0 or (crc and O.crc_degree(crc) >= K):
         pytest.skip("no information bits")
@@ -94,8 +91,7 @@ def test_list_parity_edge(N, K, L, crc, bit_level, lk):
 
 
 @pytest.mark.parametrize("cfg,random_mask", [("C1", False), ("C3", False), ("C1", True)])
-@pytest.mark.parametrize("lk", ["cta", "packed"])
-def test_list_nonsystematic_parity(cfg, random_mask, lk):
+def test_list_nonsystematic_parity(cfg, random_mask, lk="packed"):
     c = ig.CONFIGS[cfg]
     fr = _random_mask(c["N"], c["K"], 6) if random_mask else P.bhattacharyya_mask(c["N"], c["K"], c["design_db"])
     _run(fr, min(c["L"], 8), c["crc_poly"], (1.5,), 200, 41, nonsys=True, lk=lk)
@@ -119,14 +115,16 @@ def test_list_degenerate_and_limits():
     llr = (1.0 - 2.0 * dec.encode(blk).float()) * 4.0
     r = dec.decode_list(llr)
     assert torch.equal(r["bits"], blk) and float(r["pm"].abs().max()) == 0.0
-    # a list that cannot fit: L > 32 (any kernel), or the CTA kernel with L * N
-    # too large for shared memory (the packed kernel moves stages to L2)
-    for L, N, K, lk in ((33, 128, 64, "auto"), (32, 4096, 3072, "cta")):
-        d2 = P.PolarSCS(P.bhattacharyya_mask(N, K, 2.0), 8, L, 0, list_kernel=lk)
-        assert d2.info["list_ctas"] == 0
-        with pytest.raises(P.PolarError) as ei:
-            d2.decode_list(torch.zeros((1, N), dtype=torch.float32, device="cuda"))
-        assert ei.value.code == P.POLAR_ENOTSYS
+    # a list that cannot fit: L > 32
+    d2 = P.PolarSCS(P.bhattacharyya_mask(128, 64, 2.0), 8, 33, 0)
+    assert d2.info["list_ctas"] == 0
+    with pytest.raises(P.PolarError) as ei:
+        d2.decode_list(torch.zeros((1, 128), dtype=torch.float32, device="cuda"))
+    assert ei.value.code == P.POLAR_ENOTSYS
+    # the removed CTA-per-frame list kernel's flag is rejected at create
+    with pytest.raises(P.PolarError) as ei:
+        P.PolarSCS(fr, 8, 8, 0, list_kernel="packed", flags_extra=P.POLAR_FLAG_LIST_CTA)
+    assert ei.value.code == P.POLAR_EINVAL
 
 
 def test_list_full_size_sampled_parity_c2():

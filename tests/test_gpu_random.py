@@ -104,8 +104,7 @@ def test_random_list_parity(seed):
     L = min(L, 32)
     if not nonsys and not P.PolarSCS(fr, 1, 1, 0).info["systematic_ok"]:
         nonsys = True
-    dec = P.PolarSCS(fr, 8, L, crc, bit_level=bit_level, nonsystematic=nonsys,
-                     list_kernel=("packed" if seed % 2 else "cta"))
+    dec = P.PolarSCS(fr, 8, L, crc, bit_level=bit_level, nonsystematic=nonsys)
     if dec.info["list_ctas"] == 0:
         pytest.skip("list does not fit shared memory")
     n = 64 if N <= 512 else 16
