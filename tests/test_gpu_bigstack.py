@@ -84,17 +84,15 @@ def test_paper_workload_full_size_sampled():
     res = dec.decode_stats(llr)
     torch.cuda.synchronize()
     pick = ig.sample_frames(nf, 25, seed=13)
-    checked = 0
     for p, eb in enumerate(c["ebno"]):
         payp = np.concatenate([ig.payload_bits(c["seed"], int(f), 1, c["K"] - dec.c) for f in pick])
         nzp = np.concatenate([ig.unit_normals(c["seed"], int(f), 1, c["N"]) for f in pick])
         _, _, ol = _oracle_llr(fr, c["crc_poly"], payp, nzp, eb)
         rows = torch.from_numpy(p * nf + pick).cuda()
         gl = llr[rows].cpu().numpy()
-        same = (gl == ol).all(1)
-        ref = O.SCSDecoder(fr, c["D"], c["L"], c["crc_poly"]).decode(ol[same], threads=8)
-        sub = {k: v[rows[torch.from_numpy(np.nonzero(same)[0]).cuda()]] for k, v in res.items()}
+        assert (gl == ol).all(1).mean() >= 0.9, f"P@{eb}: device LLR rows differ from the recipe"
+        # the oracle decodes the GPU's own rows (same float32 LLRs in, same result out)
+        ref = O.SCSDecoder(fr, c["D"], c["L"], c["crc_poly"]).decode(gl, threads=8)
+        sub = {k: v[rows] for k, v in res.items()}
         _compare(sub, ref, f"P full @{eb}")
-        checked += int(same.sum())
-    assert checked >= 18 * npts
     assert int((res["status"] == 2).sum()) == 0

@@ -336,10 +336,12 @@ def test_full_size_sampled_parity_c2():
 @pytest.mark.parametrize("cfg", ["C3", "C4", "C5"])
 def test_full_size_sampled_parity_device_generator(cfg):
     """BASELINE configs at full size in one decode call (the bench's launch
-    configuration), inputs from the device generator.  Sampled frames: the GPU
-    LLR row must equal the oracle's row built from the same Philox draws
-    (double Box-Muller on both sides; a rare 1-ulp difference skips the frame),
-    then bits / PM / pops / switches / status must match the oracle."""
+    configuration), inputs from the device generator.  Sampled frames: the
+    oracle decodes the GPU's own LLR rows (the decoder contract is "same
+    float32 LLRs in, same result out"), bits / PM / pops / switches / status
+    must match; separately, the device rows must equal the oracle's recipe
+    built from the same Philox draws on at least 90% of the rows (double
+    Box-Muller on both sides; a rare 1-ulp difference is allowed there)."""
     c, fr = _mk(cfg)
     dec = P.PolarSCS(fr, c["D"], c["L"], c["crc_poly"])
     nf, npts = c["frames"], len(c["ebno"])
@@ -349,20 +351,17 @@ def test_full_size_sampled_parity_device_generator(cfg):
     res = dec.decode_stats(llr)
     torch.cuda.synchronize()
     pick = ig.sample_frames(nf, 40, seed=11)
-    checked = 0
     for p, eb in enumerate(c["ebno"]):
         payp = np.concatenate([ig.payload_bits(c["seed"], int(f), 1, c["K"] - dec.c) for f in pick])
         nzp = np.concatenate([ig.unit_normals(c["seed"], int(f), 1, c["N"]) for f in pick])
         _, _, ol = _oracle_llr(fr, c["crc_poly"], payp, nzp, eb)
         rows = torch.from_numpy(p * nf + pick).cuda()
         gl = llr[rows].cpu().numpy()
-        same = (gl == ol).all(1)
-        assert same.mean() >= 0.9, f"{cfg}@{eb}: device LLR rows differ from the recipe"
-        ref = O.SCSDecoder(fr, c["D"], c["L"], c["crc_poly"]).decode(ol[same], threads=8)
-        sub = {k: v[rows[torch.from_numpy(np.nonzero(same)[0]).cuda()]] for k, v in res.items()}
+        assert (gl == ol).all(1).mean() >= 0.9, f"{cfg}@{eb}: device LLR rows differ from the recipe"
+        np.testing.assert_allclose(gl, ol, rtol=1e-5, atol=1e-5)
+        ref = O.SCSDecoder(fr, c["D"], c["L"], c["crc_poly"]).decode(gl, threads=8)
+        sub = {k: v[rows] for k, v in res.items()}
         _compare(sub, ref, f"{cfg} full @{eb}")
-        checked += int(same.sum())
-    assert checked >= 30 * npts
     assert int((res["status"] == 2).sum()) == 0          # watchdog never fires
 
 
