@@ -537,63 +537,81 @@ def cpu_model():
 
 def oracle_leg(cfg, c, llr, stats, nf, npts, is_list, args):
     """The oracle (as it stands) decodes the frames this run decoded, from the
-    GPU-generated LLR buffer copied to the host: every frame when the workload
-    fits the time budget (C2: 500,000 frames, ~13 s on 16 threads), else the
-    same-length prefix of every Eb/N0 point.  Returns parity (bits, status,
-    pops, switches exact; PM rel 1e-6, the north star's contract), the
-    cpu_baseline (aggregate, per-thread average as the paper reports it
-    (PAPER.md:L968), a 1-thread figure on a ~10^4-frame prefix) and the O10
-    census of those frames (the roofline's algorithmic numerator)."""
+    GPU-generated LLR buffer copied to the host in chunks: every frame when the
+    workload fits the budget (C2: 500,000 frames, ~13 s on 16 threads), else
+    the same-length prefix of every Eb/N0 point (--parity-frames raises it).
+    Returns parity (bits, status, pops, switches exact; PM rel 1e-6, the north
+    star's contract), the cpu_baseline (aggregate, per-thread average as the
+    paper reports it, a 1-thread figure on a ~10^4-frame
+    prefix) and the O10 census of those frames (the roofline's algorithmic
+    numerator, a second untimed pass: counting slows the oracle down)."""
     import numpy as np
     threads = os.cpu_count() or 1
     N, K = c["N"], c["K"]
     cap = args.parity_frames if args.parity_frames > 0 else max(1, int(6e8 // (N * max(1, npts))))
     per = min(nf, cap)
     dec = oracle_decoder(c)
-    rows = np.concatenate([np.arange(p * nf, p * nf + per) for p in range(npts)])
-    llr_h = llr.cpu().numpy() if per == nf else llr[torch_index(rows, llr.device)].cpu().numpy()
-    t0 = time.perf_counter()
-    ref = dec.decode(llr_h, threads=threads)          # timed: the oracle as it stands
-    dt = time.perf_counter() - t0
-    g = {k: v[torch_index(rows, v.device)].cpu().numpy() if per < nf else v.cpu().numpy()
-         for k, v in stats.items() if v is not None}
-    n = rows.size
-    bad_bits = int((g["bits"] != ref["bits"]).any(1).sum())
-    bad_status = int((g["status"] != ref["status"]).sum())
-    pm_rel = np.abs(g["pm"].astype(np.float64) - ref["pm"]) / np.maximum(np.abs(ref["pm"].astype(np.float64)), 1e-30)
-    pm_rel[(g["pm"] == ref["pm"])] = 0.0
-    parity = {"frames": n, "of": nf * npts, "mismatched_bits": bad_bits, "mismatched_status": bad_status,
-              "pm_max_rel": float(pm_rel.max()) if n else 0.0, "pm_over_1e-6": int((pm_rel > 1e-6).sum()),
+    chunk = max(1, min(per, int(2.5e8 // (4 * N))))           # <= 1 GB of LLRs on the host at a time
+    bad = {"bits": 0, "status": 0, "pops": 0, "switches": 0, "pm": 0}
+    pm_max = 0.0
+    dt = 0.0
+    ct_tot = {}
+    first = None                                               # LLRs of the 1-thread sample
+    k1 = None
+    for p in range(npts):
+        for a in range(0, per, chunk):
+            b = min(per, a + chunk)
+            sl = slice(p * nf + a, p * nf + b)
+            lh = llr[sl].cpu().numpy()
+            t0 = time.perf_counter()
+            ref = dec.decode(lh, threads=threads)              # timed: the oracle as it stands
+            dt += time.perf_counter() - t0
+            g = {k: v[sl].cpu().numpy() for k, v in stats.items() if v is not None}
+            bad["bits"] += int((g["bits"] != ref["bits"]).any(1).sum())
+            bad["status"] += int((g["status"] != ref["status"]).sum())
+            rel = np.abs(g["pm"].astype(np.float64) - ref["pm"]) / np.maximum(np.abs(ref["pm"].astype(np.float64)),
+                                                                              1e-30)
+            rel[g["pm"] == ref["pm"]] = 0.0
+            pm_max = max(pm_max, float(rel.max()) if rel.size else 0.0)
+            bad["pm"] += int((rel > 1e-6).sum())
+            if not is_list:
+                bad["pops"] += int((g["pops"].astype(np.uint32) != ref["pops"]).sum())
+                bad["switches"] += int((g["switches"].astype(np.uint32) != ref["switches"]).sum())
+                for k, v in dec.decode(lh, threads=threads, counters=True)["counters"].items():
+                    ct_tot[k] = max(ct_tot.get(k, 0), v) if k == "stack_peak" else ct_tot.get(k, 0) + v
+            if a == 0:
+                if k1 is None:
+                    fps_est = (b - a) / max(dt, 1e-9)
+                    k1 = max(1, min(per, int(min(10_000, 8.0 * fps_est / threads)) // npts, b - a))
+                first = lh[:k1] if first is None else np.concatenate([first, lh[:k1]])
+    n = per * npts
+    parity = {"frames": n, "of": nf * npts, "mismatched_bits": bad["bits"], "mismatched_status": bad["status"],
+              "pm_max_rel": pm_max, "pm_over_1e-6": bad["pm"],
               "contract": "bits, status" + ("" if is_list else ", pops, switches") + " exact; PM rel 1e-6 "
                           "(BASELINE.json north_star)",
               "frames_checked": "all" if per == nf else f"first {per} of each Eb/N0 point"}
     if not is_list:
-        parity["mismatched_pops"] = int((g["pops"].astype(np.uint32) != ref["pops"]).sum())
-        parity["mismatched_switches"] = int((g["switches"].astype(np.uint32) != ref["switches"]).sum())
-    parity["mismatched"] = (bad_bits + bad_status + parity["pm_over_1e-6"] + parity.get("mismatched_pops", 0)
-                            + parity.get("mismatched_switches", 0))
+        parity["mismatched_pops"] = bad["pops"]
+        parity["mismatched_switches"] = bad["switches"]
+    parity["mismatched"] = sum(bad.values())
     fps = n / dt
-    payload = K - (O_crc_degree(c["crc_poly"]))
+    payload = K - O_crc_degree(c["crc_poly"])
     # 1 thread on a ~10^4-frame prefix (the same share of every point), cut to
     # ~8 s of work by the measured multi-thread rate
-    k1 = max(1, min(per, int(min(10_000, 8.0 * fps / threads)) // npts))
-    sel1 = np.concatenate([np.arange(p * per, p * per + k1) for p in range(npts)])
     t0 = time.perf_counter()
-    dec.decode(llr_h[sel1], threads=1)
+    dec.decode(first, threads=1)
     dt1 = time.perf_counter() - t0
     cpu = {"value": fps * K / 1e6, "unit": "Mbps", "cores": threads, "kind": "oracle",
            "frames_per_s": fps, "seconds": dt, "cpu_model": cpu_model(),
            "per_thread_Mbps": fps * K / 1e6 / threads, "payload_Mbps": fps * payload / 1e6,
-           "one_thread": {"Mbps": sel1.size / dt1 * K / 1e6, "frames": int(sel1.size), "seconds": dt1,
-                          "sample": f"first {sel1.size // npts} frames of each Eb/N0 point"},
+           "one_thread": {"Mbps": first.shape[0] / dt1 * K / 1e6, "frames": int(first.shape[0]), "seconds": dt1,
+                          "sample": f"first {k1} frames of each Eb/N0 point"},
            "sample": (f"all {n} frames of this run's workload" if per == nf else
                       f"first {per} frames of each of the {npts} Eb/N0 points ({n} of {nf * npts})") +
                      f", this run's GPU-generated LLRs copied to the host, {threads} threads, decode only"}
     census = None
     if not is_list:
-        # O10 counters over the same frames (a second, untimed pass: counting
-        # slows the oracle down)
-        ct = dec.decode(llr_h, threads=threads, counters=True)["counters"]
+        ct = ct_tot
         fg_alg = ct["f_ops"] + ct["g_ops"]
         census = {"ops_per_frame": (fg_alg + ct["node_elems"] + ct["beta_xor_bits"] + ct["key_compares"]) / n,
                   "smem_bytes_per_frame": (12 * fg_alg + 4 * ct["node_elems"]) / n,
