@@ -46,6 +46,7 @@ def parse():
     ap.add_argument("--frames", type=int, default=0, help="override frames per Eb/N0 point")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true", help="skip the oracle leg (parity, cpu_baseline, census)")
+    ap.add_argument("--no-census", action="store_true", help="oracle leg without its O10 counter pass")
     ap.add_argument("--parity-frames", type=int, default=0,
                     help="frames per Eb/N0 point the oracle checks (0: all that fit ~6e8 LLRs)")
     ap.add_argument("--cpu-seconds", type=float, default=15.0,
@@ -577,6 +578,7 @@ def oracle_leg(cfg, c, llr, stats, nf, npts, is_list, args):
             if not is_list:
                 bad["pops"] += int((g["pops"].astype(np.uint32) != ref["pops"]).sum())
                 bad["switches"] += int((g["switches"].astype(np.uint32) != ref["switches"]).sum())
+            if not is_list and not args.no_census:
                 for k, v in dec.decode(lh, threads=threads, counters=True)["counters"].items():
                     ct_tot[k] = max(ct_tot.get(k, 0), v) if k == "stack_peak" else ct_tot.get(k, 0) + v
             if a == 0:
@@ -610,7 +612,7 @@ def oracle_leg(cfg, c, llr, stats, nf, npts, is_list, args):
                       f"first {per} frames of each of the {npts} Eb/N0 points ({n} of {nf * npts})") +
                      f", this run's GPU-generated LLRs copied to the host, {threads} threads, decode only"}
     census = None
-    if not is_list:
+    if not is_list and not args.no_census:
         ct = ct_tot
         fg_alg = ct["f_ops"] + ct["g_ops"]
         census = {"ops_per_frame": (fg_alg + ct["node_elems"] + ct["beta_xor_bits"] + ct["key_compares"]) / n,

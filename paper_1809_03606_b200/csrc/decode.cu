@@ -200,10 +200,10 @@ __device__ __forceinline__ int alloc_snapshot_big(uint32_t *used, int &uhint, co
     for (int pass = 0; pass < 2 && slot < 0; pass++) {
         if (pass == 1) {
             #pragma unroll 1
-            for (int w = lane; w < UW; w += 32) used[w] = 0u;
+            for (int w_0 = 0; w_0 < (UW); w_0 += 32) if (const int w = w_0 + lane; w < (UW)) used[w] = 0u;
             __syncwarp();
             #pragma unroll 1
-            for (int i = lane; i < nS; i += 32) {
+            for (int i_0 = 0; i_0 < (nS); i_0 += 32) if (const int i = i_0 + lane; i < (nS)) {
                 const uint32_t sn = Pk<true>::snap(sjsm[i]);
                 if (i != skip && sn != Pk<true>::NONE) atomicOr(used + (sn >> 5), 1u << (sn & 31));
             }
@@ -365,7 +365,7 @@ fsscs_decode_kernel(const DecodeParams P) {
             }
         }
         #pragma unroll 1
-        for (int i = lane; i < P.cnt_words; i += 32) reinterpret_cast<uint32_t *>(cnt)[i] = 0;
+        for (int i_0 = 0; i_0 < (P.cnt_words); i_0 += 32) if (const int i = i_0 + lane; i < (P.cnt_words)) reinterpret_cast<uint32_t *>(cnt)[i] = 0;
         __syncwarp();
 
         // ---- stack: root path (PM 0, serial 0, j 0) ------------------------
@@ -380,7 +380,7 @@ fsscs_decode_kernel(const DecodeParams P) {
         if (BIG) {
             if (lane == 0) { kset(0, 0ull); sjsm[0] = PK::make(0, PK::NONE, 0); }
             #pragma unroll 1
-            for (int w = lane; w < P.used_words; w += 32) snap_used[w] = 0u;
+            for (int w_0 = 0; w_0 < (P.used_words); w_0 += 32) if (const int w = w_0 + lane; w < (P.used_words)) snap_used[w] = 0u;
         } else if (lane < 4) {
             snap_used[lane] = 0u;      // conservative snapshot-slot bitmap (alloc_snapshot_lazy)
         }
@@ -532,7 +532,7 @@ fsscs_decode_kernel(const DecodeParams P) {
                             const int nwords = (work_pl + 31) >> 5;
                             if constexpr (CNT) c_sw += (uint32_t)nwords;
                             #pragma unroll 1
-                            for (int w = lane; w < nwords; w += 32) dst[w] = beta[w];
+                            for (int w_0 = 0; w_0 < (nwords); w_0 += 32) if (const int w = w_0 + lane; w < (nwords)) dst[w] = beta[w];
                             if (lane == 0) sjsm[wi] = PK::make(PK::j(wj), (uint32_t)slot, 0);
                             __syncwarp();
                         }
@@ -555,7 +555,7 @@ fsscs_decode_kernel(const DecodeParams P) {
                         const int nwords = (work_pl + 31) >> 5;
                         if constexpr (CNT) c_sw += (uint32_t)nwords;
                         #pragma unroll 1
-                        for (int w = lane; w < nwords; w += 32) dst[w] = beta[w];
+                        for (int w_0 = 0; w_0 < (nwords); w_0 += 32) if (const int w = w_0 + lane; w < (nwords)) dst[w] = beta[w];
                         if (lane == wl) {
 #pragma unroll
                             for (int s = 0; s < SL; s++)
@@ -594,7 +594,7 @@ fsscs_decode_kernel(const DecodeParams P) {
                     if (pkind == OP_REP) {
                         if (Lam >= 32) {
                             #pragma unroll 1
-                            for (int t = lane; t < (Lam >> 5); t += 32) beta[(seg >> 5) + t] ^= FULL;
+                            for (int t_0 = 0; t_0 < ((Lam >> 5)); t_0 += 32) if (const int t = t_0 + lane; t < ((Lam >> 5))) beta[(seg >> 5) + t] ^= FULL;
                         } else if (lane == 0) {
                             beta[seg >> 5] ^= ((1u << Lam) - 1u) << (seg & 31);
                         }
@@ -650,14 +650,14 @@ fsscs_decode_kernel(const DecodeParams P) {
                     const uint32_t *cw = beta;
                     if (MODE == 0 && P.nonsys) {
                         #pragma unroll 1
-                        for (int w = lane; w < nw; w += 32) uhat[w] = beta[w];
+                        for (int w_0 = 0; w_0 < (nw); w_0 += 32) if (const int w = w_0 + lane; w < (nw)) uhat[w] = beta[w];
                         __syncwarp();
                         xform_words(uhat, N, nw, lane);
                         cw = uhat;
                     }
                     uint32_t syn = 0;
                     #pragma unroll 1
-                    for (int w = lane; w < nw; w += 32) {
+                    for (int w_0 = 0; w_0 < (nw); w_0 += 32) if (const int w = w_0 + lane; w < (nw)) {
                         const uint32_t x = cw[w];
                         const uint32_t *tw = P.crc_bytes + (size_t)w * 1024;
                         syn ^= __ldg(tw + (x & 255u)) ^ __ldg(tw + 256 + ((x >> 8) & 255u)) ^
@@ -671,20 +671,12 @@ fsscs_decode_kernel(const DecodeParams P) {
                 // data-dependent loop exit made ptxas treat the loop as divergent)
                 if (!have_best) {
                     #pragma unroll 1
-                    for (int w = lane; w < nw; w += 32) best[w] = beta[w];
+                    for (int w_0 = 0; w_0 < (nw); w_0 += 32) if (const int w = w_0 + lane; w < (nw)) best[w] = beta[w];
                     __syncwarp();
-                }
-                if (ok) { out_pm = p_pm; status = 0; break; }
-                // the climb above combined blocks that the alpha memory was
-                // computed from, so beta no longer tells the next switch which
-                // stages are stale: recompute the next spine from the channel
-                lev_mem = n;
-                if (!have_best) {
-                    have_best = true;
-                    best_pm = p_pm;
                 }
                 if (BIG && hole >= 0) {
                     // no candidate refills the hole: the last entry moves into it
+                    // (before the exit test too, for the same reason as the copy)
                     if (hole != nA - 1) {
                         const unsigned long long k = kget(nA - 1);
                         const uint32_t x = __ldcg(sjsm + nA - 1);
@@ -695,6 +687,15 @@ fsscs_decode_kernel(const DecodeParams P) {
                     __syncwarp();
                     nA--;
                     hole = -1;
+                }
+                if (ok) { out_pm = p_pm; status = 0; break; }
+                // the climb above combined blocks that the alpha memory was
+                // computed from, so beta no longer tells the next switch which
+                // stages are stale: recompute the next spine from the channel
+                lev_mem = n;
+                if (!have_best) {
+                    have_best = true;
+                    best_pm = p_pm;
                 }
                 continue;
             }
@@ -800,7 +801,7 @@ fsscs_decode_kernel(const DecodeParams P) {
             } else if (MODE == 0 && lam == n) {
                 // whole code is one node: copy the channel so the sums can work in place
                 #pragma unroll 1
-                for (int i = lane; i < N; i += 32) alpha[i] = ld1<CHAN_SMEM>(chan + i, true);
+                for (int i_0 = 0; i_0 < (N); i_0 += 32) if (const int i = i_0 + lane; i < (N)) alpha[i] = ld1<CHAN_SMEM>(chan + i, true);
                 __syncwarp();
                 a = alpha;
             }
@@ -934,7 +935,7 @@ fsscs_decode_kernel(const DecodeParams P) {
                     const uint32_t fill = (kind == OP_REP && m0) ? FULL : 0u;
                     if (Lam >= 32) {
                         #pragma unroll 1
-                        for (int t = lane; t < (Lam >> 5); t += 32) beta[(seg >> 5) + t] = fill;
+                        for (int t_0 = 0; t_0 < ((Lam >> 5)); t_0 += 32) if (const int t = t_0 + lane; t < ((Lam >> 5))) beta[(seg >> 5) + t] = fill;
                     } else if (lane == 0) {
                         const uint32_t lm = ((1u << Lam) - 1u) << (seg & 31);
                         beta[seg >> 5] = (beta[seg >> 5] & ~lm) | (fill & lm);
@@ -976,7 +977,7 @@ fsscs_decode_kernel(const DecodeParams P) {
                 const int nwords = (npl + 31) >> 5;
                 if constexpr (CNT) c_sw += (uint32_t)nwords;
                 #pragma unroll 1
-                for (int w = lane; w < nwords; w += 32) dst[w] = beta[w];
+                for (int w_0 = 0; w_0 < (nwords); w_0 += 32) if (const int w = w_0 + lane; w < (nwords)) dst[w] = beta[w];
                 if (lane == 0) *hdr_at(fslot) = make_uint2(mi[0] | (mi[1] << 16), mi[2] | (mi[3] << 16));
             };
             if (nfit > 1) write_fork_snapshot(-1, -1);
@@ -1035,7 +1036,7 @@ fsscs_decode_kernel(const DecodeParams P) {
                 if (BIG) {
                     unsigned long long xk = 0;
                     #pragma unroll 1
-                    for (int i = lane; i < nA; i += 32) {
+                    for (int i_0 = 0; i_0 < (nA); i_0 += 32) if (const int i = i_0 + lane; i < (nA)) {
                         const unsigned long long k = kget(i);
                         if (xs < 0 || k > xk) { xk = k; xs = i; }
                     }
@@ -1082,14 +1083,14 @@ fsscs_decode_kernel(const DecodeParams P) {
             const uint32_t *bsrc = from_best ? best : beta;
             if (MODE == 0 && P.nonsys) {
                 #pragma unroll 1
-                for (int w = lane; w < nw; w += 32) uhat[w] = bsrc[w];
+                for (int w_0 = 0; w_0 < (nw); w_0 += 32) if (const int w = w_0 + lane; w < (nw)) uhat[w] = bsrc[w];
                 __syncwarp();
                 xform_words(uhat, N, nw, lane);
                 bsrc = uhat;
             }
             uint8_t *ob = P.out_bits + (size_t)f * K;
             #pragma unroll 1
-            for (int q = lane; q < K; q += 32) {
+            for (int q_0 = 0; q_0 < (K); q_0 += 32) if (const int q = q_0 + lane; q < (K)) {
                 const int idx = P.info[q];
                 ob[q] = (uint8_t)((bsrc[idx >> 5] >> (idx & 31)) & 1u);
             }

@@ -22,9 +22,14 @@ constexpr uint32_t FULL = 0xFFFFFFFFu;
 // the sign bits, so it differs from a comparison-based sign only when an input
 // is -0, i.e. when the result is a zero: HD, |.|, the PM sums and every later
 // f/g see +0 and -0 alike (reading R2), so bits, PMs and counts are unchanged.
+// The sign is taken from the product a*b (IEEE: its sign bit is the XOR of the
+// operands' sign bits, zeros and underflow included), so the sign costs one
+// FMA-pipe multiply and the merge one logic op instead of two logic ops.  A
+// NaN product needs inf * 0, and then m = 0: only a zero's sign can differ.
 __device__ __forceinline__ float f_minsum(float a, float b) {
     const float m = fminf(fabsf(a), fabsf(b));
-    return __uint_as_float(__float_as_uint(m) | ((__float_as_uint(a) ^ __float_as_uint(b)) & 0x80000000u));
+    const float p = __fmul_rn(a, b);
+    return __uint_as_float(__float_as_uint(m) | (__float_as_uint(p) & 0x80000000u));
 }
 // corrected Eq. (2): g = a_hi + (1 - 2 beta) a_lo (reading R1); a_hi - a_lo is
 // a_hi + (-a_lo) exactly, so flipping the sign bit of a_lo is exact.
@@ -40,7 +45,7 @@ __device__ __forceinline__ void beta_op(uint32_t *beta, int lam, int phi, int la
     if (Lam >= 32) {
         const int wd = ((phi - 1) * Lam) >> 5, ws = (phi * Lam) >> 5, nwd = Lam >> 5;
         #pragma unroll 1
-        for (int t = lane; t < nwd; t += 32) beta[wd + t] ^= beta[ws + t];
+        for (int t_0 = 0; t_0 < (nwd); t_0 += 32) if (const int t = t_0 + lane; t < (nwd)) beta[wd + t] ^= beta[ws + t];
     } else if (lane == 0) {
         const int p = (phi - 1) * Lam;             // 2*Lam bits inside one word
         const int w = p >> 5, o = p & 31;
@@ -56,7 +61,7 @@ __device__ __forceinline__ void beta_op(uint32_t *beta, int lam, int phi, int la
 __device__ __forceinline__ void xform_words(uint32_t *w, int N, int nw, int lane) {
     const uint32_t masks[5] = {0x55555555u, 0x33333333u, 0x0F0F0F0Fu, 0x00FF00FFu, 0x0000FFFFu};
     #pragma unroll 1
-    for (int j = lane; j < nw; j += 32) {
+    for (int j_0 = 0; j_0 < (nw); j_0 += 32) if (const int j = j_0 + lane; j < (nw)) {
         uint32_t x = w[j];
 #pragma unroll
         for (int s = 0; s < 5; s++)
@@ -67,7 +72,7 @@ __device__ __forceinline__ void xform_words(uint32_t *w, int N, int nw, int lane
     #pragma unroll 1
     for (int H = 1; H < nw; H <<= 1) {
         #pragma unroll 1
-        for (int j = lane; j < nw; j += 32)
+        for (int j_0 = 0; j_0 < (nw); j_0 += 32) if (const int j = j_0 + lane; j < (nw))
             if ((j & H) == 0) w[j] ^= w[j + H];
         __syncwarp();
     }

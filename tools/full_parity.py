@@ -8,7 +8,7 @@ import sys
 
 for cfg in sys.argv[1:]:
     out = subprocess.run([sys.executable, "bench.py", "--config", cfg, "--steps", "1", "--warmup", "3", "--no-e2e",
-                          "--parity-frames", "100000000"], capture_output=True, text=True)
+                          "--parity-frames", "100000000", "--no-census"], capture_output=True, text=True)
     line = [l for l in out.stdout.splitlines() if l.startswith("{")]
     if not line:
         print(json.dumps({"config": cfg, "error": out.stderr[-2000:]}), flush=True)
