@@ -26,6 +26,10 @@
 
 namespace polar {
 
+#ifndef POLAR_SORTED_STACK
+#define POLAR_SORTED_STACK 1   // 0: the unsorted register stack for D <= 32 too (A/B builds)
+#endif
+
 constexpr uint32_t EMPTY = 0xFFFFFFFFu;
 constexpr uint32_t NO_SNAP = 0xFFFFu;
 
@@ -241,9 +245,15 @@ __device__ __forceinline__ int alloc_snapshot_big(uint32_t *used, int &uhint, co
 // launch bound (CTAs of 4 warps per SM) per instantiation: register stacks
 // of 2 or 4 entries per lane need more registers; the N = 2048 and N = 4096
 // specialisations trade registers for warps (measured)
+#ifndef POLAR_MB_PLAIN
+#define POLAR_MB_PLAIN 9       // CTAs per SM of the no-CRC register-stack instances (A/B builds override)
+#endif
+#ifndef POLAR_MB_SL1
+#define POLAR_MB_SL1 kDecodeMinBlocks
+#endif
 template <int SLOTS, int NL, bool NOCRC>
 constexpr int kDecodeMinBlocksFor() {
-    return NL == 11 ? 6 : (NL == 12 ? 5 : (SLOTS == 4 ? 3 : (SLOTS == 2 ? 5 : (NOCRC && SLOTS == 1 ? 9 : kDecodeMinBlocks))));
+    return NL == 11 ? 6 : (NL == 12 ? 5 : (SLOTS == 4 ? 3 : (SLOTS == 2 ? 5 : (NOCRC && SLOTS == 1 ? POLAR_MB_PLAIN : (SLOTS == 1 ? POLAR_MB_SL1 : kDecodeMinBlocks)))));
 }
 
 // SLOTS = 1, 2, 4: register stack of 32 SLOTS entries (D <= 128).  SLOTS = 0:
@@ -260,6 +270,9 @@ __global__ void __launch_bounds__(kDecodeWarps * 32, kDecodeMinBlocksFor<SLOTS, 
 fsscs_decode_kernel(const DecodeParams P) {
     constexpr bool BIG = (SLOTS == 0);
     constexpr int SL = BIG ? 1 : SLOTS;       // register arrays (unused when BIG)
+    // D <= 32: the register stack is kept sorted by (PM, serial), one entry per
+    // lane (lane 0 = best): select reads the head, insertion is one merge
+    constexpr bool SORTED = (SLOTS == 1) && (POLAR_SORTED_STACK != 0);
     using PK = Pk<BIG>;
     extern __shared__ __align__(16) uint32_t smem[];
     const int lane = threadIdx.x & 31;
@@ -440,16 +453,26 @@ fsscs_decode_kernel(const DecodeParams P) {
                 // speculative: every lane fetches the jsm word of its own best entry
                 // while the warp reduction runs
                 ljsm_big = (lk != ~0ull) ? __ldcg(sjsm + ls) : 0u;
-            } else {
+            } else if (!SORTED) {
 #pragma unroll
                 for (int s = 0; s < SL; s++)
                     if (s_pm[s] < lpm || (s_pm[s] == lpm && s_ser[s] < lser)) { lpm = s_pm[s]; lser = s_ser[s]; ljsm = s_jsm[s]; ls = s; }
             }
             uint32_t mpm, mser;
-            warp_min_key(lpm, lser, mpm, mser);
-            const int owner = __ffs(__ballot_sync(FULL, lpm == mpm && lser == mser)) - 1;
+            int owner = 0;
+            if (SORTED) {
+                // the sorted stack's head (lane 0) is the best path
+                mpm = __shfl_sync(FULL, s_pm[0], 0);
+                mser = __shfl_sync(FULL, s_ser[0], 0);
+            } else {
+                warp_min_key(lpm, lser, mpm, mser);
+                owner = __ffs(__ballot_sync(FULL, lpm == mpm && lser == mser)) - 1;
+            }
             uint32_t p_jsm;
-            if (BIG) {
+            if (SORTED) {
+                p_jsm = __shfl_sync(FULL, s_jsm[0], 0);
+                if (lane == 0) { s_pm[0] = EMPTY; s_ser[0] = EMPTY; }
+            } else if (BIG) {
                 // remove entry `pi`: it becomes a hole that c1 of this pop refills
                 const int pi = __shfl_sync(FULL, ls, owner);
                 p_jsm = __shfl_sync(FULL, ljsm_big, owner);
@@ -501,6 +524,24 @@ fsscs_decode_kernel(const DecodeParams P) {
                     nA = cntv;
                     hole = -1;
                     __syncwarp();
+                } else if (SORTED) {
+                    // survivors (depth > j) move to lanes 1..cntv in order (a subset
+                    // of a sorted list is sorted); lane 0 stays free
+                    const uint32_t kb = __ballot_sync(FULL, s_ser[0] != EMPTY && (int)jsm_j(s_jsm[0]) > j);
+                    cntv = __popc(kb);
+                    const bool dst = (lane >= 1 && lane <= cntv);
+                    // source lane = position of the lane-th set bit of kb (binary search on prefix counts)
+                    int src = 0;
+#pragma unroll
+                    for (int st = 16; st >= 1; st >>= 1) {
+                        const int hi = src + st - 1;                  // bits [0, hi] hold fewer than `lane` survivors?
+                        if (__popc(kb & (hi >= 31 ? FULL : ((2u << hi) - 1u))) < lane) src += st;
+                    }
+                    const uint32_t npm = __shfl_sync(FULL, s_pm[0], src), nser = __shfl_sync(FULL, s_ser[0], src);
+                    const uint32_t njsm = __shfl_sync(FULL, s_jsm[0], src);
+                    s_pm[0] = dst ? npm : EMPTY;
+                    s_ser[0] = dst ? nser : EMPTY;
+                    s_jsm[0] = njsm;
                 } else {
 #pragma unroll
                     for (int s = 0; s < SL; s++) {
@@ -687,6 +728,14 @@ fsscs_decode_kernel(const DecodeParams P) {
                     __syncwarp();
                     nA--;
                     hole = -1;
+                }
+                if (SORTED) {
+                    // nothing is inserted: the entries in lanes 1..nS move to 0..nS-1
+                    // (before the exit test too, for the same reason as the copy)
+                    s_pm[0] = __shfl_down_sync(FULL, s_pm[0], 1);
+                    s_ser[0] = __shfl_down_sync(FULL, s_ser[0], 1);
+                    s_jsm[0] = __shfl_down_sync(FULL, s_jsm[0], 1);
+                    if (lane == 31) { s_pm[0] = EMPTY; s_ser[0] = EMPTY; }
                 }
                 if (ok) { out_pm = p_pm; status = 0; break; }
                 // the climb above combined blocks that the alpha memory was
@@ -980,9 +1029,46 @@ fsscs_decode_kernel(const DecodeParams P) {
                 for (int w_0 = 0; w_0 < (nwords); w_0 += 32) if (const int w = w_0 + lane; w < (nwords)) dst[w] = beta[w];
                 if (lane == 0) *hdr_at(fslot) = make_uint2(mi[0] | (mi[1] << 16), mi[2] | (mi[3] << 16));
             };
-            if (nfit > 1) write_fork_snapshot(-1, -1);
+            if (!SORTED && nfit > 1) write_fork_snapshot(-1, -1);
             int c1_lane = 0, c1_slot = 0;
-            if (BIG) {
+            if (SORTED) {
+                // merge the candidates into the sorted stack, keeping the D smallest
+                // keys.  Equivalent to c1 always + siblings while |S| < D + strict-PM
+                // replacement of the worst (reading R8): candidate
+                // serials exceed every live serial, so "PM < worst PM" is "key <
+                // worst key", and the sequential rule keeps the D smallest keys.
+                // Entries: lanes 1..nS (sorted); candidate t: lane t, key ascending in t.
+                const uint32_t cpm = __float_as_uint(p_pm + my_d);
+                const uint32_t epm = s_pm[0];
+                // a = #{t < nc : cpm_t < epm} (candidate keys ascend: binary search)
+                int a = 0;
+                if (nc > 4) { if (__shfl_sync(FULL, cpm, a + 3) < epm) a += 4; }
+                if (nc > 2) { if (__shfl_sync(FULL, cpm, a + 1) < epm) a += 2; }
+                if (nc > 1) { if (__shfl_sync(FULL, cpm, a) < epm) a += 1; }
+                if (__shfl_sync(FULL, cpm, a) < epm) a += 1;          // a <= nc - 1 before this step
+                const int epos = lane - 1 + a;                      // merged position of entry lane
+                const bool ekeep = lane >= 1 && lane <= nS && epos < D;
+                const uint32_t Mp = __reduce_or_sync(FULL, ekeep ? (1u << epos) : 0u);
+                const int total = min(D, nS + nc);
+                // siblings that survive share one fork snapshot (taken before the
+                // merge, like the unsorted stack: slots of entries the merge drops
+                // count as used here, and at least D - nS slots are free)
+                if (total - __popc(Mp) > 1) write_fork_snapshot(-1, -1);
+                const uint32_t jb = jsm_make(jn, fslot >= 0 ? (uint32_t)fslot : SNAP_NONE, 0);
+                const int q = __popc(Mp & ((1u << lane) - 1u));      // entries before position lane
+                const bool isE = (Mp >> lane) & 1u;
+                const int t = (lane - q) & 7;                       // candidate at position lane
+                const uint32_t gpm = __shfl_sync(FULL, epm, q + 1), gser = __shfl_sync(FULL, s_ser[0], q + 1);
+                const uint32_t gjsm = __shfl_sync(FULL, s_jsm[0], q + 1);
+                const float dt = __shfl_sync(FULL, my_d, t);
+                const bool live = lane < total;
+                const uint32_t mk = (clist >> (4 * t)) & 15u;
+                s_pm[0] = !live ? EMPTY : (isE ? gpm : __float_as_uint(p_pm + dt));
+                s_ser[0] = !live ? EMPTY : (isE ? gser : ser0 + (uint32_t)t);
+                const bool isC = live && !isE;
+                s_jsm[0] = isC ? (jb | ((mk ^ (uint32_t)m0) << 21)) : gjsm;
+                nS = total;
+            } else if (BIG) {
                 const uint32_t jbase = PK::make(jn, (nfit == 1) ? PK::NONE : (uint32_t)fslot, 0);
                 // c1 refills the hole left by p (if any), the siblings are appended
                 const int pos0 = (hole >= 0) ? hole : nA;
@@ -1027,7 +1113,7 @@ fsscs_decode_kernel(const DecodeParams P) {
             // the rest (stack full): replace the least reliable iff strictly better
             // (PAPER.md:L599).  Ranks ascend, so the first one dropped ends the loop.
             #pragma unroll 1
-            for (int r = nfit; r < nc; r++) {
+            for (int r = nfit; !SORTED && r < nc; r++) {
                 const int mt = (int)((clist >> (4 * r)) & 15u);
                 const float dt = __shfl_sync(FULL, my_d, r);
                 const uint32_t cpm = __float_as_uint(p_pm + dt);
@@ -1071,7 +1157,7 @@ fsscs_decode_kernel(const DecodeParams P) {
             if (BIG) {
                 if (fslot >= 0 && lane == 0) sjsm[c1_slot] = PK::make(jn, (uint32_t)fslot, 0);
                 __syncwarp();
-            } else if (fslot >= 0 && lane == c1_lane) {
+            } else if (!SORTED && fslot >= 0 && lane == c1_lane) {
 #pragma unroll
                 for (int s = 0; s < SL; s++) if (s == c1_slot) s_jsm[s] = jsm_make(jn, (uint32_t)fslot, 0);
             }
