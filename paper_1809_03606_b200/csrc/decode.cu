@@ -26,6 +26,9 @@
 
 namespace polar {
 
+#ifndef POLAR_BETA_REGS
+#define POLAR_BETA_REGS 1      // 0: the flat beta in shared memory in every kernel (A/B builds)
+#endif
 #ifndef POLAR_SORTED_STACK
 #define POLAR_SORTED_STACK 1   // 0: the unsorted register stack for D <= 32 too (A/B builds)
 #endif
@@ -48,9 +51,10 @@ __device__ __forceinline__ float ld1(const float *p, bool) {
 }
 
 // src: stage s+1 (or the channel row when s+1 == n); dst: stage s.  UNR:
-// unroll the float4 loop (independent iterations; measured on n = 10 only)
-template <bool CHAN_SMEM, bool UNR = false>
-__device__ __forceinline__ void alpha_stage(const float *src, float *dst, const uint32_t *beta,
+// unroll the float4 loop (independent iterations; measured on n = 10 only).
+// BR: the flat beta is held in registers, word w in lane w (bw), not in beta[]
+template <bool CHAN_SMEM, bool UNR = false, bool BR = false>
+__device__ __forceinline__ void alpha_stage(const float *src, float *dst, const uint32_t *beta, uint32_t bw,
                                             int n, int s, int psi, int lane) {
     const int Ls = 1 << s;
     const bool top = (s + 1 == n);
@@ -61,7 +65,8 @@ __device__ __forceinline__ void alpha_stage(const float *src, float *dst, const 
         const float lo0 = ld1<CHAN_SMEM>(src + lane, top), lo1 = ld1<CHAN_SMEM>(src + 32 + lane, top);
         const float hi0 = ld1<CHAN_SMEM>(src + 64 + lane, top), hi1 = ld1<CHAN_SMEM>(src + 96 + lane, top);
         if (odd) {
-            const uint32_t w0 = beta[boff >> 5], w1 = beta[(boff >> 5) + 1];
+            const uint32_t w0 = BR ? __shfl_sync(FULL, bw, boff >> 5) : beta[boff >> 5];
+            const uint32_t w1 = BR ? __shfl_sync(FULL, bw, (boff >> 5) + 1) : beta[(boff >> 5) + 1];
             dst[lane] = g_exact(lo0, hi0, (w0 >> lane) & 1u);
             dst[32 + lane] = g_exact(lo1, hi1, (w1 >> lane) & 1u);
         } else {
@@ -74,7 +79,7 @@ __device__ __forceinline__ void alpha_stage(const float *src, float *dst, const 
             const float4 hi = ld4<CHAN_SMEM>(src + Ls + i, top);
             float4 o;
             if (odd) {
-                const uint32_t b = beta[(boff + i) >> 5] >> ((boff + i) & 31);
+                const uint32_t b = (BR ? __shfl_sync(FULL, bw, (boff + i) >> 5) : beta[(boff + i) >> 5]) >> ((boff + i) & 31);
                 o.x = g_exact(lo.x, hi.x, b & 1); o.y = g_exact(lo.y, hi.y, (b >> 1) & 1);
                 o.z = g_exact(lo.z, hi.z, (b >> 2) & 1); o.w = g_exact(lo.w, hi.w, (b >> 3) & 1);
             } else {
@@ -83,7 +88,17 @@ __device__ __forceinline__ void alpha_stage(const float *src, float *dst, const 
             }
             *reinterpret_cast<float4 *>(dst + i) = o;
         };
-        if constexpr (UNR) {
+        // Ls >= 128: every lane runs Ls / 128 chunks.  With the register beta
+        // (shuffles inside) the loop is written uniform so the warp stays
+        // provably converged; the shared-memory form keeps the lane-strided loop
+        // (measured faster there)
+        if constexpr (BR && UNR) {
+            #pragma unroll 4
+            for (int k = 0; k < (Ls >> 7); k++) chunk(lane * 4 + (k << 7));
+        } else if constexpr (BR) {
+            #pragma unroll 1
+            for (int k = 0; k < (Ls >> 7); k++) chunk(lane * 4 + (k << 7));
+        } else if constexpr (UNR) {
             #pragma unroll 4
             for (int i = lane * 4; i < Ls; i += 128) chunk(i);
         } else {
@@ -273,6 +288,10 @@ fsscs_decode_kernel(const DecodeParams P) {
     // D <= 32: the register stack is kept sorted by (PM, serial), one entry per
     // lane (lane 0 = best): select reads the head, insertion is one merge
     constexpr bool SORTED = (SLOTS == 1) && (POLAR_SORTED_STACK != 0);
+    // code-length-specialised kernels with N <= 1024: the flat beta (N/32 <= 32
+    // words) lives in registers, word w in lane w (bw); beta[] in shared memory
+    // only stages the output
+    constexpr bool BREG = (NL == 10 || NL == 7) && (POLAR_BETA_REGS != 0);
     using PK = Pk<BIG>;
     extern __shared__ __align__(16) uint32_t smem[];
     const int lane = threadIdx.x & 31;
@@ -399,6 +418,7 @@ fsscs_decode_kernel(const DecodeParams P) {
         }
         __syncwarp();
         uint32_t work = 0, next_serial = 1, pops = 0, switches = 0;
+        uint32_t bw = 0;                  // BREG: word `lane` of the working path's flat beta
         uint32_t c_fg = 0, c_bb = 0, c_ne = 0, c_sw = 0;     // CNT: executed work of this frame
         int work_pl = 0;
         // alpha memory content: stages s >= lev_mem hold the node (s, pos_mem >> s)
@@ -572,8 +592,11 @@ fsscs_decode_kernel(const DecodeParams P) {
                             uint32_t *dst = snap_slot(slot);
                             const int nwords = (work_pl + 31) >> 5;
                             if constexpr (CNT) c_sw += (uint32_t)nwords;
-                            #pragma unroll 1
-                            for (int w_0 = 0; w_0 < (nwords); w_0 += 32) if (const int w = w_0 + lane; w < (nwords)) dst[w] = beta[w];
+                            if (BREG) { if (lane < nwords) dst[lane] = bw; }
+                            else {
+                                #pragma unroll 1
+                                for (int w_0 = 0; w_0 < (nwords); w_0 += 32) if (const int w = w_0 + lane; w < (nwords)) dst[w] = beta[w];
+                            }
                             if (lane == 0) sjsm[wi] = PK::make(PK::j(wj), (uint32_t)slot, 0);
                             __syncwarp();
                         }
@@ -595,8 +618,11 @@ fsscs_decode_kernel(const DecodeParams P) {
                         uint32_t *dst = snap_slot(slot);
                         const int nwords = (work_pl + 31) >> 5;
                         if constexpr (CNT) c_sw += (uint32_t)nwords;
-                        #pragma unroll 1
-                        for (int w_0 = 0; w_0 < (nwords); w_0 += 32) if (const int w = w_0 + lane; w < (nwords)) dst[w] = beta[w];
+                        if (BREG) { if (lane < nwords) dst[lane] = bw; }
+                        else {
+                            #pragma unroll 1
+                            for (int w_0 = 0; w_0 < (nwords); w_0 += 32) if (const int w = w_0 + lane; w < (nwords)) dst[w] = beta[w];
+                        }
                         if (lane == wl) {
 #pragma unroll
                             for (int s = 0; s < SL; s++)
@@ -611,8 +637,22 @@ fsscs_decode_kernel(const DecodeParams P) {
                 const int nwords = (pl + 31) >> 5;
                 if constexpr (CNT) c_sw += (uint32_t)nwords;
                 int d = 0x7FFFFFFF;
+                if (BREG) {
+                    uint32_t x = 0;
+                    if (lane < nwords) {
+                        const uint32_t nv = snap_sm ? src[lane] : __ldcg(src + lane);
+                        x = nv ^ bw;
+                        if (lane == nwords - 1 && (pl & 31)) x &= (1u << (pl & 31)) - 1u;
+                        bw = nv;
+                    }
+                    const uint32_t b = __ballot_sync(FULL, x != 0);
+                    if (b) {
+                        const int fl = __ffs(b) - 1;
+                        d = 32 * fl + __ffs(__shfl_sync(FULL, x, fl)) - 1;
+                    }
+                }
                 #pragma unroll 1
-                for (int w0 = 0; w0 < nwords; w0 += 32) {
+                for (int w0 = 0; !BREG && w0 < nwords; w0 += 32) {
                     const int w = w0 + lane;
                     uint32_t x = 0;
                     if (w < nwords) {
@@ -632,7 +672,22 @@ fsscs_decode_kernel(const DecodeParams P) {
                 __syncwarp();
                 if (rel != 0u) {
                     const int Lam = 1 << plam, seg = pl - Lam;      // node j-1
-                    if (pkind == OP_REP) {
+                    if (BREG) {
+                        uint32_t fm = 0;          // this lane's word of the flip pattern
+                        if (pkind == OP_REP) {
+                            if (Lam >= 32) fm = (lane >= (seg >> 5) && lane < (seg >> 5) + (Lam >> 5)) ? FULL : 0u;
+                            else if (lane == (seg >> 5)) fm = ((1u << Lam) - 1u) << (seg & 31);
+                        } else {
+                            const uint2 hh = *hdr_at((int)ps);
+                            const uint32_t m[4] = {hh.x & 0xFFFFu, hh.x >> 16, hh.y & 0xFFFFu, hh.y >> 16};
+#pragma unroll
+                            for (int q = 0; q < 4; q++) {
+                                const int pos = seg + (int)m[q];
+                                if (((rel >> q) & 1u) && lane == (pos >> 5)) fm ^= 1u << (pos & 31);
+                            }
+                        }
+                        bw ^= fm;
+                    } else if (pkind == OP_REP) {
                         if (Lam >= 32) {
                             #pragma unroll 1
                             for (int t_0 = 0; t_0 < ((Lam >> 5)); t_0 += 32) if (const int t = t_0 + lane; t < ((Lam >> 5))) beta[(seg >> 5) + t] ^= FULL;
@@ -663,13 +718,14 @@ fsscs_decode_kernel(const DecodeParams P) {
             // x ^= (x >> Lambda) & mask; the rest word by word.
             const int l = (int)rb.w;                 // level where the climb ends
             if (rc.x != 0xFFFFFFFFu) {
-                uint32_t x = beta[rc.x];
+                uint32_t x = BREG ? bw : beta[rc.x];
                 x ^= (x >> 1) & rc.y;
                 x ^= (x >> 2) & rc.z;
                 x ^= (x >> 4) & rc.w;
                 x ^= (x >> 8) & rd.x;
                 x ^= (x >> 16) & rd.y;
-                if (lane == 0) beta[rc.x] = x;
+                if (BREG) { if (lane == (int)rc.x) bw = x; }
+                else if (lane == 0) beta[rc.x] = x;
                 __syncwarp();
                 if constexpr (CNT) c_bb += (uint32_t)(__popc(rc.y) + __popc(rc.z) + __popc(rc.w) + __popc(rd.x) + __popc(rd.y));
             }
@@ -677,13 +733,18 @@ fsscs_decode_kernel(const DecodeParams P) {
                 int ph = (int)rb.y;
                 #pragma unroll 1
                 for (int lw = (int)rb.x; ph & 1; ph >>= 1, lw++) {
-                    beta_op(beta, lw, ph, lane);
+                    if (BREG) beta_op_reg(bw, lw, ph, lane);
+                    else beta_op(beta, lw, ph, lane);
                     if constexpr (CNT) c_bb += 1u << lw;
                 }
             }
 
             if (j == M) {
                 // ---- complete path: CRC on the systematic bits
+                if (BREG) {                      // the register beta lands in beta[] (CRC, copy, output)
+                    if (lane < nw) beta[lane] = bw;
+                    __syncwarp();
+                }
                 bool ok = true;
                 if (MODE < 2 && P.c > 0) {
                     // syndrome = XOR of the contributions of the set systematic bits,
@@ -757,14 +818,13 @@ fsscs_decode_kernel(const DecodeParams P) {
                 int s_min = max(max(lev_mem, bitlen((uint32_t)(pos_mem ^ pl))), max(s_d, l + 1));
                 s_min = min(s_min, n);
                 const int s_hi = s_min - 1;
-                #pragma unroll 1
                 if constexpr (NL > 0) {
                     // shared-memory stages with compile-time sizes: enter at s_hi
 #define POLAR_SSTAGE(T)                                                                       \
     if constexpr ((T) < NL && (T) >= 6) {                                                     \
         if ((T) < lam) break;                                                                 \
         if constexpr (CNT) c_fg += 1u << (T);                                                 \
-        alpha_stage<CHAN_SMEM, (NL == 10 && SLOTS == 1)>((T) + 1 == n ? chan : SP((T) + 1), SP(T), beta, n, (T), pl >> (T), lane); \
+        alpha_stage<CHAN_SMEM, (NL == 10 && SLOTS == 1), BREG>((T) + 1 == n ? chan : SP((T) + 1), SP(T), beta, bw, n, (T), pl >> (T), lane); \
     }
                     switch (s_hi) {
                     case 12: POLAR_SSTAGE(12)
@@ -781,7 +841,7 @@ fsscs_decode_kernel(const DecodeParams P) {
                     #pragma unroll 1
                     for (int s = s_hi; s >= max(lam, 6); s--) {
                         if constexpr (CNT) c_fg += 1u << s;
-                        alpha_stage<CHAN_SMEM>(s + 1 == n ? chan : SP(s + 1), SP(s), beta, n, s, pl >> s, lane);
+                        alpha_stage<CHAN_SMEM>(s + 1 == n ? chan : SP(s + 1), SP(s), beta, 0u, n, s, pl >> s, lane);
                     }
                 }
                 // register stages (Lambda <= 32): lo = element i, hi = element i + Lambda
@@ -804,7 +864,8 @@ fsscs_decode_kernel(const DecodeParams P) {
         const int psi = pl >> (T);                                                         \
         if (psi & 1) {                                                                     \
             const int boff = (psi - 1) << (T);                                             \
-            const uint32_t bit = (beta[boff >> 5] >> (((boff & 31) + lane) & 31)) & 1u;     \
+            const uint32_t bwd = BREG ? __shfl_sync(FULL, bw, boff >> 5) : beta[boff >> 5];  \
+            const uint32_t bit = (bwd >> (((boff & 31) + lane) & 31)) & 1u;                \
             r[T] = g_exact(lo, hi, bit);                                                   \
         } else {                                                                           \
             r[T] = f_minsum(lo, hi);                                                       \
@@ -918,7 +979,8 @@ fsscs_decode_kernel(const DecodeParams P) {
                     for (int t = 0; t < R; t++) {
                         const float x = a[32 * t + lane];
                         const uint32_t b = __ballot_sync(FULL, x < 0.f);
-                        if (lane == (t & 31)) beta[(seg >> 5) + t] = b;
+                        if (BREG) { if (lane == (seg >> 5) + t) bw = b; }
+                        else if (lane == (t & 31)) beta[(seg >> 5) + t] = b;
                         par ^= (uint32_t)__popc(b);
                         top4_insert(((unsigned long long)__float_as_uint(fabsf(x)) << 32) | (uint32_t)(32 * t + lane),
                                     t0, t1, t2, t3);
@@ -979,7 +1041,32 @@ fsscs_decode_kernel(const DecodeParams P) {
 
             // ---- c1 continues in the working memory ------------------------
             const int m0 = (int)(clist & 15u);
-            {
+            if (BREG) {
+                // c1's segment into this lane's word: new bits nb under mask lm
+                const int ws = seg >> 5, o = seg & 31;
+                uint32_t nb = 0, lm = 0;
+                if (sum_kind) {
+                    const uint32_t fill = (kind == OP_REP && m0) ? FULL : 0u;
+                    if (Lam >= 32) { lm = (lane >= ws && lane < ws + (Lam >> 5)) ? FULL : 0u; nb = fill; }
+                    else { lm = (lane == ws) ? ((1u << Lam) - 1u) << o : 0u; nb = fill; }
+                } else if (Lam <= 32) {
+                    uint32_t wv = hdw_node;                // HD word with c1's flips
+#pragma unroll
+                    for (int q = 0; q < 4; q++)
+                        if ((m0 >> q) & 1) wv ^= 1u << mi[q];
+                    const uint32_t wm = (Lam == 32) ? FULL : (1u << Lam) - 1u;
+                    lm = (lane == ws) ? wm << o : 0u;
+                    nb = (wv & wm) << o;
+                } else {
+                    // the HD words are in place: flip c1's positions
+#pragma unroll
+                    for (int q = 0; q < 4; q++) {
+                        const int pos = seg + (int)mi[q];
+                        if (((m0 >> q) & 1) && lane == (pos >> 5)) bw ^= 1u << (pos & 31);
+                    }
+                }
+                bw = (bw & ~lm) | (nb & lm);
+            } else {
                 if (sum_kind) {
                     const uint32_t fill = (kind == OP_REP && m0) ? FULL : 0u;
                     if (Lam >= 32) {
@@ -1025,8 +1112,11 @@ fsscs_decode_kernel(const DecodeParams P) {
                 uint32_t *dst = snap_slot(fslot);
                 const int nwords = (npl + 31) >> 5;
                 if constexpr (CNT) c_sw += (uint32_t)nwords;
-                #pragma unroll 1
-                for (int w_0 = 0; w_0 < (nwords); w_0 += 32) if (const int w = w_0 + lane; w < (nwords)) dst[w] = beta[w];
+                if (BREG) { if (lane < nwords) dst[lane] = bw; }
+                else {
+                    #pragma unroll 1
+                    for (int w_0 = 0; w_0 < (nwords); w_0 += 32) if (const int w = w_0 + lane; w < (nwords)) dst[w] = beta[w];
+                }
                 if (lane == 0) *hdr_at(fslot) = make_uint2(mi[0] | (mi[1] << 16), mi[2] | (mi[3] << 16));
             };
             if (!SORTED && nfit > 1) write_fork_snapshot(-1, -1);
@@ -1087,8 +1177,8 @@ fsscs_decode_kernel(const DecodeParams P) {
                 nS += nfit;
             } else {
                 int base = 0;
-                bool c1_found = false;
                 const uint32_t jbase = jsm_make(jn, (nfit == 1) ? SNAP_NONE : (uint32_t)fslot, 0);
+                uint32_t fbs[SL];
 #pragma unroll
                 for (int s = 0; s < SL; s++) {
                     const bool fr = (s_ser[s] == EMPTY);
@@ -1101,9 +1191,16 @@ fsscs_decode_kernel(const DecodeParams P) {
                         s_ser[s] = ser0 + (uint32_t)k;
                         s_jsm[s] = jbase | ((mk ^ (uint32_t)m0) << 21);
                     }
-                    const uint32_t b0 = __ballot_sync(FULL, fr && k == 0);
-                    if (!c1_found && b0) { c1_found = true; c1_lane = __ffs(b0) - 1; c1_slot = s; }
+                    fbs[s] = fb;
                     base += __popc(fb);
+                }
+                // c1 took the first free entry in (slot, lane) order; found with
+                // selects only (a flag set inside the unrolled loop made ptxas
+                // treat the SLOTS = 4 decode loop as divergent)
+#pragma unroll
+                for (int s = SL - 1; s >= 0; s--) {
+                    c1_lane = fbs[s] ? __ffs(fbs[s]) - 1 : c1_lane;
+                    c1_slot = fbs[s] ? s : c1_slot;
                 }
                 nS += nfit;
             }
@@ -1157,15 +1254,22 @@ fsscs_decode_kernel(const DecodeParams P) {
             if (BIG) {
                 if (fslot >= 0 && lane == 0) sjsm[c1_slot] = PK::make(jn, (uint32_t)fslot, 0);
                 __syncwarp();
-            } else if (!SORTED && fslot >= 0 && lane == c1_lane) {
+            } else if (!SORTED && fslot >= 0) {
+                // selects, not a lane branch around the writes (that branch made
+                // ptxas treat the SLOTS = 4 decode loop as divergent)
+                const uint32_t c1j = jsm_make(jn, (uint32_t)fslot, 0);
 #pragma unroll
-                for (int s = 0; s < SL; s++) if (s == c1_slot) s_jsm[s] = jsm_make(jn, (uint32_t)fslot, 0);
+                for (int s = 0; s < SL; s++) s_jsm[s] = (lane == c1_lane && s == c1_slot) ? c1j : s_jsm[s];
             }
         }
 
         // ---- output: x_hat (systematic) or u_hat = x_hat F
         // (non-systematic) restricted to A, ascending ---------
         {
+            if (BREG && !from_best) {         // (a complete path staged it already; the watchdog exit did not)
+                if (lane < nw) beta[lane] = bw;
+                __syncwarp();
+            }
             const uint32_t *bsrc = from_best ? best : beta;
             if (MODE == 0 && P.nonsys) {
                 #pragma unroll 1

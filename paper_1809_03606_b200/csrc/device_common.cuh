@@ -56,6 +56,22 @@ __device__ __forceinline__ void beta_op(uint32_t *beta, int lam, int phi, int la
     __syncwarp();
 }
 
+// The same BETA op on a flat beta held in registers, word w in lane w
+// (N <= 1024): whole words move by one shuffle, a sub-word level is one RMW in
+// the owning lane
+__device__ __forceinline__ void beta_op_reg(uint32_t &bw, int lam, int phi, int lane) {
+    const int Lam = 1 << lam;
+    if (Lam >= 32) {
+        const int wd = ((phi - 1) * Lam) >> 5, nwd = Lam >> 5;
+        const uint32_t x = __shfl_down_sync(FULL, bw, nwd);
+        if (lane >= wd && lane < wd + nwd) bw ^= x;
+    } else {
+        const int p = (phi - 1) * Lam;             // 2*Lam bits inside one word
+        const uint32_t r = (bw >> ((p & 31) + Lam)) & ((1u << Lam) - 1u);
+        if (lane == (p >> 5)) bw ^= r << (p & 31);
+    }
+}
+
 // u <- x F^{(x)n} on nw bit-packed words: the re-encoding of
 // the root beta that gives u_hat in non-systematic mode
 __device__ __forceinline__ void xform_words(uint32_t *w, int N, int nw, int lane) {
