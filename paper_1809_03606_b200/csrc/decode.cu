@@ -29,8 +29,14 @@ namespace polar {
 #ifndef POLAR_BETA_REGS
 #define POLAR_BETA_REGS 1      // 0: the flat beta in shared memory in every kernel (A/B builds)
 #endif
+#ifndef POLAR_UNR_BIG
+#define POLAR_UNR_BIG 0        // 1: the N = 2048 / 4096 kernels unroll the float4 stage loop too (A/B builds)
+#endif
+#ifndef POLAR_BWPL
+#define POLAR_BWPL 1           // register stages below 5 read the left sibling's beta from one shuffled word
+#endif
 #ifndef POLAR_SORTED_STACK
-#define POLAR_SORTED_STACK 1   // 0: the unsorted register stack for D <= 32 too (A/B builds)
+#define POLAR_SORTED_STACK 2   // 2: every register stack sorted; 1: D <= 32 only; 0: none (A/B builds)
 #endif
 
 constexpr uint32_t EMPTY = 0xFFFFFFFFu;
@@ -285,9 +291,10 @@ __global__ void __launch_bounds__(kDecodeWarps * 32, kDecodeMinBlocksFor<SLOTS, 
 fsscs_decode_kernel(const DecodeParams P) {
     constexpr bool BIG = (SLOTS == 0);
     constexpr int SL = BIG ? 1 : SLOTS;       // register arrays (unused when BIG)
-    // D <= 32: the register stack is kept sorted by (PM, serial), one entry per
-    // lane (lane 0 = best): select reads the head, insertion is one merge
-    constexpr bool SORTED = (SLOTS == 1) && (POLAR_SORTED_STACK != 0);
+    // register stacks (D <= 128) are kept sorted by (PM, serial): position
+    // p = 32 s + lane in slot s (position 0 = best): select reads the head,
+    // insertion is one merge
+    constexpr bool SORTED = !BIG && ((SLOTS == 1 && POLAR_SORTED_STACK >= 1) || POLAR_SORTED_STACK >= 2);
     // code-length-specialised kernels with N <= 1024: the flat beta (N/32 <= 32
     // words) lives in registers, word w in lane w (bw); beta[] in shared memory
     // only stages the output
@@ -544,6 +551,48 @@ fsscs_decode_kernel(const DecodeParams P) {
                     nA = cntv;
                     hole = -1;
                     __syncwarp();
+                } else if (SORTED && SL > 1) {
+                    // survivors (depth > j) move to positions 1..cntv in order;
+                    // position P takes survivor number P: word v holding it by the
+                    // running counts, its bit by binary search on prefix counts
+                    uint32_t kb[SL];
+                    int cum[SL + 1];
+                    cum[0] = 0;
+#pragma unroll
+                    for (int q = 0; q < SL; q++) {
+                        kb[q] = __ballot_sync(FULL, s_ser[q] != EMPTY && (int)jsm_j(s_jsm[q]) > j);
+                        cum[q + 1] = cum[q] + __popc(kb[q]);
+                    }
+                    cntv = cum[SL];
+                    uint32_t npm[SL], nser[SL], njsm[SL];
+#pragma unroll
+                    for (int w = 0; w < SL; w++) {
+                        const int k = 32 * w + lane - 1;             // survivor index (0-based)
+                        const bool dst = (k >= 0 && k < cntv);
+                        int v = 0, kk = k;
+                        uint32_t wbits = kb[0];
+#pragma unroll
+                        for (int q = 1; q < SL; q++)
+                            if (k >= cum[q]) { v = q; kk = k - cum[q]; wbits = kb[q]; }
+                        int src = 0;
+#pragma unroll
+                        for (int st = 16; st >= 1; st >>= 1) {
+                            const int hi = src + st - 1;
+                            if (__popc(wbits & (hi >= 31 ? FULL : ((2u << hi) - 1u))) <= kk) src += st;
+                        }
+                        uint32_t gp = EMPTY, gs = EMPTY, gj = 0;
+#pragma unroll
+                        for (int q = 0; q < SL; q++) {
+                            const uint32_t xp = __shfl_sync(FULL, s_pm[q], src), xs = __shfl_sync(FULL, s_ser[q], src);
+                            const uint32_t xj = __shfl_sync(FULL, s_jsm[q], src);
+                            gp = (v == q) ? xp : gp; gs = (v == q) ? xs : gs; gj = (v == q) ? xj : gj;
+                        }
+                        npm[w] = dst ? gp : EMPTY;
+                        nser[w] = dst ? gs : EMPTY;
+                        njsm[w] = gj;
+                    }
+#pragma unroll
+                    for (int w = 0; w < SL; w++) { s_pm[w] = npm[w]; s_ser[w] = nser[w]; s_jsm[w] = njsm[w]; }
                 } else if (SORTED) {
                     // survivors (depth > j) move to lanes 1..cntv in order (a subset
                     // of a sorted list is sorted); lane 0 stays free
@@ -791,12 +840,22 @@ fsscs_decode_kernel(const DecodeParams P) {
                     hole = -1;
                 }
                 if (SORTED) {
-                    // nothing is inserted: the entries in lanes 1..nS move to 0..nS-1
-                    // (before the exit test too, for the same reason as the copy)
-                    s_pm[0] = __shfl_down_sync(FULL, s_pm[0], 1);
-                    s_ser[0] = __shfl_down_sync(FULL, s_ser[0], 1);
-                    s_jsm[0] = __shfl_down_sync(FULL, s_jsm[0], 1);
-                    if (lane == 31) { s_pm[0] = EMPTY; s_ser[0] = EMPTY; }
+                    // nothing is inserted: the entries at positions 1..nS move to
+                    // 0..nS-1 (before the exit test too, for the same reason as the copy)
+#pragma unroll
+                    for (int q = 0; q < SL; q++) {
+                        const uint32_t dp = __shfl_down_sync(FULL, s_pm[q], 1), ds = __shfl_down_sync(FULL, s_ser[q], 1);
+                        const uint32_t dj = __shfl_down_sync(FULL, s_jsm[q], 1);
+                        uint32_t up = EMPTY, us = EMPTY, uj = 0;
+                        if (q + 1 < SL) {
+                            up = __shfl_sync(FULL, s_pm[q + 1 < SL ? q + 1 : q], 0);
+                            us = __shfl_sync(FULL, s_ser[q + 1 < SL ? q + 1 : q], 0);
+                            uj = __shfl_sync(FULL, s_jsm[q + 1 < SL ? q + 1 : q], 0);
+                        }
+                        s_pm[q] = (lane == 31) ? up : dp;
+                        s_ser[q] = (lane == 31) ? us : ds;
+                        s_jsm[q] = (lane == 31) ? uj : dj;
+                    }
                 }
                 if (ok) { out_pm = p_pm; status = 0; break; }
                 // the climb above combined blocks that the alpha memory was
@@ -824,7 +883,7 @@ fsscs_decode_kernel(const DecodeParams P) {
     if constexpr ((T) < NL && (T) >= 6) {                                                     \
         if ((T) < lam) break;                                                                 \
         if constexpr (CNT) c_fg += 1u << (T);                                                 \
-        alpha_stage<CHAN_SMEM, (NL == 10 && SLOTS == 1), BREG>((T) + 1 == n ? chan : SP((T) + 1), SP(T), beta, bw, n, (T), pl >> (T), lane); \
+        alpha_stage<CHAN_SMEM, ((NL == 10 && SLOTS == 1) || (NL >= 11 && POLAR_UNR_BIG)), BREG>((T) + 1 == n ? chan : SP((T) + 1), SP(T), beta, bw, n, (T), pl >> (T), lane); \
     }
                     switch (s_hi) {
                     case 12: POLAR_SSTAGE(12)
@@ -864,7 +923,9 @@ fsscs_decode_kernel(const DecodeParams P) {
         const int psi = pl >> (T);                                                         \
         if (psi & 1) {                                                                     \
             const int boff = (psi - 1) << (T);                                             \
-            const uint32_t bwd = BREG ? __shfl_sync(FULL, bw, boff >> 5) : beta[boff >> 5];  \
+            uint32_t bwd;                                                                  \
+            if (BREG) bwd = ((T) == 5 || !POLAR_BWPL) ? __shfl_sync(FULL, bw, boff >> 5) : bw_pl; \
+            else bwd = beta[boff >> 5];                                                    \
             const uint32_t bit = (bwd >> (((boff & 31) + lane) & 31)) & 1u;                \
             r[T] = g_exact(lo, hi, bit);                                                   \
         } else {                                                                           \
@@ -875,6 +936,9 @@ fsscs_decode_kernel(const DecodeParams P) {
         if (lam == (T)) break;                                                             \
     }
                 if (lam <= 5) {
+                    // register beta: the left siblings of the stages below 5 lie in
+                    // node j's own word (psi odd puts bit T of pl, T <= 4, inside it)
+                    const uint32_t bw_pl = (BREG && POLAR_BWPL) ? __shfl_sync(FULL, bw, pl >> 5) : 0u;
                     switch (min(s_hi, 5)) {
                     case 5: POLAR_RSTAGE(5)
                     case 4: POLAR_RSTAGE(4)
@@ -1121,21 +1185,85 @@ fsscs_decode_kernel(const DecodeParams P) {
             };
             if (!SORTED && nfit > 1) write_fork_snapshot(-1, -1);
             int c1_lane = 0, c1_slot = 0;
-            if (SORTED) {
+            if (SORTED && SL > 1) {
+                // the same merge over SL slots (position p = 32 s + lane): entry p
+                // moves to p - 1 + a_p, which stays in slots s - 1 .. s + 1
+                const uint32_t cpm = (lane < nc) ? __float_as_uint(p_pm + my_d) : EMPTY;
+                const uint32_t c3 = __shfl_sync(FULL, cpm, 3);
+                uint32_t Mw[SL];
+#pragma unroll
+                for (int w = 0; w < SL; w++) Mw[w] = 0u;
+#pragma unroll
+                for (int q = 0; q < SL; q++) {
+                    const uint32_t epm = s_pm[q];
+                    int a = (c3 < epm) ? 4 : 0;
+                    if (__shfl_sync(FULL, cpm, a + 1) < epm) a += 2;
+                    if (__shfl_sync(FULL, cpm, a) < epm) a += 1;
+                    if (__shfl_sync(FULL, cpm, a) < epm) a += 1;
+                    const int pos = 32 * q + lane;
+                    const int epos = pos - 1 + a;
+                    const bool ekeep = pos >= 1 && pos <= nS && epos < D;
+#pragma unroll
+                    for (int w = (q > 0 ? q - 1 : 0); w <= q + 1 && w < SL; w++)
+                        Mw[w] |= (ekeep && (epos >> 5) == w) ? (1u << (epos & 31)) : 0u;
+                }
+                int nE = 0;
+#pragma unroll
+                for (int w = 0; w < SL; w++) { Mw[w] = __reduce_or_sync(FULL, Mw[w]); nE += __popc(Mw[w]); }
+                const int total = min(D, nS + nc);
+                if (total - nE > 1) write_fork_snapshot(-1, -1);
+                const uint32_t jb = jsm_make(jn, fslot >= 0 ? (uint32_t)fslot : SNAP_NONE, 0);
+                // gather, ascending output slots; slot w - 1's old entries are kept
+                uint32_t opm = EMPTY, oser = EMPTY, ojsm = 0;
+                int qbase = 0;
+#pragma unroll
+                for (int w = 0; w < SL; w++) {
+                    const int P = 32 * w + lane;
+                    const int q = qbase + __popc(Mw[w] & ((1u << lane) - 1u));   // entries before position P
+                    const bool isE = (Mw[w] >> lane) & 1u;
+                    const int t = (P - q) & 7;                                   // candidate at position P
+                    const int src = q + 1, sv = src >> 5, sl = src & 31;
+                    uint32_t gpm = __shfl_sync(FULL, s_pm[w], sl), gser = __shfl_sync(FULL, s_ser[w], sl);
+                    uint32_t gjsm = __shfl_sync(FULL, s_jsm[w], sl);
+                    if (w > 0) {
+                        const uint32_t xp = __shfl_sync(FULL, opm, sl), xs = __shfl_sync(FULL, oser, sl);
+                        const uint32_t xj = __shfl_sync(FULL, ojsm, sl);
+                        gpm = (sv == w - 1) ? xp : gpm; gser = (sv == w - 1) ? xs : gser; gjsm = (sv == w - 1) ? xj : gjsm;
+                    }
+                    if (w + 1 < SL) {
+                        const int w1 = (w + 1 < SL) ? w + 1 : w;
+                        const uint32_t xp = __shfl_sync(FULL, s_pm[w1], 0), xs = __shfl_sync(FULL, s_ser[w1], 0);
+                        const uint32_t xj = __shfl_sync(FULL, s_jsm[w1], 0);
+                        gpm = (sv == w + 1) ? xp : gpm; gser = (sv == w + 1) ? xs : gser; gjsm = (sv == w + 1) ? xj : gjsm;
+                    }
+                    qbase += __popc(Mw[w]);
+                    const uint32_t ct = __shfl_sync(FULL, cpm, t);
+                    const bool live = P < total;
+                    const uint32_t mk = (clist >> (4 * t)) & 15u;
+                    opm = s_pm[w]; oser = s_ser[w]; ojsm = s_jsm[w];
+                    s_pm[w] = !live ? EMPTY : (isE ? gpm : ct);
+                    s_ser[w] = !live ? EMPTY : (isE ? gser : ser0 + (uint32_t)t);
+                    const bool isC = live && !isE;
+                    s_jsm[w] = isC ? (jb | ((mk ^ (uint32_t)m0) << 21)) : gjsm;
+                }
+                nS = total;
+            } else if (SORTED) {
                 // merge the candidates into the sorted stack, keeping the D smallest
                 // keys.  Equivalent to c1 always + siblings while |S| < D + strict-PM
                 // replacement of the worst (reading R8): candidate
                 // serials exceed every live serial, so "PM < worst PM" is "key <
                 // worst key", and the sequential rule keeps the D smallest keys.
                 // Entries: lanes 1..nS (sorted); candidate t: lane t, key ascending in t.
-                const uint32_t cpm = __float_as_uint(p_pm + my_d);
+                // candidate keys; lanes nc..7 hold EMPTY (above every live key)
+                const uint32_t cpm = (lane < nc) ? __float_as_uint(p_pm + my_d) : EMPTY;
                 const uint32_t epm = s_pm[0];
-                // a = #{t < nc : cpm_t < epm} (candidate keys ascend: binary search)
+                // a = #{t < nc : cpm_t < epm} (candidate keys ascend: binary search
+                // over 8 slots, no branch on nc)
                 int a = 0;
-                if (nc > 4) { if (__shfl_sync(FULL, cpm, a + 3) < epm) a += 4; }
-                if (nc > 2) { if (__shfl_sync(FULL, cpm, a + 1) < epm) a += 2; }
-                if (nc > 1) { if (__shfl_sync(FULL, cpm, a) < epm) a += 1; }
-                if (__shfl_sync(FULL, cpm, a) < epm) a += 1;          // a <= nc - 1 before this step
+                if (__shfl_sync(FULL, cpm, 3) < epm) a = 4;
+                if (__shfl_sync(FULL, cpm, a + 1) < epm) a += 2;
+                if (__shfl_sync(FULL, cpm, a) < epm) a += 1;
+                if (__shfl_sync(FULL, cpm, a) < epm) a += 1;          // a <= 7 before this step
                 const int epos = lane - 1 + a;                      // merged position of entry lane
                 const bool ekeep = lane >= 1 && lane <= nS && epos < D;
                 const uint32_t Mp = __reduce_or_sync(FULL, ekeep ? (1u << epos) : 0u);
@@ -1150,10 +1278,10 @@ fsscs_decode_kernel(const DecodeParams P) {
                 const int t = (lane - q) & 7;                       // candidate at position lane
                 const uint32_t gpm = __shfl_sync(FULL, epm, q + 1), gser = __shfl_sync(FULL, s_ser[0], q + 1);
                 const uint32_t gjsm = __shfl_sync(FULL, s_jsm[0], q + 1);
-                const float dt = __shfl_sync(FULL, my_d, t);
+                const uint32_t ct = __shfl_sync(FULL, cpm, t);      // candidate t's PM bits
                 const bool live = lane < total;
                 const uint32_t mk = (clist >> (4 * t)) & 15u;
-                s_pm[0] = !live ? EMPTY : (isE ? gpm : __float_as_uint(p_pm + dt));
+                s_pm[0] = !live ? EMPTY : (isE ? gpm : ct);
                 s_ser[0] = !live ? EMPTY : (isE ? gser : ser0 + (uint32_t)t);
                 const bool isC = live && !isE;
                 s_jsm[0] = isC ? (jb | ((mk ^ (uint32_t)m0) << 21)) : gjsm;

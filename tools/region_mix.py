@@ -5,10 +5,10 @@ import csv
 import subprocess
 import sys
 
-REGIONS = [(0, 260, "helpers"), (260, 403, "frame-setup"), (403, 476, "select"), (476, 513, "count/prune"),
-           (513, 519, "records"), (519, 618, "switch"), (618, 643, "beta-climb"), (643, 702, "complete/crc"),
-           (702, 738, "alpha-smem"), (738, 792, "alpha-reg"), (792, 918, "node"), (918, 930, "cand-dpm"),
-           (930, 963, "c1-write"), (963, 1026, "insert"), (1026, 1079, "replace"), (1079, 1200, "output")]
+REGIONS = [(0, 283, "helpers"), (283, 437, "frame-setup"), (437, 519, "select"), (519, 575, "count/prune"),
+           (575, 581, "records"), (581, 714, "switch"), (714, 742, "beta-climb"), (742, 813, "complete/crc"),
+           (813, 847, "alpha-smem"), (847, 903, "alpha-reg"), (903, 1029, "node"), (1029, 1042, "cand-dpm"),
+           (1042, 1099, "c1-write"), (1099, 1210, "insert"), (1210, 1265, "replace"), (1265, 1400, "output")]
 
 rep, units = sys.argv[1], float(sys.argv[2])
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "cuda,sass"],
@@ -40,7 +40,7 @@ for a in sorted(ins):
     v, fl, ln = ins[a]
     if fl == "decode.cu":
         last = ln
-    name = next(nm for lo, hi, nm in REGIONS if lo <= last < hi) if last < 1200 else "other"
+    name = next(nm for lo, hi, nm in REGIONS if lo <= last < hi) if last < 1400 else "other"
     tot[name] = tot.get(name, 0) + v
 s = sum(tot.values())
 print(f"total {s:.1f}")
