@@ -453,8 +453,15 @@ def run_ours(args, cfg, c):
         ex_ops = executed["fg"] + executed["beta_bits"] + executed["node_elems"]
         fr["alu_executed"] = ex_ops * frames / kern_s / 1e12 / alu_peak
         fr["smem_executed"] = (12 * executed["fg"] + 4 * executed["node_elems"]) * frames / kern_s / 1e9 / smem_peak
+    if ncu_ev and ncu_ev.get("warp_inst_per_frame"):
+        # instruction issue (the saturated resource per ncu): warp-instructions per
+        # frame (committed capture) x this run's frame rate over 148 SM x 4
+        # schedulers x 1 warp-instruction per clock
+        issue_peak = 148 * 4 * sm_max * 1e6
+        fr["issue"] = ncu_ev["warp_inst_per_frame"] * frames / kern_s / issue_peak
     roofline["fractions"] = fr
     roofline["peaks"] = {"hbm_GBps": hbm_peak, "alu_Tops": alu_peak, "smem_GBps": smem_peak,
+                         "issue_Ginst_per_s": 148 * 4 * sm_max / 1e3,
                          "source": "hbm: MEASURED_PEAKS.json hbm_gbs" + ("" if "hbm_gbs" in peaks else " (fallback)") +
                                    "; alu/smem: 148 SM x 128 lanes (x 4 B) x sm_max_mhz"}
     roofline["kernel_ms"] = kern_s * 1e3

@@ -20,7 +20,7 @@ cudaError_t decode_occupancy(int n, int slots, bool snap_smem, bool chan_smem, i
                              int *blocks_per_sm);
 cudaError_t launch_decode_counts(const DecodeParams &p, int slots, int ctas, int smem, cudaStream_t st);
 cudaError_t launch_list_packed(const ListParams &p, int ctas, int smem, cudaStream_t st);
-cudaError_t list_packed_occupancy(int n, int pwarps, int smem, int *blocks_per_sm);
+cudaError_t list_packed_occupancy(int n, int pwarps, int smem, int *blocks_per_sm, bool gbeta);
 cudaError_t launch_crc_attach(const CodecParams &p, cudaStream_t st);
 cudaError_t launch_encode(const CodecParams &p, cudaStream_t st);
 cudaError_t launch_modulate(const CodecParams &p, cudaStream_t st);
@@ -46,7 +46,7 @@ int round4(int w) { return (w + 3) & ~3; }
 void free_handle(polar_scs_t h) {
     if (!h) return;
     cudaFree(h->t.nodes); cudaFree(h->t.recs); cudaFree(h->t.info); cudaFree(h->t.crc_tab); cudaFree(h->t.crc_bytes); cudaFree(h->t.info_words);
-    cudaFree(h->d_queue); cudaFree(h->d_snap); cudaFree(h->d_keys); cudaFree(h->d_jsm); cudaFree(h->d_hdr); cudaFree(h->d_galpha); cudaFree(h->d_salpha);
+    cudaFree(h->d_queue); cudaFree(h->d_snap); cudaFree(h->d_keys); cudaFree(h->d_jsm); cudaFree(h->d_hdr); cudaFree(h->d_galpha); cudaFree(h->d_gbeta); cudaFree(h->d_salpha);
     for (int b = 0; b < polar_scs_s::kStageBufs; b++) {
         cudaFree(h->d_stage_llr[b]); cudaFree(h->d_stage_bits[b]);
         if (h->ev_h2d[b]) cudaEventDestroy(h->ev_h2d[b]);
@@ -134,6 +134,7 @@ int list_impl(polar_scs_t h, const float *llr, int64_t n, uint8_t *bits, float *
     p.llr = llr; p.n_frames = n; p.out_bits = bits; p.pm = pm; p.status = status;
     p.queue = h->d_queue + slot;
     if (p.galpha) p.galpha += (size_t)h->list_ctas * p.pwarps * p.gstride * (size_t)slot;
+    if (p.gbeta) p.gbeta += (size_t)h->list_ctas * p.pwarps * (size_t)(2 * p.L * p.nw) * (size_t)slot;
     cudaError_t e = cudaMemsetAsync(p.queue, 0, sizeof(unsigned long long), st);
     if (e != cudaSuccess) return cuda_status(e);
     const int ctas = (int)std::min<int64_t>(h->list_ctas, (n + p.pwarps - 1) / p.pwarps);
@@ -150,7 +151,7 @@ int list_packed_layout(ListParams &p) {
     if (p.M == 1) p.sg = p.n;                 // the root node uses the alpha area as scratch
     p.o_alpha = o; o += round4(std::max(L * ((1 << p.sg) - 1) + 6, p.M == 1 ? N : 0));   // + stage padding
     p.gstride = (size_t)L * (size_t)(N - (1 << p.sg));
-    p.o_beta = o;  o += round4(2 * L * p.nw);
+    p.o_beta = o;  if (!p.beta_global) o += round4(2 * L * p.nw);
     p.o_clist = o; o += round4(L);
     p.o_mi = o;    o += round4(2 * L);
     p.o_prow = o;  o += round4(4 * L);
@@ -224,7 +225,7 @@ int polar_scs_create_ex(polar_scs_t *out, int32_t N, int32_t K, const uint8_t *f
     const int slots = slots_for(D);
     // per-depth records in shared memory when they fit (not for the global
     // stack, whose occupancy is shared-memory bound: it reads them through L1)
-    const int sched_words = (slots != 0 && (t.M + 1) * 64 <= 16384) ? 16 * (t.M + 1) : 0;
+    const int sched_words = (POLAR_RECS_SMEM && slots != 0 && (t.M + 1) * 64 <= 16384) ? 16 * (t.M + 1) : 0;
 
     DecodeParams &p = h->base;
     p.nodes = t.nodes; p.recs = reinterpret_cast<const uint4 *>(t.recs); p.info = t.info; p.crc_tab = t.crc_tab; p.crc_bytes = t.crc_bytes; p.queue = h->d_queue;
@@ -233,7 +234,7 @@ int polar_scs_create_ex(polar_scs_t *out, int32_t N, int32_t K, const uint8_t *f
     p.nonsys = (flags & POLAR_FLAG_NONSYSTEMATIC) ? 1 : 0;
     p.hdr_words = slots ? 2 * D : 0;
     p.used_words = slots ? 4 : round4((D + 31) / 32);
-    p.win_words = slots ? 0 : 256;
+    p.win_words = (slots || POLAR_BIG_HOT) ? 0 : 256;
     p.uhat_words = p.nonsys ? nw : 0;
 
     // Layout choice: per warp, alpha stages >= 6 (N floats incl. scratch), flat
@@ -306,7 +307,7 @@ int polar_scs_create_ex(polar_scs_t *out, int32_t N, int32_t K, const uint8_t *f
     }
     if (slots == 0) {
         const size_t warps = (size_t)h->ctas * kDecodeWarps;
-        h->stack_count = warps * (size_t)D;
+        h->stack_count = warps * (size_t)(D + kColdPad);
         h->hdr_count = warps * (size_t)D;
         e = cudaMalloc(&h->d_keys, 2 * h->stack_count * sizeof(unsigned long long));
         if (e == cudaSuccess) e = cudaMalloc(&h->d_jsm, 2 * h->stack_count * sizeof(uint32_t));
@@ -330,18 +331,28 @@ int polar_scs_create_ex(polar_scs_t *out, int32_t N, int32_t K, const uint8_t *f
         // the top alpha stages move to a global (L2-resident) arena while that
         // raises the resident warps (frames) per SM: take the fewest global
         // stages that reach the best occupancy
+        // the path betas (2 L N/32 words per frame) may move to a global arena
+        // too; that placement is taken only when it at least doubles the
+        // resident warps (measured: C5, L = 32: 6 -> 32 warps/SM, 624 -> 1307
+        // Mbps; C4, L = 16: 20 -> 32 warps/SM, 2271 -> 2250)
+        int occ_b[2] = {0, 0}, pw_b[2] = {0, 0}, smem_b[2] = {0, 0};
+        ListParams lp_b[2] = {base, base};
+        for (int bg = 0; bg <= 1; bg++)
         for (int gst = 0; gst <= t.n; gst++) {
             for (int pw = kListPackedWarps; pw >= 1; pw >>= 1) {
                 ListParams tp = base;
                 tp.pwarps = pw;
                 tp.sg = t.n - gst;
+                tp.beta_global = bg;
                 const int sm = 4 * list_packed_layout(tp);
                 int oc = 0;
-                if (sm > optin || list_packed_occupancy(t.n, pw, sm, &oc) != cudaSuccess) oc = 0;
+                if (sm > optin || list_packed_occupancy(t.n, pw, sm, &oc, bg != 0) != cudaSuccess) oc = 0;
                 cudaGetLastError();
-                if (oc * pw > occ_p * pw_best) { occ_p = oc; pw_best = pw; smem_p = sm; lpk = tp; }
+                if (oc * pw > occ_b[bg] * pw_b[bg]) { occ_b[bg] = oc; pw_b[bg] = pw; smem_b[bg] = sm; lp_b[bg] = tp; }
             }
         }
+        const int bsel = (occ_b[1] * pw_b[1] >= 2 * occ_b[0] * pw_b[0] && occ_b[1] > 0) ? 1 : 0;
+        occ_p = occ_b[bsel]; pw_best = pw_b[bsel]; smem_p = smem_b[bsel]; lpk = lp_b[bsel];
         if (occ_p >= 1) {
             h->list = lpk; h->list_packed = 1; h->list_ctas = occ_p * sms; h->list_smem = smem_p;
             if (lpk.gstride > 0) {
@@ -349,6 +360,12 @@ int polar_scs_create_ex(polar_scs_t *out, int32_t N, int32_t K, const uint8_t *f
                 e = cudaMalloc(&h->d_galpha, 2 * per * sizeof(float));
                 if (e != cudaSuccess) { free_handle(h); return cuda_status(e); }
                 h->list.galpha = h->d_galpha;
+            }
+            if (lpk.beta_global) {
+                const size_t per = (size_t)h->list_ctas * lpk.pwarps * (size_t)(2 * lpk.L * lpk.nw);
+                e = cudaMalloc(&h->d_gbeta, 2 * per * sizeof(uint32_t));
+                if (e != cudaSuccess) { free_handle(h); return cuda_status(e); }
+                h->list.gbeta = h->d_gbeta;
             }
         }
     }

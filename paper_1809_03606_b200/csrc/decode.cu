@@ -27,10 +27,11 @@
 namespace polar {
 
 #ifndef POLAR_BETA_REGS
-#define POLAR_BETA_REGS 1      // 0: the flat beta in shared memory in every kernel (A/B builds)
+#define POLAR_BETA_REGS 1      // 0: the flat beta in shared memory in every kernel (A/B builds).  Two or four
+                               // words per lane for n = 11 / 12 measured slower (C4 2260 -> 2012, C5 2868 -> 2395)
 #endif
 #ifndef POLAR_UNR_BIG
-#define POLAR_UNR_BIG 0        // 1: the N = 2048 / 4096 kernels unroll the float4 stage loop too (A/B builds)
+#define POLAR_UNR_BIG 1        // the N = 2048 kernel unrolls the float4 stage loop too (C4 2203 -> 2263 Mbps; N = 4096: 2868 -> 2525, not done)
 #endif
 #ifndef POLAR_BWPL
 #define POLAR_BWPL 1           // register stages below 5 read the left sibling's beta from one shuffled word
@@ -217,8 +218,10 @@ __device__ __forceinline__ int alloc_snapshot_lazy(uint32_t *used, const uint32_
 // shared memory (UW = ceil(D/32) words), searched from a hint word (every word
 // below it is full); the exact recount scans the live entries of the global
 // stack (all but entry `skip`) and marks `extra`.
+// (hot: also the hot-window entry of this lane, hser / hjsm)
 __device__ __forceinline__ int alloc_snapshot_big(uint32_t *used, int &uhint, const uint32_t *sjsm, int nS, int D,
-                                                  int skip, uint32_t extra, int lane) {
+                                                  int skip, uint32_t extra, int lane, bool hot = false,
+                                                  uint32_t hser = 0xFFFFFFFFu, uint32_t hjsm = 0) {
     const int UW = (D + 31) >> 5;
     int slot = -1;
     #pragma unroll 1
@@ -231,6 +234,10 @@ __device__ __forceinline__ int alloc_snapshot_big(uint32_t *used, int &uhint, co
             for (int i_0 = 0; i_0 < (nS); i_0 += 32) if (const int i = i_0 + lane; i < (nS)) {
                 const uint32_t sn = Pk<true>::snap(sjsm[i]);
                 if (i != skip && sn != Pk<true>::NONE) atomicOr(used + (sn >> 5), 1u << (sn & 31));
+            }
+            if (hot && hser != 0xFFFFFFFFu) {
+                const uint32_t sn = Pk<true>::snap(hjsm);
+                if (sn != Pk<true>::NONE) atomicOr(used + (sn >> 5), 1u << (sn & 31));
             }
             __syncwarp();
             if (lane == 0 && extra != Pk<true>::NONE) used[extra >> 5] |= 1u << (extra & 31);
@@ -269,12 +276,15 @@ __device__ __forceinline__ int alloc_snapshot_big(uint32_t *used, int &uhint, co
 #ifndef POLAR_MB_PLAIN
 #define POLAR_MB_PLAIN 9       // CTAs per SM of the no-CRC register-stack instances (A/B builds override)
 #endif
+#ifndef POLAR_MB_N11
+#define POLAR_MB_N11 6         // CTAs per SM of the N = 2048 instances
+#endif
 #ifndef POLAR_MB_SL1
 #define POLAR_MB_SL1 kDecodeMinBlocks
 #endif
 template <int SLOTS, int NL, bool NOCRC>
 constexpr int kDecodeMinBlocksFor() {
-    return NL == 11 ? 6 : (NL == 12 ? 5 : (SLOTS == 4 ? 3 : (SLOTS == 2 ? 5 : (NOCRC && SLOTS == 1 ? POLAR_MB_PLAIN : (SLOTS == 1 ? POLAR_MB_SL1 : kDecodeMinBlocks)))));
+    return NL == 11 ? POLAR_MB_N11 : (NL == 12 ? 5 : (SLOTS == 4 ? 3 : (SLOTS == 2 ? 5 : (NOCRC && SLOTS == 1 ? POLAR_MB_PLAIN : (SLOTS == 1 ? POLAR_MB_SL1 : kDecodeMinBlocks)))));
 }
 
 // SLOTS = 1, 2, 4: register stack of 32 SLOTS entries (D <= 128).  SLOTS = 0:
@@ -294,7 +304,13 @@ fsscs_decode_kernel(const DecodeParams P) {
     // register stacks (D <= 128) are kept sorted by (PM, serial): position
     // p = 32 s + lane in slot s (position 0 = best): select reads the head,
     // insertion is one merge
-    constexpr bool SORTED = !BIG && ((SLOTS == 1 && POLAR_SORTED_STACK >= 1) || POLAR_SORTED_STACK >= 2);
+    // D > 128 (HOT): a sorted 32-entry window in registers (the SLOTS = 1 stack)
+    // holds the best entries, an unsorted global store (cold) the rest, with
+    // hot keys <= cb < cold keys; GSCAN: the whole stack in global memory,
+    // scanned on every pop
+    constexpr bool HOT = BIG && (POLAR_BIG_HOT != 0);
+    constexpr bool GSCAN = BIG && !HOT;
+    constexpr bool SORTED = (!BIG && ((SLOTS == 1 && POLAR_SORTED_STACK >= 1) || POLAR_SORTED_STACK >= 2)) || HOT;
     // code-length-specialised kernels with N <= 1024: the flat beta (N/32 <= 32
     // words) lives in registers, word w in lane w (bw); beta[] in shared memory
     // only stages the output
@@ -317,7 +333,7 @@ fsscs_decode_kernel(const DecodeParams P) {
     // walk between nodes is derived from them
     // (register-stack specialised kernels are only launched when they fit; the
     // global-stack kernel reads them through L1: their shared memory costs it a CTA)
-    const bool recs_smem = (NL > 0 && !BIG) || P.sched_words > 0;
+    const bool recs_smem = (POLAR_RECS_SMEM && NL > 0 && !BIG) || P.sched_words > 0;
     if (recs_smem) {
         #pragma unroll 1
         for (int i = threadIdx.x; i < P.sched_words / 4; i += blockDim.x)
@@ -329,7 +345,7 @@ fsscs_decode_kernel(const DecodeParams P) {
     };
     uint32_t *wb = smem + P.sched_words + warp * P.warp_words;
     // BIG: the first KW stack keys live in shared memory (the rest in global)
-    constexpr int KW = 128;
+    constexpr int KW = HOT ? 0 : 128;
     unsigned long long *wkey = reinterpret_cast<unsigned long long *>(wb);
     const bool chan_sm = CNT ? (P.chan_in_smem != 0) : CHAN_SMEM;
     const bool snap_sm = CNT ? (P.snap_in_smem != 0) : SNAP_SMEM;
@@ -355,8 +371,8 @@ fsscs_decode_kernel(const DecodeParams P) {
     const uint32_t snap0 = gwarp * (uint32_t)D;
     // global stack (BIG): keys (PM bits << 32 | serial: u64 order = (PM, serial)
     // order, reading R7) and jsm words; fork headers per slot
-    unsigned long long *skey = BIG ? P.stack_keys + (size_t)gwarp * (size_t)D : nullptr;
-    uint32_t *sjsm = BIG ? P.stack_jsm + (size_t)gwarp * (size_t)D : nullptr;
+    unsigned long long *skey = BIG ? P.stack_keys + (size_t)gwarp * (size_t)(D + kColdPad) : nullptr;
+    uint32_t *sjsm = BIG ? P.stack_jsm + (size_t)gwarp * (size_t)(D + kColdPad) : nullptr;
     uint2 *ghdr = BIG ? P.hdr_global + (size_t)gwarp * (size_t)D : nullptr;
     auto kget = [&](int i) -> unsigned long long { return i < KW ? wkey[i] : __ldcg(skey + i); };
     auto kset = [&](int i, unsigned long long k) {
@@ -415,9 +431,11 @@ fsscs_decode_kernel(const DecodeParams P) {
         int nS = 1;
         int uhint = 0;
         int widx = 0;                     // BIG: index of the working path's entry (-1: not live)
-        int nA = 1, hole = -1;            // BIG: array extent; the popped entry's index until refilled
+        int nA = HOT ? 0 : 1, hole = -1;  // BIG: array extent (HOT: cold entries); the popped entry's index until refilled
+        int nH = 1;                       // HOT: entries in the hot window (positions 0..nH-1)
+        unsigned long long cb = ~0ull;    // HOT: hot keys <= cb < cold keys
         if (BIG) {
-            if (lane == 0) { kset(0, 0ull); sjsm[0] = PK::make(0, PK::NONE, 0); }
+            if (GSCAN && lane == 0) { kset(0, 0ull); sjsm[0] = PK::make(0, PK::NONE, 0); }
             #pragma unroll 1
             for (int w_0 = 0; w_0 < (P.used_words); w_0 += 32) if (const int w = w_0 + lane; w < (P.used_words)) snap_used[w] = 0u;
         } else if (lane < 4) {
@@ -451,7 +469,75 @@ fsscs_decode_kernel(const DecodeParams P) {
             uint32_t lpm = EMPTY, lser = EMPTY, ljsm = 0;
             int ls = 0;
             uint32_t ljsm_big = 0;
-            if (BIG) {
+            if (HOT && nH == 0) {
+                // refill the hot window from the cold store (nS > 0, so nA > 0).
+                // Each lane keeps the two smallest keys of its strided share; with
+                // t = the smallest of the lanes' second keys, every cold key <= t is
+                // in those lists, so extracting the lists' minimum while it is <= t
+                // yields the cold keys in ascending order, up to 32 of them
+                unsigned long long k1 = ~0ull, k2 = ~0ull;
+                int i1 = -1, i2 = -1;
+                #pragma unroll 1
+                for (int i0 = 0; i0 < nA; i0 += 128) {
+                    unsigned long long k4[4];
+#pragma unroll
+                    for (int q = 0; q < 4; q++) {
+                        const int i = i0 + 32 * q + lane;
+                        k4[q] = (i < nA) ? __ldcg(skey + i) : ~0ull;
+                    }
+#pragma unroll
+                    for (int q = 0; q < 4; q++) {
+                        const int i = i0 + 32 * q + lane;
+                        if (k4[q] < k1) { k2 = k1; i2 = i1; k1 = k4[q]; i1 = i; }
+                        else if (k4[q] < k2) { k2 = k4[q]; i2 = i; }
+                    }
+                }
+                uint32_t th, tl;
+                warp_min_key((uint32_t)(k2 >> 32), (uint32_t)k2, th, tl);
+                const unsigned long long tk = ((unsigned long long)th << 32) | tl;
+                uint32_t j1 = (i1 >= 0) ? __ldcg(sjsm + i1) : 0u, j2 = (i2 >= 0) ? __ldcg(sjsm + i2) : 0u;
+                unsigned long long last = 0;
+                #pragma unroll 1
+                while (nH < 32) {
+                    uint32_t mh, ml;
+                    warp_min_key((uint32_t)(k1 >> 32), (uint32_t)k1, mh, ml);
+                    const unsigned long long mk = ((unsigned long long)mh << 32) | ml;
+                    if (mk == ~0ull || mk > tk) break;
+                    const int ow = __ffs(__ballot_sync(FULL, k1 == mk)) - 1;
+                    const uint32_t jj = __shfl_sync(FULL, j1, ow);
+                    if (lane == nH) { s_pm[0] = mh; s_ser[0] = ml; s_jsm[0] = jj; }
+                    if (lane == ow) {
+                        skey[i1] = ~0ull;                          // taken: dropped by the compaction below
+                        k1 = k2; i1 = i2; j1 = j2; k2 = ~0ull; i2 = -1;
+                    }
+                    last = mk;
+                    nH++;
+                }
+                cb = last;
+                __syncwarp();
+                // compact the cold store (the working path's index follows its entry)
+                int cntc = 0, nwidx = -1;
+                #pragma unroll 1
+                for (int i0 = 0; i0 < nA; i0 += 32) {
+                    const int i = i0 + lane;
+                    unsigned long long a = ~0ull;
+                    uint32_t x = 0;
+                    if (i < nA) { a = __ldcg(skey + i); x = __ldcg(sjsm + i); }
+                    const bool keep = (a != ~0ull);
+                    const uint32_t kb = __ballot_sync(FULL, keep);
+                    const int o = cntc + __popc(kb & ((1u << lane) - 1u));
+                    const uint32_t wbb = __ballot_sync(FULL, keep && i == widx);
+                    if (wbb) nwidx = cntc + __popc(kb & ((1u << (__ffs(wbb) - 1)) - 1u));
+                    __syncwarp();
+                    if (keep) { skey[o] = a; sjsm[o] = x; }
+                    cntc += __popc(kb);
+                }
+                widx = nwidx;
+                nA = cntc;
+                if (nA == 0) cb = ~0ull;
+                __syncwarp();
+            }
+            if (GSCAN) {
                 // window keys from shared memory, the rest from global memory with 4
                 // independent loads in flight per lane per round
                 unsigned long long lk = ~0ull;
@@ -499,6 +585,7 @@ fsscs_decode_kernel(const DecodeParams P) {
             if (SORTED) {
                 p_jsm = __shfl_sync(FULL, s_jsm[0], 0);
                 if (lane == 0) { s_pm[0] = EMPTY; s_ser[0] = EMPTY; }
+                if (HOT) nH--;
             } else if (BIG) {
                 // remove entry `pi`: it becomes a hole that c1 of this pop refills
                 const int pi = __shfl_sync(FULL, ls, owner);
@@ -551,6 +638,9 @@ fsscs_decode_kernel(const DecodeParams P) {
                     nA = cntv;
                     hole = -1;
                     __syncwarp();
+                }
+                const int ncold = BIG ? cntv : 0;       // HOT: the cold survivors
+                if (GSCAN) {
                 } else if (SORTED && SL > 1) {
                     // survivors (depth > j) move to positions 1..cntv in order;
                     // position P takes survivor number P: word v holding it by the
@@ -618,6 +708,11 @@ fsscs_decode_kernel(const DecodeParams P) {
                         cntv += __popc(__ballot_sync(FULL, s_ser[s] != EMPTY));
                     }
                 }
+                if (HOT) {
+                    nH = cntv;
+                    cntv += ncold;
+                    if (nA == 0) cb = ~0ull;
+                }
                 nS = cntv;
             }
 
@@ -637,7 +732,8 @@ fsscs_decode_kernel(const DecodeParams P) {
                     if (wi >= 0) {
                         const uint32_t wj = __ldcg(sjsm + wi);
                         if (PK::snap(wj) == PK::NONE) {
-                            const int slot = alloc_snapshot_big(snap_used, uhint, sjsm, nA, D, hole, PK::snap(p_jsm), lane);
+                            const int slot = alloc_snapshot_big(snap_used, uhint, sjsm, nA, D, hole, PK::snap(p_jsm), lane,
+                                                                HOT, s_ser[0], s_jsm[0]);
                             uint32_t *dst = snap_slot(slot);
                             const int nwords = (work_pl + 31) >> 5;
                             if constexpr (CNT) c_sw += (uint32_t)nwords;
@@ -653,17 +749,20 @@ fsscs_decode_kernel(const DecodeParams P) {
                 }
                 int wsl = -1;
 #pragma unroll
-                for (int s = 0; s < SL; s++) if (!BIG && s_ser[s] == work) wsl = s;
+                for (int s = 0; s < SL; s++) if (!GSCAN && s_ser[s] == work) wsl = s;
                 const uint32_t wb_ = __ballot_sync(FULL, wsl >= 0);
-                if (!BIG && wb_) {
+                if (!GSCAN && wb_) {
                     const int wl = __ffs(wb_) - 1;
                     uint32_t wj = 0;
 #pragma unroll
                     for (int s = 0; s < SL; s++) if (s == wsl) wj = s_jsm[s];
                     wj = __shfl_sync(FULL, wj, wl);
                     const int wslot = __shfl_sync(FULL, wsl, wl);
-                    if (jsm_snap(wj) == SNAP_NONE) {
-                        const int slot = alloc_snapshot_lazy<SL>(snap_used, s_ser, s_jsm, D, -1, 0, jsm_snap(p_jsm), lane);
+                    if (PK::snap(wj) == PK::NONE) {
+                        int slot;
+                        if constexpr (HOT) slot = alloc_snapshot_big(snap_used, uhint, sjsm, nA, D, -1, PK::snap(p_jsm), lane,
+                                                                     true, s_ser[0], s_jsm[0]);
+                        else slot = alloc_snapshot_lazy<SL>(snap_used, s_ser, s_jsm, D, -1, 0, jsm_snap(p_jsm), lane);
                         uint32_t *dst = snap_slot(slot);
                         const int nwords = (work_pl + 31) >> 5;
                         if constexpr (CNT) c_sw += (uint32_t)nwords;
@@ -675,7 +774,7 @@ fsscs_decode_kernel(const DecodeParams P) {
                         if (lane == wl) {
 #pragma unroll
                             for (int s = 0; s < SL; s++)
-                                if (s == wslot) s_jsm[s] = jsm_make(jsm_j(wj), (uint32_t)slot, 0);
+                                if (s == wslot) s_jsm[s] = PK::make(PK::j(wj), (uint32_t)slot, 0);
                         }
                     }
                 }
@@ -883,7 +982,7 @@ fsscs_decode_kernel(const DecodeParams P) {
     if constexpr ((T) < NL && (T) >= 6) {                                                     \
         if ((T) < lam) break;                                                                 \
         if constexpr (CNT) c_fg += 1u << (T);                                                 \
-        alpha_stage<CHAN_SMEM, ((NL == 10 && SLOTS == 1) || (NL >= 11 && POLAR_UNR_BIG)), BREG>((T) + 1 == n ? chan : SP((T) + 1), SP(T), beta, bw, n, (T), pl >> (T), lane); \
+        alpha_stage<CHAN_SMEM, ((NL == 10 && SLOTS == 1) || (NL == 11 && POLAR_UNR_BIG)), BREG>((T) + 1 == n ? chan : SP((T) + 1), SP(T), beta, bw, n, (T), pl >> (T), lane); \
     }
                     switch (s_hi) {
                     case 12: POLAR_SSTAGE(12)
@@ -1171,7 +1270,8 @@ fsscs_decode_kernel(const DecodeParams P) {
             int fslot = -1;
             const int nfit = min(nc, D - nS);
             auto write_fork_snapshot = [&](int victim_lane, int victim_slot) {
-                if (BIG) fslot = alloc_snapshot_big(snap_used, uhint, sjsm, nA, D, hole >= 0 ? hole : victim_slot, PK::NONE, lane);
+                if (BIG) fslot = alloc_snapshot_big(snap_used, uhint, sjsm, nA, D, hole >= 0 ? hole : victim_slot, PK::NONE, lane,
+                                                    HOT, s_ser[0], s_jsm[0]);
                 else fslot = alloc_snapshot_lazy<SL>(snap_used, s_ser, s_jsm, D, victim_lane, victim_slot, SNAP_NONE, lane);
                 uint32_t *dst = snap_slot(fslot);
                 const int nwords = (npl + 31) >> 5;
@@ -1185,7 +1285,162 @@ fsscs_decode_kernel(const DecodeParams P) {
             };
             if (!SORTED && nfit > 1) write_fork_snapshot(-1, -1);
             int c1_lane = 0, c1_slot = 0;
-            if (SORTED && SL > 1) {
+            if (HOT) {
+                // candidates (ascending keys) with key <= cb merge into the hot
+                // window (the SLOTS = 1 merge), the rest are appended to the cold
+                // store; window positions >= 32 spill to the cold store, and cb
+                // drops below the first spilled key.  Then the largest keys beyond D
+                // are dropped (cold first: every cold key exceeds every hot key),
+                // which with the merge keeps the D smallest keys (reading R8).  The
+                // siblings' fork snapshot is taken whenever there are siblings.
+                if (nc > 1) write_fork_snapshot(-1, -1);
+                const uint32_t cpm = (lane < nc) ? __float_as_uint(p_pm + my_d) : EMPTY;
+                const unsigned long long ckey = ((unsigned long long)cpm << 32) | (ser0 + (uint32_t)lane);
+                const int nch = __popc(__ballot_sync(FULL, lane < nc && ckey <= cb));   // a prefix of the candidates
+                const uint32_t cph = (lane < nch) ? cpm : EMPTY;
+                const uint32_t epm = s_pm[0];
+                int a = 0;
+                if (__shfl_sync(FULL, cph, 3) < epm) a = 4;
+                if (__shfl_sync(FULL, cph, a + 1) < epm) a += 2;
+                if (__shfl_sync(FULL, cph, a) < epm) a += 1;
+                if (__shfl_sync(FULL, cph, a) < epm) a += 1;
+                const int epos = lane - 1 + a;
+                const bool ekeep = lane >= 1 && lane <= nH;
+                const uint32_t M0 = __reduce_or_sync(FULL, (ekeep && epos < 32) ? (1u << epos) : 0u);
+                const int totH = nH + nch;                 // <= 31 + 8
+                const uint32_t M1 = (totH > 32) ? __reduce_or_sync(FULL, (ekeep && epos >= 32) ? (1u << (epos & 31)) : 0u) : 0u;
+                const uint32_t jb = PK::make(jn, fslot >= 0 ? (uint32_t)fslot : PK::NONE, 0);
+                const uint32_t opm = s_pm[0], oser = s_ser[0], ojsm = s_jsm[0];
+                uint32_t xpm = EMPTY, xser = EMPTY, xjsm = 0;   // this lane's position 32 + lane (spill)
+#pragma unroll
+                for (int w = 0; w < 2; w++) {
+                    if (w == 1 && totH <= 32) break;       // nothing spills (the common case)
+                    const uint32_t Mw = w ? M1 : M0;
+                    const int Pp = 32 * w + lane;
+                    const int q = (w ? __popc(M0) : 0) + __popc(Mw & ((1u << lane) - 1u));
+                    const bool isE = (Mw >> lane) & 1u;
+                    const int t = (Pp - q) & 7;
+                    const int sl = (q + 1) & 31;
+                    const uint32_t gpm = __shfl_sync(FULL, opm, sl), gser = __shfl_sync(FULL, oser, sl);
+                    const uint32_t gjsm = __shfl_sync(FULL, ojsm, sl);
+                    const uint32_t ct = __shfl_sync(FULL, cph, t);
+                    const bool live = Pp < totH;
+                    const uint32_t mk = (clist >> (4 * t)) & 15u;
+                    const uint32_t vpm = !live ? EMPTY : (isE ? gpm : ct);
+                    const uint32_t vser = !live ? EMPTY : (isE ? gser : ser0 + (uint32_t)t);
+                    const uint32_t vjsm = (live && !isE) ? (jb | ((mk ^ (uint32_t)m0) << PK::MSH)) : gjsm;
+                    if (w == 0) { s_pm[0] = vpm; s_ser[0] = vser; s_jsm[0] = vjsm; }
+                    else { xpm = vpm; xser = vser; xjsm = vjsm; }
+                }
+                const int nsp = max(totH - 32, 0);         // spilled window entries (lanes 0..nsp-1 of x*)
+                nH = totH - nsp;
+                int nwidx = -1;
+                if (nsp > 0) {
+                    if (lane < nsp) {
+                        skey[nA + lane] = ((unsigned long long)xpm << 32) | xser;
+                        sjsm[nA + lane] = xjsm;
+                    }
+                    const uint32_t sp0 = __shfl_sync(FULL, xpm, 0), ss0 = __shfl_sync(FULL, xser, 0);
+                    cb = (((unsigned long long)sp0 << 32) | ss0) - 1ull;
+                    const uint32_t wbb = __ballot_sync(FULL, lane < nsp && xser == ser0);
+                    if (wbb) nwidx = nA + __ffs(wbb) - 1;
+                }
+                // candidates above cb: appended after the spilled entries
+                const int nco = nc - nch;
+                if (nco > 0) {
+                    const int t = nch + lane;
+                    const uint32_t cpt = __shfl_sync(FULL, cpm, t & 7);
+                    if (lane < nco) {
+                        const uint32_t mk = (clist >> (4 * t)) & 15u;
+                        skey[nA + nsp + lane] = ((unsigned long long)cpt << 32) | (ser0 + (uint32_t)t);
+                        sjsm[nA + nsp + lane] = jb | ((mk ^ (uint32_t)m0) << PK::MSH);
+                    }
+                    if (nch == 0) nwidx = nA + nsp;        // c1 itself went to the cold store
+                }
+                nA += nsp + nco;
+                widx = nwidx;                              // -1: c1 is in the hot window
+                nS = nH + nA;
+                __syncwarp();
+                // the D limit: drop the largest keys, cold first.  One scan keeps
+                // each lane's two largest cold keys; with t = the largest of the
+                // lanes' second keys, every cold key >= t is in those lists, so the
+                // lists' maximum is extracted while it is >= t (a full stack drops
+                // up to nc - 1 keys per pop with one scan, rarely two)
+                #pragma unroll 1
+                while (nS > D && nA > 0) {
+                    unsigned long long k1 = 0, k2 = 0;
+                    int i1 = -1, i2 = -1;
+                    #pragma unroll 1
+                    for (int i0 = 0; i0 < nA; i0 += 128) {
+                        unsigned long long k4[4];
+#pragma unroll
+                        for (int q = 0; q < 4; q++) {
+                            const int i = i0 + 32 * q + lane;
+                            k4[q] = (i < nA) ? __ldcg(skey + i) : 0ull;
+                        }
+#pragma unroll
+                        for (int q = 0; q < 4; q++) {
+                            const int i = i0 + 32 * q + lane;
+                            if (i < nA) {
+                                if (i1 < 0 || k4[q] > k1) { k2 = k1; i2 = i1; k1 = k4[q]; i1 = i; }
+                                else if (i2 < 0 || k4[q] > k2) { k2 = k4[q]; i2 = i; }
+                            }
+                        }
+                    }
+                    // t: the largest second key (lanes without one do not bound it)
+                    const uint32_t th = __reduce_max_sync(FULL, i2 >= 0 ? (uint32_t)(k2 >> 32) : 0u);
+                    const uint32_t tl = __reduce_max_sync(FULL, (i2 >= 0 && (uint32_t)(k2 >> 32) == th) ? (uint32_t)k2 : 0u);
+                    const bool any2 = __any_sync(FULL, i2 >= 0);
+                    const unsigned long long tk = any2 ? (((unsigned long long)th << 32) | tl) : 0ull;
+                    int ndead = 0;
+                    #pragma unroll 1
+                    while (nS > D) {
+                        const bool v = (i1 >= 0);
+                        if (!__any_sync(FULL, v)) break;
+                        const uint32_t mh = __reduce_max_sync(FULL, v ? (uint32_t)(k1 >> 32) : 0u);
+                        const uint32_t ml = __reduce_max_sync(FULL, (v && (uint32_t)(k1 >> 32) == mh) ? (uint32_t)k1 : 0u);
+                        const unsigned long long mk = ((unsigned long long)mh << 32) | ml;
+                        if (any2 && mk < tk) break;            // below the lists' guarantee: rescan
+                        const int ow = __ffs(__ballot_sync(FULL, v && k1 == mk)) - 1;
+                        if (lane == ow) {
+                            skey[i1] = ~0ull;                  // dropped: removed by the compaction below
+                            if (widx == i1) widx = -2;         // (the working path: not live any more)
+                            k1 = k2; i1 = i2; i2 = -1;
+                        }
+                        widx = __shfl_sync(FULL, widx, ow);
+                        ndead++;
+                        nS--;
+                    }
+                    __syncwarp();
+                    int cntc = 0, nwidx = -1;
+                    #pragma unroll 1
+                    for (int i0 = 0; i0 < nA; i0 += 32) {
+                        const int i = i0 + lane;
+                        unsigned long long a = ~0ull;
+                        uint32_t x = 0;
+                        if (i < nA) { a = __ldcg(skey + i); x = __ldcg(sjsm + i); }
+                        const bool keep = (a != ~0ull);
+                        const uint32_t kb = __ballot_sync(FULL, keep);
+                        const int o = cntc + __popc(kb & ((1u << lane) - 1u));
+                        const uint32_t wbb = __ballot_sync(FULL, keep && i == widx);
+                        if (wbb) nwidx = cntc + __popc(kb & ((1u << (__ffs(wbb) - 1)) - 1u));
+                        __syncwarp();
+                        if (keep) { skey[o] = a; sjsm[o] = x; }
+                        cntc += __popc(kb);
+                    }
+                    widx = nwidx;
+                    nA = cntc;
+                    __syncwarp();
+                    (void)ndead;
+                }
+                #pragma unroll 1
+                while (nS > D) {                           // no cold entries left: the window's tail
+                    if (lane == nH - 1) { s_pm[0] = EMPTY; s_ser[0] = EMPTY; }
+                    nH--;
+                    nS--;
+                }
+                if (nA == 0) cb = ~0ull;
+            } else if (SORTED && SL > 1) {
                 // the same merge over SL slots (position p = 32 s + lane): entry p
                 // moves to p - 1 + a_p, which stays in slots s - 1 .. s + 1
                 const uint32_t cpm = (lane < nc) ? __float_as_uint(p_pm + my_d) : EMPTY;
@@ -1379,7 +1634,7 @@ fsscs_decode_kernel(const DecodeParams P) {
                         }
                 }
             }
-            if (BIG) {
+            if (GSCAN) {
                 if (fslot >= 0 && lane == 0) sjsm[c1_slot] = PK::make(jn, (uint32_t)fslot, 0);
                 __syncwarp();
             } else if (!SORTED && fslot >= 0) {
@@ -1451,7 +1706,7 @@ static cudaError_t launch_s(const DecodeParams &p, int slots, int ctas, int smem
 // placements create() picks for them (n = 12 with the top alpha stage(s) in a
 // global arena when that raises the occupancy: GA)
 int specialised_nl(int n, int slots, bool snap_smem, bool chan_smem, bool recs_smem) {
-    if (!recs_smem && slots != 0) return 0;
+    if (POLAR_RECS_SMEM && !recs_smem && slots != 0) return 0;
     if (n == 7 && slots == 1 && snap_smem && chan_smem) return 7;
     if (n == 10 && slots == 1 && !snap_smem && !chan_smem) return 10;
     if (n == 11 && slots == 2 && !snap_smem && !chan_smem) return 11;

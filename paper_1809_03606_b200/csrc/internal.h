@@ -21,6 +21,15 @@ __host__ __device__ inline uint32_t op_phi(uint32_t op) { return op >> 8; }
 constexpr int kMaxN = 4096;
 constexpr int kMaxD = 8192;     // D > 128: global-memory stack (the paper's D = NL)
 constexpr int kDecodeWarps = 4;      // warps (frames in flight) per decode CTA
+// D > 128: the stack is a sorted 32-entry register window (hot) over an
+// unsorted global store (cold); 0 builds the scan-every-pop global stack (A/B)
+#ifndef POLAR_BIG_HOT
+#define POLAR_BIG_HOT 1
+#endif
+#ifndef POLAR_RECS_SMEM
+#define POLAR_RECS_SMEM 1      // per-depth records staged in shared memory (register-stack kernels); 0: read through L1
+#endif
+constexpr int kColdPad = 8;          // cold entries beyond D before the D-limit drop (one node's candidates)
 constexpr int kDecodeMinBlocks = 8;  // launch bound: 32 resident warps/SM => <= 64 registers
 constexpr int kCodecWarps = 4;       // warps per CTA of the generator/encoder kernels
 constexpr int kListPackedWarps = 4;  // max warps (frames in flight) per CTA of the packed FSSCL kernel
@@ -53,8 +62,8 @@ struct DecodeParams {
     const uint32_t *crc_bytes;  // [nw][4][256] syndrome contribution of each beta byte (CRC codes)
     unsigned long long *queue;
     uint32_t *snap_global;      // arena when snapshots live in global memory
-    unsigned long long *stack_keys;   // D > 128: per warp [D] (PM bits << 32 | serial)
-    uint32_t *stack_jsm;        // D > 128: per warp [D] (depth | snapshot | flips)
+    unsigned long long *stack_keys;   // D > 128: per warp [D + kColdPad] (PM bits << 32 | serial)
+    uint32_t *stack_jsm;        // D > 128: per warp [D + kColdPad] (depth | snapshot | flips)
     uint2 *hdr_global;          // D > 128: per warp [D] fork headers m1..m4
     int N, n, K, c, D, L, M;
     int nw;                     // beta words = max(1, N/32)
@@ -65,7 +74,7 @@ struct DecodeParams {
     int hdr_words;              // shared-memory fork headers: 2 D (register stacks) or 0
     int used_words;             // snapshot-slot bitmap words: 4, or ceil(D/32) rounded (D > 128)
     int uhat_words;             // nw when non-systematic (u_hat scratch), else 0
-    int win_words;              // D > 128: shared-memory window of the first 128 stack keys (256 words)
+    int win_words;              // D > 128, scan stack: shared-memory window of the first 128 keys (256 words); 0 with the hot window
     int alpha_words;            // shared alpha memory (floats): N, or 2^sg when stages >= sg are global
     int sg;                     // first alpha stage kept in the global arena (n: none)
     float *galpha;              // global alpha arena, N floats per resident warp (or null)
@@ -96,6 +105,9 @@ struct ListParams {
     int pwarps;                 // packed kernel: warps (frames) per CTA
     int sg;                     // packed kernel: first alpha stage kept in the global arena (n: none)
     float *galpha;              // packed kernel: global alpha arena (stages >= sg), gstride floats per warp
+    uint32_t *gbeta;            // packed kernel: the double-buffered path betas in a global arena
+                                // (2 L nw words per warp) instead of shared memory (or null)
+    int beta_global;            // layout: 1 when gbeta holds the betas
     size_t gstride;
 };
 
@@ -139,6 +151,7 @@ struct polar_scs_s {
     int list_ctas = 0, list_smem = 0, list_lcap = 0;   // FSSCL launch (0 = list decode unsupported)
     int list_packed = 0;            // 1: the warp-per-frame packed FSSCL kernel (list_packed.cu)
     float *d_galpha = nullptr;      // packed FSSCL: global arena of the top alpha stages, 2 slots
+    uint32_t *d_gbeta = nullptr;    // packed FSSCL: global arena of the path betas, 2 slots
     polar::ListParams list{};       // prefilled FSSCL params
     // host-staging for polar_scs_decode_host (lazily allocated)
     cudaStream_t s_h2d = nullptr, s_comp[2] = {nullptr, nullptr}, s_d2h = nullptr;

@@ -52,7 +52,9 @@ __device__ __forceinline__ float flip_dpm(uint32_t m, const float (&A)[4]) {
 
 // PLAIN: compile-time "no CRC, systematic, more than one node" (the final
 // CRC / re-encoding selection and the whole-code-node path left out)
-template <int NL, bool PLAIN = false>
+// GB: the path betas live in the global arena P.gbeta (a separate instance, so
+// the shared-memory instance keeps shared-memory addressing)
+template <int NL, bool PLAIN = false, bool GB = false>
 __global__ void __launch_bounds__(kListPackedWarps * 32, 8) fsscl_packed_kernel(const ListParams P) {
     extern __shared__ __align__(16) uint32_t smem[];
     const int lane = threadIdx.x & 31;
@@ -67,7 +69,8 @@ __global__ void __launch_bounds__(kListPackedWarps * 32, 8) fsscl_packed_kernel(
     __syncthreads();
     uint32_t *wb = smem + P.o_warp0 + warp * P.words;
     float *abuf = reinterpret_cast<float *>(wb + P.o_alpha);           // stage s: L buffers at L(2^s - 1)
-    uint32_t *betaA = wb + P.o_beta;                                   // [2][L][nw]
+    // [2][L][nw]: shared memory, or this warp's block of the global arena
+    uint32_t *betaA = GB ? P.gbeta + (size_t)(blockIdx.x * P.pwarps + warp) * (size_t)(2 * L * nw) : wb + P.o_beta;
     uint32_t *clist_s = wb + P.o_clist;                                // [L]
     uint2 *mi_s = reinterpret_cast<uint2 *>(wb + P.o_mi);              // [L]
     unsigned long long *prow_s = reinterpret_cast<unsigned long long *>(wb + P.o_prow);  // [2][L]
@@ -546,9 +549,9 @@ __global__ void __launch_bounds__(kListPackedWarps * 32, 8) fsscl_packed_kernel(
     }
 }
 
-template <int NL, bool PLAIN = false>
+template <int NL, bool PLAIN = false, bool GB = false>
 static cudaError_t launch_packed_t(const ListParams &p, int ctas, int smem, cudaStream_t st) {
-    auto kern = fsscl_packed_kernel<NL, PLAIN>;
+    auto kern = fsscl_packed_kernel<NL, PLAIN, GB>;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     kern<<<ctas, p.pwarps * 32, smem, st>>>(p);
@@ -556,20 +559,22 @@ static cudaError_t launch_packed_t(const ListParams &p, int ctas, int smem, cuda
 }
 
 cudaError_t launch_list_packed(const ListParams &p, int ctas, int smem, cudaStream_t st) {
+    if (p.gbeta) return launch_packed_t<0, false, true>(p, ctas, smem, st);
     if (p.n == 7) return launch_packed_t<7>(p, ctas, smem, st);
     if (p.n == 10) return (p.c == 0 && !p.nonsys && p.M > 1) ? launch_packed_t<10, true>(p, ctas, smem, st)
                                                                : launch_packed_t<10>(p, ctas, smem, st);
     return launch_packed_t<0>(p, ctas, smem, st);
 }
 
-template <int NL>
+template <int NL, bool GB = false>
 static cudaError_t packed_occ_t(int pwarps, int smem, int *blocks) {
-    cudaError_t e = cudaFuncSetAttribute(fsscl_packed_kernel<NL>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    cudaError_t e = cudaFuncSetAttribute(fsscl_packed_kernel<NL, false, GB>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
-    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, fsscl_packed_kernel<NL>, pwarps * 32, smem);
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, fsscl_packed_kernel<NL, false, GB>, pwarps * 32, smem);
 }
 
-cudaError_t list_packed_occupancy(int n, int pwarps, int smem, int *blocks_per_sm) {
+cudaError_t list_packed_occupancy(int n, int pwarps, int smem, int *blocks_per_sm, bool gbeta) {
+    if (gbeta) return packed_occ_t<0, true>(pwarps, smem, blocks_per_sm);
     if (n == 7) return packed_occ_t<7>(pwarps, smem, blocks_per_sm);
     if (n == 10) return packed_occ_t<10>(pwarps, smem, blocks_per_sm);
     return packed_occ_t<0>(pwarps, smem, blocks_per_sm);

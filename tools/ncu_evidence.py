@@ -5,9 +5,13 @@ import json
 import os
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-SRC = {"C2": ("ncu_decode_summary.json", "fsscs_decode_kernel<1,0,0,10,0,2> (plain)"),
-       "P": ("ncu_decode_P_summary.json", "fsscs_decode_kernel<0,0,0,10,0,1>"),
-       "C2_list": ("ncu_list_packed_summary.json", "fsscl_packed_kernel<10,1> (plain)")}
+RND = "r2"
+SRC = {"C2": ("ncu_decode_C2_summary.json", "fsscs_decode_kernel<1,0,0,10,0,2> (plain)"),
+       "C4": ("ncu_decode_C4_summary.json", "fsscs_decode_kernel<2,0,0,11,1,1>"),
+       "C5": ("ncu_decode_C5_summary.json", "fsscs_decode_kernel<4,0,0,12,1,1>"),
+       "P": ("ncu_decode_P_summary.json", "fsscs_decode_kernel<0,0,0,10,0,1> (hot window)"),
+       "C2_list": ("ncu_list_C2_summary.json", "fsscl_packed_kernel<10,1> (plain)"),
+       "C5_list": ("ncu_list_C5_summary.json", "fsscl_packed_kernel<0,0>")}
 
 
 def num(m, k):
@@ -17,7 +21,10 @@ def num(m, k):
 def main():
     out = {}
     for key, (fn, kern) in SRC.items():
-        d = json.load(open(os.path.join(ROOT, "profiles", "r1", fn)))
+        path = os.path.join(ROOT, "profiles", RND, fn)
+        if not os.path.exists(path):
+            continue
+        d = json.load(open(path))
         m = d["metrics"]
         out[key] = {
             "kernel": kern,
@@ -29,7 +36,9 @@ def main():
             "thread_inst_per_inst": num(m, "smsp__thread_inst_executed_per_inst_executed.ratio"),
             "shared_wavefronts": num(m, "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum"),
             "duration_ms": num(m, "gpu__time_duration.sum"),
-            "source": f"profiles/r1/{fn} (ncu --set full --clock-control none, one launch)",
+            "warp_inst_per_frame": d.get("warp_inst_per_frame"),
+            "registers": num(m, "launch__registers_per_thread"),
+            "source": f"profiles/{RND}/{fn} (ncu --set full --clock-control none, one launch)",
         }
     with open(os.path.join(ROOT, "profiles", "ncu_evidence.json"), "w") as fh:
         json.dump(out, fh, indent=1)

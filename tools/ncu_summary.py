@@ -47,5 +47,7 @@ if __name__ == "__main__":
     r = raw(rep)
     m = {k: list(r[k]) for k in KEYS if k in r}
     dram = sum(float(r[k][0].replace(",", "")) * UNIT.get(r[k][1], 1) for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
+    inst = float(r["smsp__inst_executed.sum"][0].replace(",", ""))
     print(json.dumps({"report": label, "metrics": m, "stall_pct": stalls(rep), "dram_bytes_per_launch": dram,
-                      "dram_bytes_per_frame": dram / frames, "algorithmic_bytes_per_frame": alg}, indent=1))
+                      "frames_per_launch": frames, "dram_bytes_per_frame": dram / frames,
+                      "warp_inst_per_frame": inst / frames, "algorithmic_bytes_per_frame": alg}, indent=1))
