@@ -33,6 +33,16 @@ namespace polar {
 #ifndef POLAR_UNR_BIG
 #define POLAR_UNR_BIG 1        // the N = 2048 kernel unrolls the float4 stage loop too (C4 2203 -> 2263 Mbps; N = 4096: 2868 -> 2525, not done)
 #endif
+#ifndef POLAR_MERGE_FAST
+#define POLAR_MERGE_FAST 0     // register stacks: the all-candidates-first merge as a shift (measured slower:
+                               // C2 6702 -> 6654, C4 2264 -> 2203, C5 2872 -> 2822 Mbps)
+#endif
+#ifndef POLAR_MERGE_FAST_HOT
+#define POLAR_MERGE_FAST_HOT 1 // the same for the D > 128 window (P 2838 -> 2870)
+#endif
+#ifndef POLAR_SNAP_SOFT
+#define POLAR_SNAP_SOFT 32     // snapshot slots above this trigger an exact recount (lazy bitmaps); 1 << 30: never
+#endif
 #ifndef POLAR_BWPL
 #define POLAR_BWPL 1           // register stages below 5 read the left sibling's beta from one shuffled word
 #endif
@@ -173,7 +183,7 @@ __device__ __forceinline__ int alloc_snapshot(const uint32_t (&s_ser)[SLOTS], co
 template <int SLOTS>
 __device__ __forceinline__ int alloc_snapshot_lazy(uint32_t *used, const uint32_t (&s_ser)[SLOTS],
                                                    const uint32_t (&s_jsm)[SLOTS], int D, int skip_lane,
-                                                   int skip_slot, uint32_t extra, int lane) {
+                                                   int skip_slot, uint32_t extra, int lane, int nlive = 0) {
     if (SLOTS == 1) return alloc_snapshot<SLOTS>(s_ser, s_jsm, D, skip_lane, skip_slot, extra, lane);  // 1 REDUX: exact
     int slot = -1;
 #pragma unroll
@@ -183,7 +193,11 @@ __device__ __forceinline__ int alloc_snapshot_lazy(uint32_t *used, const uint32_
         if (lim < 32) freem &= (lim > 0) ? ((1u << lim) - 1u) : 0u;
         if (slot < 0 && freem) slot = w * 32 + __ffs(freem) - 1;
     }
-    if (slot < 0) {
+    // an exact recount also when the first free slot is above POLAR_SNAP_SOFT
+    // + the live entries (so a recount always lands below the cap):
+    // the slots in use stay compact, so the per-warp arena stays L2-resident
+    if (slot < 0 || slot >= POLAR_SNAP_SOFT + nlive) {
+        slot = -1;
 #pragma unroll
         for (int w = 0; w < SLOTS; w++) {
             uint32_t u = 0;
@@ -224,6 +238,9 @@ __device__ __forceinline__ int alloc_snapshot_big(uint32_t *used, int &uhint, co
                                                   uint32_t hser = 0xFFFFFFFFu, uint32_t hjsm = 0) {
     const int UW = (D + 31) >> 5;
     int slot = -1;
+    // (pass 0 finds a slot above max(POLAR_SNAP_SOFT, 2 nS): recount, so the
+    // slots in use stay compact and the arena L2-resident)
+    const int soft = max(POLAR_SNAP_SOFT, 2 * nS + 64);
     #pragma unroll 1
     for (int pass = 0; pass < 2 && slot < 0; pass++) {
         if (pass == 1) {
@@ -259,6 +276,7 @@ __device__ __forceinline__ int alloc_snapshot_big(uint32_t *used, int &uhint, co
                 const uint32_t fv = __shfl_sync(FULL, fm, fl);
                 slot = 32 * (w0 + fl) + __ffs(fv) - 1;
                 uhint = w0 + fl;
+                if (pass == 0 && slot >= soft) slot = -1;
                 break;
             }
         }
@@ -277,7 +295,7 @@ __device__ __forceinline__ int alloc_snapshot_big(uint32_t *used, int &uhint, co
 #define POLAR_MB_PLAIN 9       // CTAs per SM of the no-CRC register-stack instances (A/B builds override)
 #endif
 #ifndef POLAR_MB_N11
-#define POLAR_MB_N11 6         // CTAs per SM of the N = 2048 instances
+#define POLAR_MB_N11 7         // CTAs per SM of the N = 2048 instances (7 x 29 KB shared memory fits)
 #endif
 #ifndef POLAR_MB_SL1
 #define POLAR_MB_SL1 kDecodeMinBlocks
@@ -762,7 +780,7 @@ fsscs_decode_kernel(const DecodeParams P) {
                         int slot;
                         if constexpr (HOT) slot = alloc_snapshot_big(snap_used, uhint, sjsm, nA, D, -1, PK::snap(p_jsm), lane,
                                                                      true, s_ser[0], s_jsm[0]);
-                        else slot = alloc_snapshot_lazy<SL>(snap_used, s_ser, s_jsm, D, -1, 0, jsm_snap(p_jsm), lane);
+                        else slot = alloc_snapshot_lazy<SL>(snap_used, s_ser, s_jsm, D, -1, 0, jsm_snap(p_jsm), lane, nS);
                         uint32_t *dst = snap_slot(slot);
                         const int nwords = (work_pl + 31) >> 5;
                         if constexpr (CNT) c_sw += (uint32_t)nwords;
@@ -1272,7 +1290,7 @@ fsscs_decode_kernel(const DecodeParams P) {
             auto write_fork_snapshot = [&](int victim_lane, int victim_slot) {
                 if (BIG) fslot = alloc_snapshot_big(snap_used, uhint, sjsm, nA, D, hole >= 0 ? hole : victim_slot, PK::NONE, lane,
                                                     HOT, s_ser[0], s_jsm[0]);
-                else fslot = alloc_snapshot_lazy<SL>(snap_used, s_ser, s_jsm, D, victim_lane, victim_slot, SNAP_NONE, lane);
+                else fslot = alloc_snapshot_lazy<SL>(snap_used, s_ser, s_jsm, D, victim_lane, victim_slot, SNAP_NONE, lane, nS);
                 uint32_t *dst = snap_slot(fslot);
                 const int nwords = (npl + 31) >> 5;
                 if constexpr (CNT) c_sw += (uint32_t)nwords;
@@ -1298,6 +1316,20 @@ fsscs_decode_kernel(const DecodeParams P) {
                 const unsigned long long ckey = ((unsigned long long)cpm << 32) | (ser0 + (uint32_t)lane);
                 const int nch = __popc(__ballot_sync(FULL, lane < nc && ckey <= cb));   // a prefix of the candidates
                 const uint32_t cph = (lane < nch) ? cpm : EMPTY;
+                const int totH = nH + nch;                 // <= 31 + 8
+                const uint32_t jb = PK::make(jn, fslot >= 0 ? (uint32_t)fslot : PK::NONE, 0);
+                uint32_t xpm = EMPTY, xser = EMPTY, xjsm = 0;   // this lane's position 32 + lane (spill)
+                const uint32_t e1 = __shfl_sync(FULL, s_pm[0], 1), clast = __shfl_sync(FULL, cph, (nch - 1) & 7);
+                if (POLAR_MERGE_FAST_HOT && nch > 0 && totH <= 32 && clast < e1) {
+                    // the window candidates all precede its entries: a shift (no spill)
+                    const int sh = nch - 1;
+                    const uint32_t upm = __shfl_up_sync(FULL, s_pm[0], sh), user = __shfl_up_sync(FULL, s_ser[0], sh);
+                    const uint32_t ujsm = __shfl_up_sync(FULL, s_jsm[0], sh);
+                    const bool live = lane < totH, isC = lane < nch;
+                    s_pm[0] = !live ? EMPTY : (isC ? cph : upm);
+                    s_ser[0] = !live ? EMPTY : (isC ? ser0 + (uint32_t)lane : user);
+                    s_jsm[0] = (live && isC) ? (jb | ((my_m ^ (uint32_t)m0) << PK::MSH)) : ujsm;
+                } else {
                 const uint32_t epm = s_pm[0];
                 int a = 0;
                 if (__shfl_sync(FULL, cph, 3) < epm) a = 4;
@@ -1307,11 +1339,8 @@ fsscs_decode_kernel(const DecodeParams P) {
                 const int epos = lane - 1 + a;
                 const bool ekeep = lane >= 1 && lane <= nH;
                 const uint32_t M0 = __reduce_or_sync(FULL, (ekeep && epos < 32) ? (1u << epos) : 0u);
-                const int totH = nH + nch;                 // <= 31 + 8
                 const uint32_t M1 = (totH > 32) ? __reduce_or_sync(FULL, (ekeep && epos >= 32) ? (1u << (epos & 31)) : 0u) : 0u;
-                const uint32_t jb = PK::make(jn, fslot >= 0 ? (uint32_t)fslot : PK::NONE, 0);
                 const uint32_t opm = s_pm[0], oser = s_ser[0], ojsm = s_jsm[0];
-                uint32_t xpm = EMPTY, xser = EMPTY, xjsm = 0;   // this lane's position 32 + lane (spill)
 #pragma unroll
                 for (int w = 0; w < 2; w++) {
                     if (w == 1 && totH <= 32) break;       // nothing spills (the common case)
@@ -1331,6 +1360,7 @@ fsscs_decode_kernel(const DecodeParams P) {
                     const uint32_t vjsm = (live && !isE) ? (jb | ((mk ^ (uint32_t)m0) << PK::MSH)) : gjsm;
                     if (w == 0) { s_pm[0] = vpm; s_ser[0] = vser; s_jsm[0] = vjsm; }
                     else { xpm = vpm; xser = vser; xjsm = vjsm; }
+                }
                 }
                 const int nsp = max(totH - 32, 0);         // spilled window entries (lanes 0..nsp-1 of x*)
                 nH = totH - nsp;
@@ -1444,6 +1474,36 @@ fsscs_decode_kernel(const DecodeParams P) {
                 // the same merge over SL slots (position p = 32 s + lane): entry p
                 // moves to p - 1 + a_p, which stays in slots s - 1 .. s + 1
                 const uint32_t cpm = (lane < nc) ? __float_as_uint(p_pm + my_d) : EMPTY;
+#if POLAR_MERGE_FAST
+                const uint32_t e1 = __shfl_sync(FULL, s_pm[0], 1), clast = __shfl_sync(FULL, cpm, (nc - 1) & 7);
+                if (clast < e1) {
+                    // every candidate ahead of every entry: candidates at 0..nc-1, the
+                    // entries shift up by nc - 1 (slots descending: slot q reads the
+                    // old slots q and q - 1)
+                    const int total = min(D, nS + nc);
+                    if (min(nc, D) > 1) write_fork_snapshot(-1, -1);
+                    const uint32_t jb = jsm_make(jn, fslot >= 0 ? (uint32_t)fslot : SNAP_NONE, 0);
+                    const int sh = nc - 1;
+#pragma unroll
+                    for (int q = SL - 1; q >= 0; q--) {
+                        uint32_t vp = __shfl_up_sync(FULL, s_pm[q], sh), vs = __shfl_up_sync(FULL, s_ser[q], sh);
+                        uint32_t vj = __shfl_up_sync(FULL, s_jsm[q], sh);
+                        if (q > 0) {
+                            const int qq = q > 0 ? q - 1 : 0, sl = (lane + 32 - sh) & 31;
+                            const uint32_t yp = __shfl_sync(FULL, s_pm[qq], sl), ys = __shfl_sync(FULL, s_ser[qq], sl);
+                            const uint32_t yj = __shfl_sync(FULL, s_jsm[qq], sl);
+                            vp = (lane < sh) ? yp : vp; vs = (lane < sh) ? ys : vs; vj = (lane < sh) ? yj : vj;
+                        }
+                        const int Pp = 32 * q + lane;
+                        const bool live = Pp < total, isC = Pp < nc;
+                        s_pm[q] = !live ? EMPTY : (isC ? cpm : vp);
+                        s_ser[q] = !live ? EMPTY : (isC ? ser0 + (uint32_t)lane : vs);
+                        s_jsm[q] = (live && isC) ? (jb | ((my_m ^ (uint32_t)m0) << 21)) : vj;
+                    }
+                    nS = total;
+                } else
+#endif
+                {
                 const uint32_t c3 = __shfl_sync(FULL, cpm, 3);
                 uint32_t Mw[SL];
 #pragma unroll
@@ -1502,6 +1562,7 @@ fsscs_decode_kernel(const DecodeParams P) {
                     s_jsm[w] = isC ? (jb | ((mk ^ (uint32_t)m0) << 21)) : gjsm;
                 }
                 nS = total;
+                }
             } else if (SORTED) {
                 // merge the candidates into the sorted stack, keeping the D smallest
                 // keys.  Equivalent to c1 always + siblings while |S| < D + strict-PM
@@ -1512,6 +1573,26 @@ fsscs_decode_kernel(const DecodeParams P) {
                 // candidate keys; lanes nc..7 hold EMPTY (above every live key)
                 const uint32_t cpm = (lane < nc) ? __float_as_uint(p_pm + my_d) : EMPTY;
                 const uint32_t epm = s_pm[0];
+                // every candidate ahead of every entry (the search continues along
+                // the best path: the common case): candidates take positions
+                // 0..nc-1, the entries shift up by nc - 1
+#if POLAR_MERGE_FAST
+                const uint32_t e1 = __shfl_sync(FULL, epm, 1), clast = __shfl_sync(FULL, cpm, (nc - 1) & 7);
+                if (clast < e1) {
+                    const int total = min(D, nS + nc);
+                    if (min(nc, D) > 1) write_fork_snapshot(-1, -1);
+                    const uint32_t jb = jsm_make(jn, fslot >= 0 ? (uint32_t)fslot : SNAP_NONE, 0);
+                    const int sh = nc - 1;
+                    const uint32_t upm = __shfl_up_sync(FULL, epm, sh), user = __shfl_up_sync(FULL, s_ser[0], sh);
+                    const uint32_t ujsm = __shfl_up_sync(FULL, s_jsm[0], sh);
+                    const bool live = lane < total, isC = lane < nc;
+                    s_pm[0] = !live ? EMPTY : (isC ? cpm : upm);
+                    s_ser[0] = !live ? EMPTY : (isC ? ser0 + (uint32_t)lane : user);
+                    s_jsm[0] = (live && isC) ? (jb | ((my_m ^ (uint32_t)m0) << 21)) : ujsm;
+                    nS = total;
+                } else
+#endif
+                {
                 // a = #{t < nc : cpm_t < epm} (candidate keys ascend: binary search
                 // over 8 slots, no branch on nc)
                 int a = 0;
@@ -1541,6 +1622,7 @@ fsscs_decode_kernel(const DecodeParams P) {
                 const bool isC = live && !isE;
                 s_jsm[0] = isC ? (jb | ((mk ^ (uint32_t)m0) << 21)) : gjsm;
                 nS = total;
+                }
             } else if (BIG) {
                 const uint32_t jbase = PK::make(jn, (nfit == 1) ? PK::NONE : (uint32_t)fslot, 0);
                 // c1 refills the hole left by p (if any), the siblings are appended
