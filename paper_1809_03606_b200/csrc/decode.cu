@@ -297,12 +297,18 @@ __device__ __forceinline__ int alloc_snapshot_big(uint32_t *used, int &uhint, co
 #ifndef POLAR_MB_N11
 #define POLAR_MB_N11 7         // CTAs per SM of the N = 2048 instances (7 x 29 KB shared memory fits)
 #endif
+#ifndef POLAR_MB_N12
+#define POLAR_MB_N12 6         // CTAs per SM of the N = 4096 instances (80 registers, no spill: C5 2874 -> 3038 Mbps; 7: 2900)
+#endif
+#ifndef POLAR_MB_BIG
+#define POLAR_MB_BIG kDecodeMinBlocks
+#endif
 #ifndef POLAR_MB_SL1
 #define POLAR_MB_SL1 kDecodeMinBlocks
 #endif
 template <int SLOTS, int NL, bool NOCRC>
 constexpr int kDecodeMinBlocksFor() {
-    return NL == 11 ? POLAR_MB_N11 : (NL == 12 ? 5 : (SLOTS == 4 ? 3 : (SLOTS == 2 ? 5 : (NOCRC && SLOTS == 1 ? POLAR_MB_PLAIN : (SLOTS == 1 ? POLAR_MB_SL1 : kDecodeMinBlocks)))));
+    return NL == 11 ? POLAR_MB_N11 : (NL == 12 ? POLAR_MB_N12 : (SLOTS == 4 ? 3 : (SLOTS == 2 ? 5 : (NOCRC && SLOTS == 1 ? POLAR_MB_PLAIN : (SLOTS == 1 ? POLAR_MB_SL1 : (SLOTS == 0 ? POLAR_MB_BIG : kDecodeMinBlocks))))));
 }
 
 // SLOTS = 1, 2, 4: register stack of 32 SLOTS entries (D <= 128).  SLOTS = 0:
