@@ -43,6 +43,12 @@ namespace polar {
 #ifndef POLAR_SNAP_SOFT
 #define POLAR_SNAP_SOFT 32     // snapshot slots above this trigger an exact recount (lazy bitmaps); 1 << 30: never
 #endif
+#ifndef POLAR_CONST_AW
+#define POLAR_CONST_AW 1       // specialised kernels: the alpha area's size as a compile-time constant
+#endif
+#ifndef POLAR_LEAN_WATCHDOG
+#define POLAR_LEAN_WATCHDOG 1  // specialised (MODE >= 1) kernels: no pop-count watchdog
+#endif
 #ifndef POLAR_BWPL
 #define POLAR_BWPL 1           // register stages below 5 read the left sibling's beta from one shuffled word
 #endif
@@ -375,7 +381,8 @@ fsscs_decode_kernel(const DecodeParams P) {
     const bool snap_sm = CNT ? (P.snap_in_smem != 0) : SNAP_SMEM;
     float *chan_s = reinterpret_cast<float *>(wb + P.win_words);   // channel row (chan_sm)
     float *alpha = chan_sm ? chan_s + N : chan_s;                  // stages >= 6 (+ scratch)
-    uint32_t *beta = reinterpret_cast<uint32_t *>(alpha + P.alpha_words);
+    // (code-length-specialised kernels without the L2 arena: alpha_words = N, a constant)
+    uint32_t *beta = reinterpret_cast<uint32_t *>(alpha + ((POLAR_CONST_AW && NL > 0 && !GA && !CNT) ? (1 << NL) : P.alpha_words));
     // stage t lives at [2^t, 2^{t+1}) of the shared alpha memory, or of this
     // warp's global (L2) arena for t >= sg (sg = n: everything in shared memory)
     const int sg = P.sg;
@@ -484,7 +491,9 @@ fsscs_decode_kernel(const DecodeParams P) {
 
         #pragma unroll 1
         for (;;) {
-            if (nS == 0 || pops >= pop_cap) {
+            // (the watchdog cannot fire: cnt[j] <= L bounds the pops by L (M + 1);
+            // the specialised kernels leave it out)
+            if (nS == 0 || ((MODE == 0 || !POLAR_LEAN_WATCHDOG) && pops >= pop_cap)) {
                 if (nS == 0) { from_best = true; out_pm = best_pm; status = 1; }   // reading R13
                 else { status = 2; out_pm = -1.f; }        // watchdog: cannot happen (cnt[j] <= L)
                 break;
