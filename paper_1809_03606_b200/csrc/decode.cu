@@ -1009,32 +1009,6 @@ fsscs_decode_kernel(const DecodeParams P) {
                 int s_min = max(max(lev_mem, bitlen((uint32_t)(pos_mem ^ pl))), max(s_d, l + 1));
                 s_min = min(s_min, n);
                 const int s_hi = s_min - 1;
-                if constexpr (NL > 0) {
-                    // shared-memory stages with compile-time sizes: enter at s_hi
-#define POLAR_SSTAGE(T)                                                                       \
-    if constexpr ((T) < NL && (T) >= 6) {                                                     \
-        if ((T) < lam) break;                                                                 \
-        if constexpr (CNT) c_fg += 1u << (T);                                                 \
-        alpha_stage<CHAN_SMEM, ((NL == 10 && SLOTS == 1) || (NL == 11 && POLAR_UNR_BIG)), BREG>((T) + 1 == n ? chan : SP((T) + 1), SP(T), beta, bw, n, (T), pl >> (T), lane); \
-    }
-                    switch (s_hi) {
-                    case 12: POLAR_SSTAGE(12)
-                    case 11: POLAR_SSTAGE(11)
-                    case 10: POLAR_SSTAGE(10)
-                    case 9: POLAR_SSTAGE(9)
-                    case 8: POLAR_SSTAGE(8)
-                    case 7: POLAR_SSTAGE(7)
-                    case 6: POLAR_SSTAGE(6)
-                    default: break;
-                    }
-#undef POLAR_SSTAGE
-                } else {
-                    #pragma unroll 1
-                    for (int s = s_hi; s >= max(lam, 6); s--) {
-                        if constexpr (CNT) c_fg += 1u << s;
-                        alpha_stage<CHAN_SMEM>(s + 1 == n ? chan : SP(s + 1), SP(s), beta, 0u, n, s, pl >> s, lane);
-                    }
-                }
                 // register stages (Lambda <= 32): lo = element i, hi = element i + Lambda
                 // by shuffle; enter the cascade at the first stage to compute, leave
                 // after the node's own stage (its value is the node input xr)
@@ -1067,11 +1041,27 @@ fsscs_decode_kernel(const DecodeParams P) {
         if constexpr (CNT) c_fg += Lt;                                                     \
         if (lam == (T)) break;                                                             \
     }
-                if (lam <= 5) {
-                    // register beta: the left siblings of the stages below 5 lie in
-                    // node j's own word (psi odd puts bit T of pl, T <= 4, inside it)
-                    const uint32_t bw_pl = (BREG && POLAR_BWPL) ? __shfl_sync(FULL, bw, pl >> 5) : 0u;
-                    switch (min(s_hi, 5)) {
+                // register beta: the left siblings of the stages below 5 lie in node
+                // j's own word (psi odd puts bit T of pl, T <= 4, inside it)
+                const uint32_t bw_pl = (BREG && POLAR_BWPL && lam <= 5) ? __shfl_sync(FULL, bw, pl >> 5) : 0u;
+                if constexpr (NL > 0) {
+                    // shared-memory stages with compile-time sizes, then the register
+                    // stages, in one cascade entered at s_hi
+#define POLAR_SSTAGE(T)                                                                       \
+    if constexpr ((T) < NL && (T) >= 6) {                                                     \
+        if ((T) < lam) break;                                                                 \
+        if constexpr (CNT) c_fg += 1u << (T);                                                 \
+        alpha_stage<CHAN_SMEM, ((NL == 10 && SLOTS == 1) || (NL == 11 && POLAR_UNR_BIG)), BREG>((T) + 1 == n ? chan : SP((T) + 1), SP(T), beta, bw, n, (T), pl >> (T), lane); \
+    }
+                    switch (s_hi) {
+                    case 12: POLAR_SSTAGE(12)
+                    case 11: POLAR_SSTAGE(11)
+                    case 10: POLAR_SSTAGE(10)
+                    case 9: POLAR_SSTAGE(9)
+                    case 8: POLAR_SSTAGE(8)
+                    case 7: POLAR_SSTAGE(7)
+                    case 6: POLAR_SSTAGE(6)
+                        if (lam > 5) break;
                     case 5: POLAR_RSTAGE(5)
                     case 4: POLAR_RSTAGE(4)
                     case 3: POLAR_RSTAGE(3)
@@ -1079,6 +1069,24 @@ fsscs_decode_kernel(const DecodeParams P) {
                     case 1: POLAR_RSTAGE(1)
                     case 0: POLAR_RSTAGE(0)
                     default: break;
+                    }
+#undef POLAR_SSTAGE
+                } else {
+                    #pragma unroll 1
+                    for (int s = s_hi; s >= max(lam, 6); s--) {
+                        if constexpr (CNT) c_fg += 1u << s;
+                        alpha_stage<CHAN_SMEM>(s + 1 == n ? chan : SP(s + 1), SP(s), beta, 0u, n, s, pl >> s, lane);
+                    }
+                    if (lam <= 5) {
+                        switch (min(s_hi, 5)) {
+                        case 5: POLAR_RSTAGE(5)
+                        case 4: POLAR_RSTAGE(4)
+                        case 3: POLAR_RSTAGE(3)
+                        case 2: POLAR_RSTAGE(2)
+                        case 1: POLAR_RSTAGE(1)
+                        case 0: POLAR_RSTAGE(0)
+                        default: break;
+                        }
                     }
                 }
 #undef POLAR_RSTAGE
