@@ -49,6 +49,9 @@ namespace polar {
 #ifndef POLAR_LEAN_WATCHDOG
 #define POLAR_LEAN_WATCHDOG 1  // specialised (MODE >= 1) kernels: no pop-count watchdog
 #endif
+#ifndef POLAR_PREFETCH_SNAP
+#define POLAR_PREFETCH_SNAP 0  // register beta: the switch's snapshot load issued right after the pop (measured slower: C2 6931 -> 6908, P 3012 -> 2965)
+#endif
 #ifndef POLAR_BWPL
 #define POLAR_BWPL 1           // register stages below 5 read the left sibling's beta from one shuffled word
 #endif
@@ -637,6 +640,14 @@ fsscs_decode_kernel(const DecodeParams P) {
             pops++;
             const float p_pm = __uint_as_float(mpm);
             const uint32_t p_ser = mser;
+            // register beta: a switch restores p's fork snapshot; its load is issued
+            // here, ahead of the counter, prune and record reads (the slot holds nw
+            // words, so every lane's word is in bounds)
+            uint32_t pre_nv = 0;
+            if (BREG && POLAR_PREFETCH_SNAP && p_ser != work && lane < nw) {
+                const uint32_t *ps_src = snap_slot((int)PK::snap(p_jsm));
+                pre_nv = snap_sm ? ps_src[lane] : __ldcg(ps_src + lane);
+            }
             const int j = (int)jsm_j(p_jsm);
 #ifdef POLAR_TRACE_FRAME
             if (f == POLAR_TRACE_FRAME && lane == 0)
@@ -821,7 +832,7 @@ fsscs_decode_kernel(const DecodeParams P) {
                 if (BREG) {
                     uint32_t x = 0;
                     if (lane < nwords) {
-                        const uint32_t nv = snap_sm ? src[lane] : __ldcg(src + lane);
+                        const uint32_t nv = POLAR_PREFETCH_SNAP ? pre_nv : (snap_sm ? src[lane] : __ldcg(src + lane));
                         x = nv ^ bw;
                         if (lane == nwords - 1 && (pl & 31)) x &= (1u << (pl & 31)) - 1u;
                         bw = nv;
