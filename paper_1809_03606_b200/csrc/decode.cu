@@ -52,6 +52,14 @@ namespace polar {
 #ifndef POLAR_PREFETCH_SNAP
 #define POLAR_PREFETCH_SNAP 0  // register beta: the switch's snapshot load issued right after the pop (measured slower: C2 6931 -> 6908, P 3012 -> 2965)
 #endif
+#ifndef POLAR_NOSER
+#define POLAR_NOSER 0          // sorted 32-entry register stacks (D <= 32) without serials: the order is the
+                               // position (candidates carry the largest serials, so they follow equal PMs),
+                               // the working path is a flag bit in its entry's jsm word (A/B)
+#endif
+#ifndef POLAR_SUM_FULL
+#define POLAR_SUM_FULL 0       // R0 / REP nodes with Lambda <= 32: the full five-level shuffle tree, unrolled (A/B)
+#endif
 #ifndef POLAR_BWPL
 #define POLAR_BWPL 1           // register stages below 5 read the left sibling's beta from one shuffled word
 #endif
@@ -348,6 +356,11 @@ fsscs_decode_kernel(const DecodeParams P) {
     // words) lives in registers, word w in lane w (bw); beta[] in shared memory
     // only stages the output
     constexpr bool BREG = (NL == 10 || NL == 7) && (POLAR_BETA_REGS != 0);
+    // NOSER: no serial word per entry (sorted register stacks): an entry is
+    // live iff its PM word is not EMPTY (a NaN pattern no PM takes), and the
+    // working path's entry carries WFLAG in its jsm word
+    constexpr bool NOSER = SORTED && !BIG && (POLAR_NOSER != 0);
+    constexpr uint32_t WFLAG = 1u << 25;
     using PK = Pk<BIG>;
     extern __shared__ __align__(16) uint32_t smem[];
     const int lane = threadIdx.x & 31;
@@ -461,7 +474,7 @@ fsscs_decode_kernel(const DecodeParams P) {
         uint32_t s_pm[SL], s_ser[SL], s_jsm[SL];
 #pragma unroll
         for (int s = 0; s < SL; s++) { s_pm[s] = EMPTY; s_ser[s] = EMPTY; s_jsm[s] = PK::make(0, PK::NONE, 0); }
-        if (lane == 0) { s_pm[0] = 0u; s_ser[0] = 0u; }
+        if (lane == 0) { s_pm[0] = 0u; s_ser[0] = 0u; if (NOSER) s_jsm[0] |= WFLAG; }
         int nS = 1;
         int uhint = 0;
         int widx = 0;                     // BIG: index of the working path's entry (-1: not live)
@@ -612,7 +625,7 @@ fsscs_decode_kernel(const DecodeParams P) {
             if (SORTED) {
                 // the sorted stack's head (lane 0) is the best path
                 mpm = __shfl_sync(FULL, s_pm[0], 0);
-                mser = __shfl_sync(FULL, s_ser[0], 0);
+                mser = NOSER ? 0u : __shfl_sync(FULL, s_ser[0], 0);
             } else {
                 warp_min_key(lpm, lser, mpm, mser);
                 owner = __ffs(__ballot_sync(FULL, lpm == mpm && lser == mser)) - 1;
@@ -640,11 +653,12 @@ fsscs_decode_kernel(const DecodeParams P) {
             pops++;
             const float p_pm = __uint_as_float(mpm);
             const uint32_t p_ser = mser;
+            const bool sw = NOSER ? ((p_jsm & WFLAG) == 0u) : (p_ser != work);   // p is not the working path
             // register beta: a switch restores p's fork snapshot; its load is issued
             // here, ahead of the counter, prune and record reads (the slot holds nw
             // words, so every lane's word is in bounds)
             uint32_t pre_nv = 0;
-            if (BREG && POLAR_PREFETCH_SNAP && p_ser != work && lane < nw) {
+            if (BREG && POLAR_PREFETCH_SNAP && sw && lane < nw) {
                 const uint32_t *ps_src = snap_slot((int)PK::snap(p_jsm));
                 pre_nv = snap_sm ? ps_src[lane] : __ldcg(ps_src + lane);
             }
@@ -694,7 +708,7 @@ fsscs_decode_kernel(const DecodeParams P) {
                     cum[0] = 0;
 #pragma unroll
                     for (int q = 0; q < SL; q++) {
-                        kb[q] = __ballot_sync(FULL, s_ser[q] != EMPTY && (int)jsm_j(s_jsm[q]) > j);
+                        kb[q] = __ballot_sync(FULL, (NOSER ? s_pm[q] : s_ser[q]) != EMPTY && (int)jsm_j(s_jsm[q]) > j);
                         cum[q + 1] = cum[q] + __popc(kb[q]);
                     }
                     cntv = cum[SL];
@@ -717,7 +731,8 @@ fsscs_decode_kernel(const DecodeParams P) {
                         uint32_t gp = EMPTY, gs = EMPTY, gj = 0;
 #pragma unroll
                         for (int q = 0; q < SL; q++) {
-                            const uint32_t xp = __shfl_sync(FULL, s_pm[q], src), xs = __shfl_sync(FULL, s_ser[q], src);
+                            const uint32_t xp = __shfl_sync(FULL, s_pm[q], src);
+                            const uint32_t xs = NOSER ? 0u : __shfl_sync(FULL, s_ser[q], src);
                             const uint32_t xj = __shfl_sync(FULL, s_jsm[q], src);
                             gp = (v == q) ? xp : gp; gs = (v == q) ? xs : gs; gj = (v == q) ? xj : gj;
                         }
@@ -730,7 +745,7 @@ fsscs_decode_kernel(const DecodeParams P) {
                 } else if (SORTED) {
                     // survivors (depth > j) move to lanes 1..cntv in order (a subset
                     // of a sorted list is sorted); lane 0 stays free
-                    const uint32_t kb = __ballot_sync(FULL, s_ser[0] != EMPTY && (int)jsm_j(s_jsm[0]) > j);
+                    const uint32_t kb = __ballot_sync(FULL, (NOSER ? s_pm[0] : s_ser[0]) != EMPTY && (int)jsm_j(s_jsm[0]) > j);
                     cntv = __popc(kb);
                     const bool dst = (lane >= 1 && lane <= cntv);
                     // source lane = position of the lane-th set bit of kb (binary search on prefix counts)
@@ -740,10 +755,13 @@ fsscs_decode_kernel(const DecodeParams P) {
                         const int hi = src + st - 1;                  // bits [0, hi] hold fewer than `lane` survivors?
                         if (__popc(kb & (hi >= 31 ? FULL : ((2u << hi) - 1u))) < lane) src += st;
                     }
-                    const uint32_t npm = __shfl_sync(FULL, s_pm[0], src), nser = __shfl_sync(FULL, s_ser[0], src);
+                    const uint32_t npm = __shfl_sync(FULL, s_pm[0], src);
                     const uint32_t njsm = __shfl_sync(FULL, s_jsm[0], src);
                     s_pm[0] = dst ? npm : EMPTY;
-                    s_ser[0] = dst ? nser : EMPTY;
+                    if constexpr (!NOSER) {
+                        const uint32_t nser = __shfl_sync(FULL, s_ser[0], src);
+                        s_ser[0] = dst ? nser : EMPTY;
+                    }
                     s_jsm[0] = njsm;
                 } else {
 #pragma unroll
@@ -768,7 +786,7 @@ fsscs_decode_kernel(const DecodeParams P) {
 
             // ---- path switch ---------------------
             int s_d = 0;
-            if (p_ser != work) {
+            if (sw) {
                 switches++;
                 // the path being left keeps its beta in a snapshot if it is still live
                 if (BIG) {
@@ -793,7 +811,8 @@ fsscs_decode_kernel(const DecodeParams P) {
                 }
                 int wsl = -1;
 #pragma unroll
-                for (int s = 0; s < SL; s++) if (!GSCAN && s_ser[s] == work) wsl = s;
+                for (int s = 0; s < SL; s++)
+                    if (!GSCAN && (NOSER ? (s_pm[s] != EMPTY && (s_jsm[s] & WFLAG) != 0u) : (s_ser[s] == work))) wsl = s;
                 const uint32_t wb_ = __ballot_sync(FULL, wsl >= 0);
                 if (!GSCAN && wb_) {
                     const int wl = __ffs(wb_) - 1;
@@ -806,7 +825,7 @@ fsscs_decode_kernel(const DecodeParams P) {
                         int slot;
                         if constexpr (HOT) slot = alloc_snapshot_big(snap_used, uhint, sjsm, nA, D, -1, PK::snap(p_jsm), lane,
                                                                      true, s_ser[0], s_jsm[0]);
-                        else slot = alloc_snapshot_lazy<SL>(snap_used, s_ser, s_jsm, D, -1, 0, jsm_snap(p_jsm), lane, nS);
+                        else slot = alloc_snapshot_lazy<SL>(snap_used, NOSER ? s_pm : s_ser, s_jsm, D, -1, 0, jsm_snap(p_jsm), lane, nS);
                         uint32_t *dst = snap_slot(slot);
                         const int nwords = (work_pl + 31) >> 5;
                         if constexpr (CNT) c_sw += (uint32_t)nwords;
@@ -821,6 +840,10 @@ fsscs_decode_kernel(const DecodeParams P) {
                                 if (s == wslot) s_jsm[s] = PK::make(PK::j(wj), (uint32_t)slot, 0);
                         }
                     }
+                }
+                if (NOSER) {                          // the path being left is no longer the working path
+#pragma unroll
+                    for (int s = 0; s < SL; s++) s_jsm[s] &= ~WFLAG;
                 }
                 // restore p's beta (fork snapshot), locating the first bit d where it
                 // differs from the beta the alpha memory was computed from
@@ -987,12 +1010,13 @@ fsscs_decode_kernel(const DecodeParams P) {
                     // 0..nS-1 (before the exit test too, for the same reason as the copy)
 #pragma unroll
                     for (int q = 0; q < SL; q++) {
-                        const uint32_t dp = __shfl_down_sync(FULL, s_pm[q], 1), ds = __shfl_down_sync(FULL, s_ser[q], 1);
+                        const uint32_t dp = __shfl_down_sync(FULL, s_pm[q], 1);
+                        const uint32_t ds = NOSER ? 0u : __shfl_down_sync(FULL, s_ser[q], 1);
                         const uint32_t dj = __shfl_down_sync(FULL, s_jsm[q], 1);
                         uint32_t up = EMPTY, us = EMPTY, uj = 0;
                         if (q + 1 < SL) {
                             up = __shfl_sync(FULL, s_pm[q + 1 < SL ? q + 1 : q], 0);
-                            us = __shfl_sync(FULL, s_ser[q + 1 < SL ? q + 1 : q], 0);
+                            us = NOSER ? 0u : __shfl_sync(FULL, s_ser[q + 1 < SL ? q + 1 : q], 0);
                             uj = __shfl_sync(FULL, s_jsm[q + 1 < SL ? q + 1 : q], 0);
                         }
                         s_pm[q] = (lane == 31) ? up : dp;
@@ -1174,11 +1198,21 @@ fsscs_decode_kernel(const DecodeParams P) {
                 } else {
                     vn = negpart(xr);
                     vp = pospart(xr);
+#if POLAR_SUM_FULL
+                    // lanes >= Lambda hold +0 and x + 0 = x exactly, so the full
+                    // five-level tree equals the Lambda-element tree-order sum
+#pragma unroll
+                    for (int h = 16; h >= 1; h >>= 1) {
+                        vn += __shfl_down_sync(FULL, vn, h);
+                        if (rep) vp += __shfl_down_sync(FULL, vp, h);
+                    }
+#else
                     #pragma unroll 1
                     for (int h = Lam >> 1; h >= 1; h >>= 1) {
                         vn += __shfl_down_sync(FULL, vn, h);
                         if (rep) vp += __shfl_down_sync(FULL, vp, h);
                     }
+#endif
                 }
                 vn = __shfl_sync(FULL, vn, 0);
                 vp = __shfl_sync(FULL, vp, 0);
@@ -1324,7 +1358,7 @@ fsscs_decode_kernel(const DecodeParams P) {
             auto write_fork_snapshot = [&](int victim_lane, int victim_slot) {
                 if (BIG) fslot = alloc_snapshot_big(snap_used, uhint, sjsm, nA, D, hole >= 0 ? hole : victim_slot, PK::NONE, lane,
                                                     HOT, s_ser[0], s_jsm[0]);
-                else fslot = alloc_snapshot_lazy<SL>(snap_used, s_ser, s_jsm, D, victim_lane, victim_slot, SNAP_NONE, lane, nS);
+                else fslot = alloc_snapshot_lazy<SL>(snap_used, NOSER ? s_pm : s_ser, s_jsm, D, victim_lane, victim_slot, SNAP_NONE, lane, nS);
                 uint32_t *dst = snap_slot(fslot);
                 const int nwords = (npl + 31) >> 5;
                 if constexpr (CNT) c_sw += (uint32_t)nwords;
@@ -1572,16 +1606,16 @@ fsscs_decode_kernel(const DecodeParams P) {
                     const bool isE = (Mw[w] >> lane) & 1u;
                     const int t = (P - q) & 7;                                   // candidate at position P
                     const int src = q + 1, sv = src >> 5, sl = src & 31;
-                    uint32_t gpm = __shfl_sync(FULL, s_pm[w], sl), gser = __shfl_sync(FULL, s_ser[w], sl);
+                    uint32_t gpm = __shfl_sync(FULL, s_pm[w], sl), gser = NOSER ? 0u : __shfl_sync(FULL, s_ser[w], sl);
                     uint32_t gjsm = __shfl_sync(FULL, s_jsm[w], sl);
                     if (w > 0) {
-                        const uint32_t xp = __shfl_sync(FULL, opm, sl), xs = __shfl_sync(FULL, oser, sl);
+                        const uint32_t xp = __shfl_sync(FULL, opm, sl), xs = NOSER ? 0u : __shfl_sync(FULL, oser, sl);
                         const uint32_t xj = __shfl_sync(FULL, ojsm, sl);
                         gpm = (sv == w - 1) ? xp : gpm; gser = (sv == w - 1) ? xs : gser; gjsm = (sv == w - 1) ? xj : gjsm;
                     }
                     if (w + 1 < SL) {
                         const int w1 = (w + 1 < SL) ? w + 1 : w;
-                        const uint32_t xp = __shfl_sync(FULL, s_pm[w1], 0), xs = __shfl_sync(FULL, s_ser[w1], 0);
+                        const uint32_t xp = __shfl_sync(FULL, s_pm[w1], 0), xs = NOSER ? 0u : __shfl_sync(FULL, s_ser[w1], 0);
                         const uint32_t xj = __shfl_sync(FULL, s_jsm[w1], 0);
                         gpm = (sv == w + 1) ? xp : gpm; gser = (sv == w + 1) ? xs : gser; gjsm = (sv == w + 1) ? xj : gjsm;
                     }
@@ -1591,9 +1625,9 @@ fsscs_decode_kernel(const DecodeParams P) {
                     const uint32_t mk = (clist >> (4 * t)) & 15u;
                     opm = s_pm[w]; oser = s_ser[w]; ojsm = s_jsm[w];
                     s_pm[w] = !live ? EMPTY : (isE ? gpm : ct);
-                    s_ser[w] = !live ? EMPTY : (isE ? gser : ser0 + (uint32_t)t);
+                    if constexpr (!NOSER) s_ser[w] = !live ? EMPTY : (isE ? gser : ser0 + (uint32_t)t);
                     const bool isC = live && !isE;
-                    s_jsm[w] = isC ? (jb | ((mk ^ (uint32_t)m0) << 21)) : gjsm;
+                    s_jsm[w] = isC ? (jb | ((mk ^ (uint32_t)m0) << 21) | (NOSER ? ((uint32_t)(t - 1) & WFLAG) : 0u)) : gjsm;
                 }
                 nS = total;
                 }
@@ -1646,15 +1680,17 @@ fsscs_decode_kernel(const DecodeParams P) {
                 const int q = __popc(Mp & ((1u << lane) - 1u));      // entries before position lane
                 const bool isE = (Mp >> lane) & 1u;
                 const int t = (lane - q) & 7;                       // candidate at position lane
-                const uint32_t gpm = __shfl_sync(FULL, epm, q + 1), gser = __shfl_sync(FULL, s_ser[0], q + 1);
+                const uint32_t gpm = __shfl_sync(FULL, epm, q + 1);
+                const uint32_t gser = NOSER ? 0u : __shfl_sync(FULL, s_ser[0], q + 1);
                 const uint32_t gjsm = __shfl_sync(FULL, s_jsm[0], q + 1);
                 const uint32_t ct = __shfl_sync(FULL, cpm, t);      // candidate t's PM bits
                 const bool live = lane < total;
                 const uint32_t mk = (clist >> (4 * t)) & 15u;
                 s_pm[0] = !live ? EMPTY : (isE ? gpm : ct);
-                s_ser[0] = !live ? EMPTY : (isE ? gser : ser0 + (uint32_t)t);
+                if constexpr (!NOSER) s_ser[0] = !live ? EMPTY : (isE ? gser : ser0 + (uint32_t)t);
                 const bool isC = live && !isE;
-                s_jsm[0] = isC ? (jb | ((mk ^ (uint32_t)m0) << 21)) : gjsm;
+                // (NOSER: candidate 0 = c1 becomes the working path: t - 1 = all ones only for t = 0)
+                s_jsm[0] = isC ? (jb | ((mk ^ (uint32_t)m0) << 21) | (NOSER ? ((uint32_t)(t - 1) & WFLAG) : 0u)) : gjsm;
                 nS = total;
                 }
             } else if (BIG) {

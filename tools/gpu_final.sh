@@ -18,6 +18,4 @@ timeout 900 $NCU -k regex:fsscs_decode -o $O/prof_P python bench.py --config P -
 timeout 900 $NCU -k regex:fsscl -o $O/prof_C2_list python bench.py --list --frames 20000 --steps 1 --warmup 3 --no-e2e --no-cpu > $O/ncu_C2_list.log 2>&1
 timeout 900 $NCU -k regex:fsscl -o $O/prof_C5_list python bench.py --config C5 --list --frames 20000 --steps 1 --warmup 3 --no-e2e --no-cpu > $O/ncu_C5_list.log 2>&1
 echo done >> $O/status.txt
-# every frame of every config's timed workload through the oracle (C5: 2 M frames, ~18 min of host time)
-timeout 3000 python tools/full_parity.py C1 C2 C3 C4 P C5 > $O/full_parity.jsonl 2> $O/full_parity.err
-echo full_parity=$? >> $O/status.txt
+# all-frame oracle parity of every config: tools/gpu_full_parity.sh (a separate call: ~30 min of host time)
