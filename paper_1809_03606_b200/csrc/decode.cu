@@ -57,6 +57,9 @@ namespace polar {
                                // position (candidates carry the largest serials, so they follow equal PMs),
                                // the working path is a flag bit in its entry's jsm word (A/B)
 #endif
+#ifndef POLAR_R0_FAST
+#define POLAR_R0_FAST 0        // sorted register stacks: an R0 node's single candidate inserted by one shift (A/B)
+#endif
 #ifndef POLAR_SUM_FULL
 #define POLAR_SUM_FULL 0       // R0 / REP nodes with Lambda <= 32: the full five-level shuffle tree, unrolled (A/B)
 #endif
@@ -1538,6 +1541,33 @@ fsscs_decode_kernel(const DecodeParams P) {
                     nS--;
                 }
                 if (nA == 0) cb = ~0ull;
+            } else if (SORTED && POLAR_R0_FAST && kind == OP_R0) {
+                // one candidate (an R0 node), no sibling, no fork snapshot: the entries
+                // whose PM is not above the candidate's (a prefix 1..k of the sorted
+                // positions; ties keep the entry first, its serial is smaller) move
+                // down by one, the candidate takes position k, the rest stay.  nS < D
+                // after the pop, so nothing is dropped.
+                const uint32_t c = __float_as_uint(p_pm + vn);     // (vn is warp-uniform)
+                int k = 0;
+#pragma unroll
+                for (int q = 0; q < SL; q++) k += __popc(__ballot_sync(FULL, s_pm[q] <= c));   // dead entries hold EMPTY
+                const uint32_t cj = PK::make(jn, PK::NONE, 0) | (NOSER ? WFLAG : 0u);
+#pragma unroll
+                for (int q = 0; q < SL; q++) {
+                    uint32_t np = __shfl_down_sync(FULL, s_pm[q], 1), nj = __shfl_down_sync(FULL, s_jsm[q], 1);
+                    uint32_t ns = NOSER ? 0u : __shfl_down_sync(FULL, s_ser[q], 1);
+                    if (q + 1 < SL) {
+                        const int q1 = (q + 1 < SL) ? q + 1 : q;
+                        const uint32_t up = __shfl_sync(FULL, s_pm[q1], 0), uj = __shfl_sync(FULL, s_jsm[q1], 0);
+                        const uint32_t us = NOSER ? 0u : __shfl_sync(FULL, s_ser[q1], 0);
+                        np = (lane == 31) ? up : np; nj = (lane == 31) ? uj : nj; ns = (lane == 31) ? us : ns;
+                    }
+                    const int Pp = 32 * q + lane;
+                    s_pm[q] = (Pp < k) ? np : ((Pp == k) ? c : s_pm[q]);
+                    s_jsm[q] = (Pp < k) ? nj : ((Pp == k) ? cj : s_jsm[q]);
+                    if constexpr (!NOSER) s_ser[q] = (Pp < k) ? ns : ((Pp == k) ? ser0 : s_ser[q]);
+                }
+                nS++;
             } else if (SORTED && SL > 1) {
                 // the same merge over SL slots (position p = 32 s + lane): entry p
                 // moves to p - 1 + a_p, which stays in slots s - 1 .. s + 1

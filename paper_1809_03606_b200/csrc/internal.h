@@ -86,8 +86,8 @@ struct DecodeParams {
     int chan_in_smem, snap_in_smem;   // placement (read by the counting instance only)
 };
 
-// Kernel parameter block of the FSSCL list decoder (list.cu).  One CTA of
-// L warps per frame; the shared-memory offsets (in 32-bit words) are computed
+// Kernel parameter block of the FSSCL list decoder (list_packed.cu).  One warp
+// per frame; the shared-memory offsets (in 32-bit words) are computed
 // by the host (capi.cu, list_layout).
 struct ListParams {
     const float *llr;

@@ -2,9 +2,9 @@
 // paths of the list live in one warp (§2.2.3-2.2.4; list
 // memory with lazy copy, §3.2).
 //
-// The CTA kernel of list.cu gives every path its own warp; most decision nodes
+// A kernel with one warp per path (round 1's list.cu, removed) idles: most decision nodes
 // of a fast-simplified schedule are small (Lambda <= 4 for most of them), so
-// those warps idle on 28+ lanes and pay two CTA barriers per node.  Here the
+// such warps idle on 28+ lanes and pay two CTA barriers per node.  Here the
 // lanes are spread over (path, element) pairs instead: a stage or node of
 // size Lambda <= 32 processes 32 / Lambda paths per warp instruction (node
 // reductions become segmented shuffles inside lane groups of Lambda lanes),
