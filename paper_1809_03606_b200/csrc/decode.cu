@@ -60,6 +60,9 @@ namespace polar {
 #ifndef POLAR_R0_FAST
 #define POLAR_R0_FAST 0        // sorted register stacks: an R0 node's single candidate inserted by one shift (A/B)
 #endif
+#ifndef POLAR_REP_FAST
+#define POLAR_REP_FAST 0       // sorted register stacks: a REP node's two uniform candidates inserted by shifts (A/B)
+#endif
 #ifndef POLAR_SUM_FULL
 #define POLAR_SUM_FULL 0       // R0 / REP nodes with Lambda <= 32: the full five-level shuffle tree, unrolled (A/B)
 #endif
@@ -1568,6 +1571,54 @@ fsscs_decode_kernel(const DecodeParams P) {
                     if constexpr (!NOSER) s_ser[q] = (Pp < k) ? ns : ((Pp == k) ? ser0 : s_ser[q]);
                 }
                 nS++;
+            } else if (SORTED && POLAR_REP_FAST && kind == OP_REP) {
+                // two warp-uniform candidates c0 <= c1 (a REP node: all zeros / all ones).
+                // k0, k1 = the entries not above c0, c1 (prefixes of the sorted
+                // positions 1..nS).  New position P takes: old P + 1 for P < k0, c0 at
+                // k0, old P for k0 < P <= k1, c1 at k1 + 1, old P - 1 above; positions
+                // >= min(D, nS + 2) are dropped (c1 survives iff k1 + 1 < D).
+                const uint32_t m0u = clist & 15u;
+                const uint32_t c0 = __float_as_uint(p_pm + (m0u ? vp : vn)), c1 = __float_as_uint(p_pm + (m0u ? vn : vp));
+                int k0 = 0, k1 = 0;
+#pragma unroll
+                for (int q = 0; q < SL; q++) {
+                    k0 += __popc(__ballot_sync(FULL, s_pm[q] <= c0));      // dead entries hold EMPTY
+                    k1 += __popc(__ballot_sync(FULL, s_pm[q] <= c1));
+                }
+                const int total = min(D, nS + 2);
+                if (k1 + 1 < D) write_fork_snapshot(-1, -1);
+                const uint32_t jb = PK::make(jn, fslot >= 0 ? (uint32_t)fslot : PK::NONE, 0);
+                const uint32_t cj0 = jb | (NOSER ? WFLAG : 0u), cj1 = jb | (1u << PK::MSH);   // c1's flip: mask 0 ^ 1
+                uint32_t ppm = EMPTY, pjs = 0, pse = EMPTY;      // the previous slot's old words
+#pragma unroll
+                for (int q = 0; q < SL; q++) {
+                    const uint32_t opm = s_pm[q], ojs = s_jsm[q], ose = s_ser[q];
+                    uint32_t dp = __shfl_down_sync(FULL, opm, 1), dj = __shfl_down_sync(FULL, ojs, 1);
+                    uint32_t up = __shfl_up_sync(FULL, opm, 1), uj = __shfl_up_sync(FULL, ojs, 1);
+                    uint32_t ds = NOSER ? 0u : __shfl_down_sync(FULL, ose, 1), us = NOSER ? 0u : __shfl_up_sync(FULL, ose, 1);
+                    if (q + 1 < SL) {
+                        const int q1 = (q + 1 < SL) ? q + 1 : q;
+                        const uint32_t xp = __shfl_sync(FULL, s_pm[q1], 0), xj = __shfl_sync(FULL, s_jsm[q1], 0);
+                        const uint32_t xs = NOSER ? 0u : __shfl_sync(FULL, s_ser[q1], 0);
+                        dp = (lane == 31) ? xp : dp; dj = (lane == 31) ? xj : dj; ds = (lane == 31) ? xs : ds;
+                    }
+                    if (q > 0) {
+                        const uint32_t xp = __shfl_sync(FULL, ppm, 31), xj = __shfl_sync(FULL, pjs, 31);
+                        const uint32_t xs = NOSER ? 0u : __shfl_sync(FULL, pse, 31);
+                        up = (lane == 0) ? xp : up; uj = (lane == 0) ? xj : uj; us = (lane == 0) ? xs : us;
+                    }
+                    const int Pp = 32 * q + lane;
+                    const bool lo = Pp < k0, at0 = Pp == k0, mid = Pp <= k1, at1 = Pp == k1 + 1;
+                    const uint32_t vpm = lo ? dp : (at0 ? c0 : (mid ? opm : (at1 ? c1 : up)));
+                    s_pm[q] = (Pp < total) ? vpm : EMPTY;
+                    s_jsm[q] = lo ? dj : (at0 ? cj0 : (mid ? ojs : (at1 ? cj1 : uj)));
+                    if constexpr (!NOSER) {
+                        const uint32_t vs = lo ? ds : (at0 ? ser0 : (mid ? ose : (at1 ? ser0 + 1u : us)));
+                        s_ser[q] = (Pp < total) ? vs : EMPTY;
+                    }
+                    ppm = opm; pjs = ojs; pse = ose;
+                }
+                nS = total;
             } else if (SORTED && SL > 1) {
                 // the same merge over SL slots (position p = 32 s + lane): entry p
                 // moves to p - 1 + a_p, which stays in slots s - 1 .. s + 1

@@ -77,10 +77,40 @@ class PositionStack:
                 t += 1
         self.e = out
 
+    def _old(self, P):
+        """Entry at position P after the pop (positions 1..nS; 0 is the freed head)."""
+        return self.e[P - 1] if 1 <= P <= len(self.e) else None
+
+    def push_fast(self, ppm, dpm, depth):
+        """The kernel's shift forms for one (R0) or two (REP) warp-uniform candidates."""
+        nS, nc = len(self.e), len(dpm)
+        c = [ppm + d for d in dpm]
+        k = [sum(1 for x in self.e if x[0] <= ci) for ci in c]
+        total = min(self.D, nS + nc)
+        out = []
+        for P in range(total):
+            if nc == 1:
+                v = self._old(P + 1) if P < k[0] else ([c[0], depth, True] if P == k[0] else self._old(P))
+            else:
+                if P < k[0]:
+                    v = self._old(P + 1)
+                elif P == k[0]:
+                    v = [c[0], depth, True]
+                elif P <= k[1]:
+                    v = self._old(P)
+                elif P == k[1] + 1:
+                    v = [c[1], depth, False]
+                else:
+                    v = self._old(P - 1)
+            assert v is not None
+            out.append(v)
+        self.e = out
+
 
 @pytest.mark.parametrize("D", [1, 2, 5, 8, 32, 64, 128])
 @pytest.mark.parametrize("seed", range(6))
-def test_position_order_equals_pm_serial_order(D, seed):
+@pytest.mark.parametrize("fast", [False, True])
+def test_position_order_equals_pm_serial_order(D, seed, fast):
     rng = random.Random(1000 * D + seed)
     A, B = SerialStack(D), PositionStack(D)
     depth_max = 12
@@ -101,7 +131,10 @@ def test_position_order_equals_pm_serial_order(D, seed):
         # small integer increments: many equal PMs (the ties the serial breaks)
         dpm = sorted(rng.randrange(0, 3) for _ in range(nc))
         A.push(pm, dpm, dep + 1)
-        B.push(pm, dpm, dep + 1)
+        if nc <= 2 and fast:
+            B.push_fast(pm, dpm, dep + 1)
+        else:
+            B.push(pm, dpm, dep + 1)
         assert [(x[0], x[2]) for x in A.e] == [(x[0], x[1]) for x in B.e]
         # the flagged entry is the working path (when it is still live)
         flagged = [i for i, x in enumerate(B.e) if x[2]]
