@@ -53,18 +53,25 @@ namespace polar {
 #define POLAR_PREFETCH_SNAP 0  // register beta: the switch's snapshot load issued right after the pop (measured slower: C2 6931 -> 6908, P 3012 -> 2965)
 #endif
 #ifndef POLAR_NOSER
-#define POLAR_NOSER 0          // sorted 32-entry register stacks (D <= 32) without serials: the order is the
-                               // position (candidates carry the largest serials, so they follow equal PMs),
-                               // the working path is a flag bit in its entry's jsm word (A/B)
+#define POLAR_NOSER 0          // sorted register stacks without serial words: the order is the position
+                               // (candidates carry the largest serials, so they follow equal PMs), the working
+                               // path is a flag bit in its entry's jsm word.  Measured: C2 6942 -> 6956, C5 3117
+                               // -> 3156, C4 2326 -> 2290 Mbps; with POLAR_R0_FAST ptxas no longer proves the
+                               // CRC kernels' decode loop converged (C3 6490 -> 5956): not taken
 #endif
+// The next three: 0 off, 1 in the kernels where measured faster, 2 in every kernel (A/B and test builds)
 #ifndef POLAR_R0_FAST
-#define POLAR_R0_FAST 0        // sorted register stacks: an R0 node's single candidate inserted by one shift (A/B)
+#define POLAR_R0_FAST 1        // sorted register stacks: an R0 node's single candidate inserted by one shift
+                               // (n = 10, 11 kernels: C2 6937 -> 7113, C3 6480 -> 6661, C4 2326 -> 2394 Mbps with
+                               // POLAR_SUM_FULL; n = 12: C5 3122 -> 3052, n = 7: C1 -12%: left off there)
 #endif
 #ifndef POLAR_REP_FAST
-#define POLAR_REP_FAST 0       // sorted register stacks: a REP node's two uniform candidates inserted by shifts (A/B)
+#define POLAR_REP_FAST 1       // the same for a REP node's two warp-uniform candidates (n = 10 kernels: C2 7125
+                               // -> 7197; n = 11: C4 2394 -> 2338, n = 12: C5 3052 -> 2497: left off there)
 #endif
 #ifndef POLAR_SUM_FULL
-#define POLAR_SUM_FULL 0       // R0 / REP nodes with Lambda <= 32: the full five-level shuffle tree, unrolled (A/B)
+#define POLAR_SUM_FULL 1       // R0 / REP nodes with Lambda <= 32: the full five-level shuffle tree, unrolled
+                               // (n = 10, 11 kernels; C2 alone 6942 -> 6975)
 #endif
 #ifndef POLAR_BWPL
 #define POLAR_BWPL 1           // register stages below 5 read the left sibling's beta from one shuffled word
@@ -367,6 +374,10 @@ fsscs_decode_kernel(const DecodeParams P) {
     // working path's entry carries WFLAG in its jsm word
     constexpr bool NOSER = SORTED && !BIG && (POLAR_NOSER != 0);
     constexpr uint32_t WFLAG = 1u << 25;
+    // node-kind-specialised inserts and the full sum tree, per kernel as measured
+    constexpr bool R0F = SORTED && !HOT && (POLAR_R0_FAST == 2 || (POLAR_R0_FAST == 1 && !CNT && (NL == 10 || NL == 11)));
+    constexpr bool REPF = SORTED && !HOT && (POLAR_REP_FAST == 2 || (POLAR_REP_FAST == 1 && !CNT && NL == 10));
+    constexpr bool SUMF = (POLAR_SUM_FULL == 2 || (POLAR_SUM_FULL == 1 && !CNT && (NL == 10 || NL == 11)));
     using PK = Pk<BIG>;
     extern __shared__ __align__(16) uint32_t smem[];
     const int lane = threadIdx.x & 31;
@@ -1204,21 +1215,21 @@ fsscs_decode_kernel(const DecodeParams P) {
                 } else {
                     vn = negpart(xr);
                     vp = pospart(xr);
-#if POLAR_SUM_FULL
                     // lanes >= Lambda hold +0 and x + 0 = x exactly, so the full
                     // five-level tree equals the Lambda-element tree-order sum
+                    if constexpr (SUMF) {
 #pragma unroll
-                    for (int h = 16; h >= 1; h >>= 1) {
-                        vn += __shfl_down_sync(FULL, vn, h);
-                        if (rep) vp += __shfl_down_sync(FULL, vp, h);
+                        for (int h = 16; h >= 1; h >>= 1) {
+                            vn += __shfl_down_sync(FULL, vn, h);
+                            if (rep) vp += __shfl_down_sync(FULL, vp, h);
+                        }
+                    } else {
+                        #pragma unroll 1
+                        for (int h = Lam >> 1; h >= 1; h >>= 1) {
+                            vn += __shfl_down_sync(FULL, vn, h);
+                            if (rep) vp += __shfl_down_sync(FULL, vp, h);
+                        }
                     }
-#else
-                    #pragma unroll 1
-                    for (int h = Lam >> 1; h >= 1; h >>= 1) {
-                        vn += __shfl_down_sync(FULL, vn, h);
-                        if (rep) vp += __shfl_down_sync(FULL, vp, h);
-                    }
-#endif
                 }
                 vn = __shfl_sync(FULL, vn, 0);
                 vp = __shfl_sync(FULL, vp, 0);
@@ -1544,7 +1555,7 @@ fsscs_decode_kernel(const DecodeParams P) {
                     nS--;
                 }
                 if (nA == 0) cb = ~0ull;
-            } else if (SORTED && POLAR_R0_FAST && kind == OP_R0) {
+            } else if (R0F && kind == OP_R0) {
                 // one candidate (an R0 node), no sibling, no fork snapshot: the entries
                 // whose PM is not above the candidate's (a prefix 1..k of the sorted
                 // positions; ties keep the entry first, its serial is smaller) move
@@ -1571,7 +1582,7 @@ fsscs_decode_kernel(const DecodeParams P) {
                     if constexpr (!NOSER) s_ser[q] = (Pp < k) ? ns : ((Pp == k) ? ser0 : s_ser[q]);
                 }
                 nS++;
-            } else if (SORTED && POLAR_REP_FAST && kind == OP_REP) {
+            } else if (REPF && kind == OP_REP) {
                 // two warp-uniform candidates c0 <= c1 (a REP node: all zeros / all ones).
                 // k0, k1 = the entries not above c0, c1 (prefixes of the sorted
                 // positions 1..nS).  New position P takes: old P + 1 for P < k0, c0 at
