@@ -16,6 +16,7 @@
 namespace polar {
 cudaError_t launch_decode(const DecodeParams &p, int slots, bool snap_smem, bool chan_smem, int ctas, int smem,
                           cudaStream_t st);
+int specialised_nl(int n, int slots, bool snap_smem, bool chan_smem, bool recs_smem);
 cudaError_t decode_occupancy(int n, int slots, bool snap_smem, bool chan_smem, int mode, bool recs_smem, int smem,
                              int *blocks_per_sm);
 cudaError_t launch_decode_counts(const DecodeParams &p, int slots, int ctas, int smem, cudaStream_t st);
@@ -252,7 +253,12 @@ int polar_scs_create_ex(polar_scs_t *out, int32_t N, int32_t K, const uint8_t *f
     // shared scratch)
     // (only the specialised N = 2048 / 4096 kernels are built with the arena:
     // measured +10% on C4, +12% on C5; a run-time arena cost C2 5%)
-    const int gst_max = (t.M == 1 || !((t.n == 12 && slots == 4) || (t.n == 11 && slots == 2))) ? 0 : 2;
+    // (and only when that kernel is the one launched: a code whose per-depth
+    // records do not fit shared memory runs the general kernel, which has no arena —
+    // choosing arena stages for it overran the shared alpha area: found by the
+    // randomised sweep on N = 2048 random information sets with ~1000 nodes)
+    const int snl = specialised_nl(t.n, slots, false, false, sched_words > 0);
+    const int gst_max = (t.M == 1 || !(snl == 11 || snl == 12)) ? 0 : 2;
     for (int gst = 0; gst <= gst_max; gst++)
     for (int ci = 0; ci < 2; ci++) {
         const bool chan_smem = (ci == 0);

@@ -89,6 +89,17 @@ def test_random_stack_regressions(seed):
     test_random_stack_parity(seed)
 
 
+@pytest.mark.parametrize("seed", [30063, 30391, 40919, 41495])
+def test_random_stack_regressions_arena(seed):
+    """Seeds of the round-2 sweep (profiles/r2/pytest_random_sweep4_before_fix.log):
+    N = 2048, 32 < D <= 64, a random information set with ~1000 decision nodes.
+    Its per-depth records do not fit shared memory, so the general kernel runs,
+    but create() had moved the top alpha stages to the L2 arena only the
+    N = 2048 specialised kernel has: the shared alpha area was overrun (an
+    illegal address).  create() now takes arena stages only for that kernel."""
+    test_random_stack_parity(seed)
+
+
 @pytest.mark.skipif(not os.environ.get("POLAR_SLOW"), reason="slow oracle (minutes per case); POLAR_SLOW=1")
 @pytest.mark.parametrize("seed", [245, 396, 1361, 2086])
 def test_random_stack_regressions_visit_limit(seed):
