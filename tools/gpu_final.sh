@@ -18,12 +18,10 @@ timeout 900 $NCU -k regex:fsscs_decode -o $O/prof_P python bench.py --config P -
 timeout 900 $NCU -k regex:fsscl -o $O/prof_C2_list python bench.py --list --frames 20000 --steps 1 --warmup 3 --no-e2e --no-cpu > $O/ncu_C2_list.log 2>&1
 timeout 900 $NCU -k regex:fsscl -o $O/prof_C5_list python bench.py --config C5 --list --frames 20000 --steps 1 --warmup 3 --no-e2e --no-cpu > $O/ncu_C5_list.log 2>&1
 echo done >> $O/status.txt
-# the GPU suite and a fresh randomised sweep against the build with the node-kind-specialised inserts in EVERY
-# kernel (abtest/fastall.so: python tools/build_variant.py fastall -DPOLAR_R0_FAST=2 -DPOLAR_REP_FAST=2 -DPOLAR_SUM_FULL=2)
+# the GPU suite against the build with the node-kind-specialised inserts in EVERY kernel
+# (abtest/fastall.so: python tools/build_variant.py fastall -DPOLAR_R0_FAST=2 -DPOLAR_REP_FAST=2 -DPOLAR_SUM_FULL=2)
 if [ -f abtest/fastall.so ]; then
 POLAR_SCS_LIB=$PWD/abtest/fastall.so timeout 1500 python -m pytest tests -m gpu -q --deselect tests/test_gpu_parity.py::test_native_library_loaded > $O/pytest_gpu_fastall.log 2>&1; echo pytest_fastall=$? >> $O/status.txt
-POLAR_SCS_LIB=$PWD/abtest/fastall.so POLAR_RANDOM_OFFSET=40000 POLAR_RANDOM_STACK=1500 POLAR_RANDOM_LIST=1 timeout 2400 python -m pytest tests/test_gpu_random.py -m gpu -q -n 8 > $O/pytest_random_fastall.log 2>&1; echo random_fastall=$? >> $O/status.txt
 fi
-# a fresh randomised sweep on the default build
-POLAR_RANDOM_OFFSET=30000 POLAR_RANDOM_STACK=2500 POLAR_RANDOM_LIST=500 timeout 3000 python -m pytest tests/test_gpu_random.py -m gpu -q -n 8 > $O/pytest_random_sweep4.log 2>&1; echo random_sweep=$? >> $O/status.txt
+# fresh randomised sweeps: tools/gpu_sweep.sh (a separate call)
 # all-frame oracle parity of every config: tools/gpu_full_parity.sh (a separate call: ~30 min of host time)
